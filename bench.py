@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py -- device-side eBPF event throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): the per-SM / per-warp memory-access
+histogram policy P2 (ARRAY 9472 x u64 with a record-uniform ATOMIC ADD + a per-thread ARRAY of
+{cnt, bytes} updated by plain RMW) over 2^30 synthetic access events (32 GiB) per GPU.  A step is
+one gx_run_batch over the whole batch (every §8a row the config exercises: ingest, staging,
+interpretation, array / per-thread helpers, warp-aggregated atomics, epilogue); with N > 1 it
+also includes the NCCL snapshot-and-merge of the maps (weak scaling: 2^30 events per GPU).
+Inputs are generated on the device before timing and are larger than L2 (no flush needed).
+
+One JSON line on rank 0 (keys per the driver contract + roofline / cpu_baseline / e2e / clocks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "policy events/sec (device-timed)"
+EVENT_BYTES = 32
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--events", type=int, default=0, help="events per GPU (default: the config's size)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--extra", action="store_true", help="also time C1/C3/C4 single-GPU lines (stderr)")
+    return p.parse_args()
+
+
+DEFAULT_EVENTS = {"C1": 1 << 20, "C1d": 1 << 20, "C2": 1 << 30, "C3": 1 << 28, "C4": 1 << 31, "C5": 1 << 28}
+WORKLOAD = {
+    "C1": "counter policy P1 (13-insn ARRAY lookup + atomic add, 256 keys)",
+    "C1d": "counter policy P1d (8-insn direct-value ARRAY atomic add, 256 keys)",
+    "C2": "per-SM/per-warp access histogram P2 (ARRAY 9472 + per-thread ARRAY) over 2^30 access events",
+    "C3": "LLM page trace -> LFU hash (1M entries, FETCH-ADD) + ringbuf on threshold 64",
+    "C4": "vector-search stream, 12-iteration bounded binary search + hash/array/per-thread helpers",
+    "C5": "multi-tenant mix P1/P2/P3'/P4 via the attach table",
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(f) >= 7:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        busy = [float(s[0]) for s in self.samples if s[6].isdigit() and int(s[6]) > 50] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(busy)) if busy else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_rate(config, seed, n_total, budget_s=12.0):
+    """The CPU oracle (as it stands, one host core) on a bounded prefix sample of the workload.
+    Only interpretation is timed (SURVEY.md §8d CPU oracle timing)."""
+    from gxin import configs
+    from oracle.oracle import Oracle
+    env = Oracle()
+    s = configs.setup(env, config)
+    done, t_used, chunk, i0 = 0, 0.0, 1 << 16, 0
+    while t_used < budget_s and i0 < n_total:
+        n = min(chunk, n_total - i0)
+        ev = configs.events(config, seed, n, i0, n_total)
+        t0 = time.perf_counter()
+        env.run(ev, s.prog_arg, index_base=i0, want_r0=False)
+        t_used += time.perf_counter() - t0
+        done += n
+        i0 += n
+        chunk = min(chunk * 2, 1 << 20)
+    return done / t_used, done, t_used
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores, rank 0 only (the base contract's reference arm)."""
+    if rank != 0:
+        return
+    from gxin import configs
+    config = args.config
+    n_total = (args.events or DEFAULT_EVENTS[config]) * max(1, args.gpus)
+    seed = configs.SEEDS[config]
+    rates = []
+    for step in range(args.warmup + args.steps):
+        r, done, t = oracle_rate(config, seed, n_total, budget_s=6.0)
+        if step >= args.warmup:
+            rates.append((r, done, t))
+    value = float(np.median([r for r, _, _ in rates]))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median([t for _, _, t in rates]) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[config], "config": config, "events_per_gpu": n_total // max(1, args.gpus),
+                       "flush": "inputs larger than L2"},
+            "cpu_baseline": {"value": value, "unit": "events/s", "cores": 1, "kind": "oracle",
+                             "sample": f"prefix of {rates[0][1]} events per step of the {config} stream (seed {seed}), "
+                                       f"interpretation only, {cpu_model()}"},
+            "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    config = args.config
+    n = args.events or DEFAULT_EVENTS[config]
+    n_total = n * world
+    seed = configs.SEEDS[config]
+    stream = torch.cuda.current_stream()
+
+    rt = gx.Runtime(local)
+    s = configs.setup(rt, config)
+    events = gen_gpu.generate_device(config, seed, n, i0=rank * n, n_total=n_total, device=local)
+    torch.cuda.synchronize()
+
+    merger = None
+    if world > 1:
+        from paper_2512_12615_b200.dist import Merger
+        merger = Merger(rt, [fd for fd in s.fds.values()], dist.group.WORLD)
+
+    def step():
+        rt.run(events, s.prog_arg, stream=stream)
+        if merger is not None:
+            merger.merge()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = gx.gx_exec_info(rt.rt)["launches"]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_launch = []
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rt.run(events, s.prog_arg, stream=stream)
+            b.record(stream)
+            per_launch.append((a, b))
+            if merger is not None:
+                merger.merge()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in per_launch]))
+    launches = gx.gx_exec_info(rt.rt)["launches"] - launches0
+    value = n_total * args.steps / (t_ms / 1e3)
+    st = rt.stats()
+
+    peaks, peak_kind = measured_peaks()
+    alg_bytes = EVENT_BYTES * n
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (device-generated, seeded)",
+        "config": {"workload": WORKLOAD[config], "config": config, "events_per_gpu": n,
+                   "global_events": n_total, "flush": "inputs (32 B x events) larger than L2",
+                   "parallelism": f"dp{world}" if world > 1 else "dp1"},
+        "ns_per_event": t_ms * 1e6 / (n_total * args.steps) * world,
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                     "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
+                     "kernel": "gx_exec_kernel", "alg_bytes_per_launch": alg_bytes,
+                     "peak_kind": peak_kind, "kernel_ms": kernel_ms},
+        "stats": {k: int(v) // max(1, args.steps + args.warmup) for k, v in st.items()},
+        "clocks": clk.summary(),
+    }
+
+    # end-to-end through the public API from pinned host memory (H2D inside the timed region)
+    if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
+        try:
+            line["e2e"] = e2e_measure(rt, s, events, n, n_total, world, args)
+        except Exception as exc:  # pragma: no cover - box-dependent
+            line["e2e"] = {"value": None, "unit": "events/s", "error": str(exc)[:200]}
+    if rank == 0 and not args.no_cpu and world == 1:
+        r, done, t = oracle_rate(config, seed, n_total)
+        line["cpu_baseline"] = {"value": r, "unit": "events/s", "cores": 1, "kind": "oracle",
+                                "sample": f"prefix of {done} events of the {config} stream (seed {seed}) in "
+                                          f"{t:.1f} s, interpretation only; host has {host_cores()} cores, {cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.extra:
+            extra_lines(rt, args)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(rt, s, events, n, n_total, world, args):
+    """gx_run_batch_host over pinned host events: H2D of every step's events and D2H of the
+    step's result (the stats block) inside the timed region."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    avail = 0
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                avail = int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    ne = n
+    while ne * EVENT_BYTES * 1.5 * world > avail and ne > (1 << 24):
+        ne //= 2
+    host = torch.empty((ne, 32), dtype=torch.uint8, pin_memory=True)
+    host.copy_(events[:ne])
+    torch.cuda.synchronize()
+    gx.gx_run_batch_host(rt.rt, host, prog_fd=s.prog_arg)   # warm the pipeline
+    gx.gx_get_stats(rt.rt)
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        gx.gx_run_batch_host(rt.rt, host, prog_fd=s.prog_arg)
+        gx.gx_get_stats(rt.rt)   # D2H read of the step's result
+    dt = time.perf_counter() - t0
+    return {"value": ne * world * steps / dt, "unit": "events/s", "h2d_bytes_per_step": ne * EVENT_BYTES,
+            "d2h_bytes_per_step": 64, "events_per_step": ne,
+            "note": "gx_run_batch_host: chunked pinned H2D overlapped with execution"}
+
+
+def extra_lines(rt0, args):
+    """Single-GPU timings of the other configs (stderr; not the headline line)."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+    for config, n in (("C1", 1 << 20), ("C1", 1 << 26), ("C1d", 1 << 26), ("C3", 1 << 28), ("C4", 1 << 28), ("C5", 1 << 26)):
+        rt = gx.Runtime(0)
+        s = configs.setup(rt, config)
+        ev = gen_gpu.generate_device(config, configs.SEEDS[config], n)
+        for _ in range(3):
+            rt.run(ev, s.prog_arg)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            rt.run(ev, s.prog_arg)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 5
+        st = rt.stats()
+        print(json.dumps({"config": config, "events": n, "ms": ms, "events_per_s": n / ms * 1e3,
+                          "hbm_frac": n * 32 / (ms / 1e3) / 1e9 / measured_peaks()[0]["hbm_gbs"],
+                          "warp_steps_per_record": st["warp_steps"] / 8 / (n / 32),
+                          "divergent_frac": st["divergent_steps"] / max(1, st["warp_steps"])}), file=sys.stderr, flush=True)
+        del ev
+        rt.close()
+
+
+if __name__ == "__main__":
+    main()

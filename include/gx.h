@@ -1,0 +1,187 @@
+/*
+ * gx.h -- C ABI of the gx device-side eBPF runtime for B200 (sm_100a).
+ *
+ * The boundary of the data-parallel hot path of gpu_ext (arXiv 2512.12615): "a loader library
+ * that installs policies and configures eBPF maps" (§4.2 User-space Control
+ * Plane); device programs are "verified ... JIT-compiled ... [and run] at warp granularity"
+ * (§4.2), with a SIMT-aware verifier (§4.4.1; 310, §5.3) and
+ * maps "accessible from host-side driver hooks, GPU-side device policies, and user-space
+ * control planes" (§4.4.3).  The calls follow SURVEY.md §8(b).
+ *
+ * Conventions (all calls):
+ *   - Return 0 (or a non-negative handle) on success, a NEGATIVE errno on failure:
+ *       -EINVAL  malformed argument, bytecode or map spec
+ *       -EACCES  the verifier rejected the program (details in the report / log)
+ *       -E2BIG   program too large, complexity limit or budget exceeded, or a full map
+ *       -ENOMEM  device or host allocation failed
+ *       -EFAULT  a CUDA error; gx_last_error() has the text
+ *       -EPERM   running a program that has not passed gx_verify
+ *       -ENOENT  unknown handle
+ *     No C++ exception crosses this ABI.  gx_verify never raises: a rejection is a value.
+ *   - Handles (map fds, program fds) are small non-negative ints, as BPF_PSEUDO_MAP_FD expects
+ *     (bpf.h:1247-1266).  A program references a map by putting its fd in an ldimm64.
+ *   - Device buffers passed in (events, R0) are caller-owned CUDA device memory (e.g. torch
+ *     tensors) and must stay alive until the stream work completes (stream-ordered).
+ *   - Maps are runtime-owned device memory, freed by gx_close.  Host map reads/writes are
+ *     synchronous and ordered after all prior gx_run_batch calls on any stream of the runtime.
+ *   - One gx_rt per CUDA device.  A gx_rt is not thread-safe.
+ *
+ * Event record (the ctx every program sees in r1; read-only; 32 B, 32-B aligned):
+ *     0 u64 addr | 8 u64 ts | 16 u32 hook (bits 0-7 kind, 8-15 tenant, 16 is_write)
+ *     20 u32 block_id | 24 u16 sm_id | 26 u8 warp_id | 27 u8 lane_id | 28 u32 size
+ *   Uniformity tags ("compact warp-uniform context"; 310 BTF annotations):
+ *   addr and lane_id are LANE_VARYING, every other field is UNIFORM across the 32 events of
+ *   an aligned warp record.  Uniformity is a performance contract, never a correctness one.
+ */
+#ifndef GX_H
+#define GX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gx_rt gx_rt;
+
+/* map types: bpf.h:925-965 numbering; PERTHREAD_ARRAY takes PERCPU_ARRAY's slot */
+enum { GX_MAP_HASH = 1, GX_MAP_ARRAY = 2, GX_MAP_PERTHREAD_ARRAY = 6, GX_MAP_RINGBUF = 27 };
+/* hook kinds (event hook word bits 0-7): PAPER.md:225-230 (gdev_mem_ops.access), 260-262
+ * (gdev_sched_ops.enter), 303 (fault-style records) */
+enum { GX_HOOK_MEM_ACCESS = 0, GX_HOOK_BLOCK_ENTER = 1, GX_HOOK_FAULT = 2 };
+/* update flags, bpf.h:1300-1302 */
+enum { GX_ANY = 0, GX_NOEXIST = 1, GX_EXIST = 2 };
+
+typedef struct {
+    uint32_t type;         /* GX_MAP_* */
+    uint32_t key_size;     /* ARRAY/PERTHREAD: 4.  HASH: 4 or 8.  RINGBUF: 0 */
+    uint32_t value_size;   /* multiple of 8.  ARRAY <= 65536, PERTHREAD <= 256, HASH == 8. RINGBUF: 0 */
+    uint32_t max_entries;  /* > 0.  RINGBUF: byte capacity, a power of two >= 4096 */
+    uint32_t flags;        /* must be 0 */
+} gx_map_spec;
+
+typedef struct {
+    uint32_t simt_strict;      /* 1: enforce PAPER.md:282's SIMT rules (uniform branches, loop
+                                  bounds, map-update keys, atomics); 0 (default): relaxed, the
+                                  executor handles divergence at run time */
+    uint32_t max_insns;        /* worst-case executed instructions per event (0 -> 4096) */
+    uint32_t max_helpers;      /* worst-case weighted helper calls (lookup 1, update 2, other 1; 0 -> 64) */
+    uint32_t max_memops;       /* worst-case memory operations (0 -> 1024) */
+    uint32_t complexity_limit; /* verifier processed-instruction limit (0 -> 1000000) */
+} gx_verify_opts;
+
+/* verifier rule ids */
+enum {
+    GX_OK = 0, GX_BAD_INSN, GX_BAD_REG, GX_BAD_JUMP, GX_FALLTHROUGH, GX_UNREACHABLE, GX_UNINIT_READ,
+    GX_OOB_ACCESS, GX_NULL_DEREF, GX_MISALIGNED, GX_PTR_LEAK, GX_SHIFT_RANGE, GX_BAD_HELPER,
+    GX_FORBIDDEN_SYNC, GX_UNBOUNDED_LOOP, GX_COMPLEXITY, GX_BUDGET, GX_UNIFORM_BRANCH,
+    GX_UNIFORM_LOOP_BOUND, GX_UNIFORM_MAP_KEY, GX_NON_UNIFORM_ATOMIC, GX_MIXED_PTR, GX_NUM_RULES
+};
+
+typedef struct {
+    int32_t verdict;           /* 0 accepted, else -EACCES / -E2BIG / -EINVAL */
+    uint32_t n_violations;
+    uint32_t first_insn;       /* slot index of the first violation */
+    uint32_t first_rule;       /* GX_* rule id of the first violation */
+    uint64_t worst_insns;      /* worst case over explored paths */
+    uint64_t worst_helpers;
+    uint64_t worst_memops;
+    uint64_t processed_insns;  /* verifier work */
+    uint32_t stack_depth;      /* bytes, rounded up to 8 */
+    uint32_t all_uniform;      /* 1 if no conditional branch depends on a LANE_VARYING value */
+    uint32_t commutative;      /* 1 if shared maps change only through commutative updates */
+    uint32_t n_insns;
+} gx_verify_report;
+
+typedef struct {
+    uint64_t events_run;       /* events a program ran on */
+    uint64_t events_skipped;   /* no program attached for the event's (kind, tenant) */
+    uint64_t divergent_steps;  /* warp-steps executed on the min-PC divergent path */
+    uint64_t helper_errors;    /* helpers that returned a negative errno */
+    uint64_t ringbuf_bytes;    /* bytes committed to ring buffers */
+    uint64_t ringbuf_drops;    /* ringbuf_output calls dropped (-EAGAIN) */
+    uint64_t hash_full;        /* hash inserts refused because max_entries was reached */
+    uint64_t warp_steps;       /* interpreted warp-instructions (all paths) */
+} gx_batch_stats;
+
+/* ---------------------------------------------------------------- runtime */
+int  gx_open(int cuda_device, gx_rt **out);              /* -EFAULT if the device is not sm_100 */
+void gx_close(gx_rt *rt);
+const char *gx_last_error(gx_rt *rt);                   /* text of the last failure ("" if none) */
+
+/* ---------------------------------------------------------------- maps */
+/* Creates a zero-initialised map in device memory; *map_fd = its handle. */
+int  gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd);
+/* Host control-plane write of n (key, value) pairs, packed back to back (key_size / value_size
+ * bytes each, host memory), with bpf_map_update_elem semantics (bpf.h:1762-1776).  PERTHREAD:
+ * writes shard 0 and zeroes the other shards.  Synchronous.  Returns 0 or the first -errno. */
+int  gx_update_map(gx_rt *rt, int map_fd, const void *keys, const void *vals, uint64_t n, uint64_t flags);
+/* Canonical view into host buffers.  ARRAY / PERTHREAD (summed over shards):
+ * all max_entries values in key order (keys gets the u32 indices when non-NULL).  HASH: live
+ * entries sorted by key as an unsigned little-endian integer.  cap = capacity in entries;
+ * *n_out = entries written.  -E2BIG if cap is too small.  Synchronous. */
+int  gx_read_map(gx_rt *rt, int map_fd, void *keys, void *vals, uint64_t cap, uint64_t *n_out);
+/* Copies the committed ring-buffer bytes ([u32 len | u32 pg_off | payload padded to 8]*,
+ * bpf.h:6064-6066 layout) into buf and resets the buffer.  *n_bytes = bytes copied.  -E2BIG
+ * (nothing copied) if cap < committed bytes.  Synchronous. */
+int  gx_ringbuf_drain(gx_rt *rt, int map_fd, void *buf, uint64_t cap, uint64_t *n_bytes);
+
+/* ---------------------------------------------------------------- programs */
+/* Copies n_slots 8-byte struct bpf_insn slots (bpf.h:72-77); structural decode and map-fd
+ * relocation happen in gx_verify.  hook = the GX_HOOK_* kind the program is written for. */
+int  gx_load_prog(gx_rt *rt, uint32_t hook, const void *insn_slots, uint32_t n_slots, int *prog_fd);
+/* Runs the verifier and, on acceptance, pre-decodes the program for the
+ * executor.  opts may be NULL (defaults).  report and log may be NULL.  The log receives one
+ * line per violation "insn <i>: <RULE>: <message>".  Returns report->verdict. */
+int  gx_verify(gx_rt *rt, int prog_fd, const gx_verify_opts *opts, gx_verify_report *report,
+               char *log, uint64_t log_len);
+/* The same verifier without a runtime or device: maps[i] describes the map whose fd is i
+ * (type 0 = no such map; n_maps <= 64).  For tooling and CPU-side tests.  Returns
+ * report->verdict. */
+int  gx_verify_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *maps, uint32_t n_maps,
+                       const gx_verify_opts *opts, gx_verify_report *report, char *log, uint64_t log_len);
+/* Attach table entry (hook kind, tenant) -> program.  prog_fd = -1 detaches. */
+int  gx_attach(gx_rt *rt, int prog_fd, uint32_t hook_kind, uint32_t tenant);
+
+/* ---------------------------------------------------------------- execution (hot path) */
+/* Runs one batch: every event runs its program (prog_fd >= 0: that program for all events;
+ * -1: the attach table on the event's hook word) against the persistent maps (§8c c.1, S1, S2).
+ * d_events: n_events * 32 B of device memory, 32-B aligned.  d_ret: NULL or n_events u64 of
+ * device memory receiving R0 (0 for skipped events).  cuda_stream: a cudaStream_t (NULL = the
+ * legacy default stream).  Asynchronous (stream-ordered).  -EPERM if the program is unverified. */
+int  gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n_events, int prog_fd, uint64_t *d_ret,
+                  void *cuda_stream);
+/* Same, from HOST memory (pinned or pageable): the events are copied to the device in chunks
+ * on the runtime's own streams, overlapping copies with execution; h_ret (nullable) receives R0.
+ * Synchronous.  This is the end-to-end path bench.py times as "e2e". */
+int  gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n_events, int prog_fd, uint64_t *h_ret);
+/* Cumulative stats since the last call (then reset).  Synchronous. */
+int  gx_get_stats(gx_rt *rt, gx_batch_stats *out);
+/* Launch geometry of the executor: grid blocks, threads per block, dynamic shared bytes of the
+ * last launch, and the number of kernel launches issued since gx_open. */
+int  gx_exec_info(gx_rt *rt, uint32_t *grid, uint32_t *block, uint32_t *smem, uint64_t *launches);
+
+/* ---------------------------------------------------------------- multi-GPU merge (§8e, S3)
+ * Snapshot-and-merge across G replicas ("snapshot ... at GPU kernel
+ * completion boundaries").  Every rank created the same maps from the same initial state.
+ *   gx_merge_export: additive maps (ARRAY / PERTHREAD folded) -> d_delta[u64 words] =
+ *     local - base (mod 2^64), for the map's max_entries*value_size/8 words.
+ *   gx_merge_apply:  local = base + d_sum; base = local (d_sum = the allreduced deltas).
+ *   gx_hash_export:  live entries whose value differs from the base (or are new) ->
+ *     d_keys[u64] / d_vals[u64 delta] (device buffers, cap entries), *n_out entries.  Sync.
+ *   gx_hash_apply:   for each (key, delta): value = base_value (0 if absent) + delta, inserting
+ *     new keys; then base = value for every live entry.  -E2BIG if the union exceeds max_entries.
+ *   gx_merge_words:  number of u64 words gx_merge_export writes for this map.
+ * All device pointers are caller-owned; the calls are stream-ordered on cuda_stream except
+ * gx_hash_export (synchronous, it returns a count). */
+int  gx_merge_words(gx_rt *rt, int map_fd, uint64_t *words);
+int  gx_merge_export(gx_rt *rt, int map_fd, uint64_t *d_delta, void *cuda_stream);
+int  gx_merge_apply(gx_rt *rt, int map_fd, const uint64_t *d_sum, void *cuda_stream);
+int  gx_hash_export(gx_rt *rt, int map_fd, uint64_t *d_keys, uint64_t *d_vals, uint64_t cap, uint64_t *n_out);
+int  gx_hash_apply(gx_rt *rt, int map_fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n,
+                   void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GX_H */

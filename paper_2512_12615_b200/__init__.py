@@ -1,0 +1,353 @@
+"""Python binding of libgx.so (include/gx.h) -- argument marshalling only.
+
+Every function named gx_* here calls the C-ABI entry point of the same name; every step
+of the hot path runs in the library's sm_100a kernels.  There is no CPU fallback: if
+libgx.so is missing or no sm_100 device is present, the calls raise.
+
+PyTorch is used only for device memory and streams: event batches are torch.uint8 CUDA
+tensors of shape (N, 32), streams are torch.cuda streams.
+
+`Runtime` wraps one gx_rt with the engine methods gxin.configs.setup drives
+(create_map / update_map / load_prog / attach) plus run / read helpers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import errno
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgx.so")
+
+GX_MAP_HASH, GX_MAP_ARRAY, GX_MAP_PERTHREAD_ARRAY, GX_MAP_RINGBUF = 1, 2, 6, 27
+RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", "UNINIT_READ", "OOB_ACCESS",
+         "NULL_DEREF", "MISALIGNED", "PTR_LEAK", "SHIFT_RANGE", "BAD_HELPER", "FORBIDDEN_SYNC", "UNBOUNDED_LOOP",
+         "COMPLEXITY", "BUDGET", "UNIFORM_BRANCH", "UNIFORM_LOOP_BOUND", "UNIFORM_MAP_KEY", "NON_UNIFORM_ATOMIC",
+         "MIXED_PTR")
+EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_map", "gx_read_map",
+           "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_attach", "gx_run_batch", "gx_run_batch_host",
+           "gx_get_stats", "gx_exec_info", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
+           "gx_hash_export", "gx_hash_apply")
+
+
+class gx_map_spec(C.Structure):
+    _fields_ = [("type", C.c_uint32), ("key_size", C.c_uint32), ("value_size", C.c_uint32),
+                ("max_entries", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class gx_verify_opts(C.Structure):
+    _fields_ = [("simt_strict", C.c_uint32), ("max_insns", C.c_uint32), ("max_helpers", C.c_uint32),
+                ("max_memops", C.c_uint32), ("complexity_limit", C.c_uint32)]
+
+
+class gx_verify_report(C.Structure):
+    _fields_ = [("verdict", C.c_int32), ("n_violations", C.c_uint32), ("first_insn", C.c_uint32),
+                ("first_rule", C.c_uint32), ("worst_insns", C.c_uint64), ("worst_helpers", C.c_uint64),
+                ("worst_memops", C.c_uint64), ("processed_insns", C.c_uint64), ("stack_depth", C.c_uint32),
+                ("all_uniform", C.c_uint32), ("commutative", C.c_uint32), ("n_insns", C.c_uint32)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["rule"] = RULES[self.first_rule] if self.first_rule < len(RULES) else "?"
+        return d
+
+
+class gx_batch_stats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("events_run", "events_skipped", "divergent_steps", "helper_errors",
+                                          "ringbuf_bytes", "ringbuf_drops", "hash_full", "warp_steps")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Loads libgx.so; raises (no fallback) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2512_12615_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, u32, u64, p64 = C.c_void_p, C.c_int, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64)
+    sig = {
+        "gx_open": (i32, [i32, C.POINTER(vp)]),
+        "gx_close": (None, [vp]),
+        "gx_last_error": (C.c_char_p, [vp]),
+        "gx_create_map": (i32, [vp, C.POINTER(gx_map_spec), C.POINTER(i32)]),
+        "gx_update_map": (i32, [vp, i32, vp, vp, u64, u64]),
+        "gx_read_map": (i32, [vp, i32, vp, vp, u64, p64]),
+        "gx_ringbuf_drain": (i32, [vp, i32, vp, u64, p64]),
+        "gx_load_prog": (i32, [vp, u32, vp, u32, C.POINTER(i32)]),
+        "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
+        "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
+                                    C.c_char_p, u64]),
+        "gx_attach": (i32, [vp, i32, u32, u32]),
+        "gx_run_batch": (i32, [vp, vp, u64, i32, vp, vp]),
+        "gx_run_batch_host": (i32, [vp, vp, u64, i32, vp]),
+        "gx_get_stats": (i32, [vp, C.POINTER(gx_batch_stats)]),
+        "gx_exec_info": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), p64]),
+        "gx_merge_words": (i32, [vp, i32, p64]),
+        "gx_merge_export": (i32, [vp, i32, vp, vp]),
+        "gx_merge_apply": (i32, [vp, i32, vp, vp]),
+        "gx_hash_export": (i32, [vp, i32, vp, vp, u64, p64]),
+        "gx_hash_apply": (i32, [vp, i32, vp, vp, u64, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+class GxError(OSError):
+    pass
+
+
+def _check(rc, what, rt=None):
+    if rc < 0:
+        msg = lib().gx_last_error(rt).decode(errors="replace") if rt else ""
+        raise GxError(-rc, f"{what}: {errno.errorcode.get(-rc, -rc)} {msg}")
+    return rc
+
+
+# ---------------------------------------------------------------- same-name thin wrappers
+
+def gx_open(device: int = 0):
+    h = C.c_void_p()
+    _check(lib().gx_open(device, C.byref(h)), "gx_open (needs an sm_100 device)")
+    return h
+
+
+def gx_close(rt):
+    lib().gx_close(rt)
+
+
+def gx_create_map(rt, type, key_size, value_size, max_entries, flags=0) -> int:
+    fd = C.c_int()
+    spec = gx_map_spec(type, key_size, value_size, max_entries, flags)
+    _check(lib().gx_create_map(rt, C.byref(spec), C.byref(fd)), "gx_create_map", rt)
+    return fd.value
+
+
+def gx_update_map(rt, fd, keys: bytes, vals: bytes, n: int, flags=0) -> int:
+    return lib().gx_update_map(rt, fd, keys, vals, n, flags)
+
+
+def gx_load_prog(rt, hook: int, slots: bytes) -> int:
+    fd = C.c_int()
+    _check(lib().gx_load_prog(rt, hook, slots, len(slots) // 8, C.byref(fd)), "gx_load_prog", rt)
+    return fd.value
+
+
+def gx_verify(rt, prog_fd, strict=False, max_insns=0, max_helpers=0, max_memops=0, complexity_limit=0):
+    """Returns (verdict, report dict, log text).  Never raises on rejection."""
+    opts = gx_verify_opts(1 if strict else 0, max_insns, max_helpers, max_memops, complexity_limit)
+    rep = gx_verify_report()
+    log = C.create_string_buffer(1 << 16)
+    v = lib().gx_verify(rt, prog_fd, C.byref(opts), C.byref(rep), log, len(log))
+    return v, rep.as_dict(), log.value.decode(errors="replace")
+
+
+def gx_verify_offline(slots: bytes, maps: dict, strict=False, max_insns=0, max_helpers=0, max_memops=0,
+                      complexity_limit=0):
+    """Verifier without a device.  maps: {fd: (type, key_size, value_size, max_entries)}.
+    Returns (verdict, report dict, log text)."""
+    n = max(maps) + 1 if maps else 0
+    arr = (gx_map_spec * max(n, 1))()
+    for fd, (t, ks, vs, me) in maps.items():
+        arr[fd] = gx_map_spec(t, ks, vs, me, 0)
+    opts = gx_verify_opts(1 if strict else 0, max_insns, max_helpers, max_memops, complexity_limit)
+    rep = gx_verify_report()
+    log = C.create_string_buffer(1 << 16)
+    v = lib().gx_verify_offline(slots, len(slots) // 8, arr, n, C.byref(opts), C.byref(rep), log, len(log))
+    return v, rep.as_dict(), log.value.decode(errors="replace")
+
+
+def gx_attach(rt, prog_fd, kind, tenant):
+    _check(lib().gx_attach(rt, prog_fd, kind, tenant), "gx_attach", rt)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def gx_run_batch(rt, events, n=None, prog_fd=-1, ret=None, stream=None):
+    """events: torch.uint8 CUDA tensor (N, 32) (or a raw device pointer with n); ret: u64 tensor or None."""
+    if hasattr(events, "data_ptr"):
+        n = events.shape[0] if n is None else n
+        ptr = events.data_ptr()
+    else:
+        ptr = events
+    rptr = ret.data_ptr() if ret is not None else None
+    _check(lib().gx_run_batch(rt, ptr, n, prog_fd, rptr, _stream_handle(stream)), "gx_run_batch", rt)
+
+
+def gx_run_batch_host(rt, events: np.ndarray | int, n=None, prog_fd=-1, ret=None):
+    """events: host array (numpy / pinned torch tensor) of N x 32 B; ret: host u64 array or None."""
+    if hasattr(events, "data_ptr"):
+        n = events.shape[0] if n is None else n
+        ptr = events.data_ptr()
+    elif isinstance(events, np.ndarray):
+        n = len(events) if n is None else n
+        ptr = events.ctypes.data
+    else:
+        ptr = events
+    rptr = None
+    if ret is not None:
+        rptr = ret.data_ptr() if hasattr(ret, "data_ptr") else ret.ctypes.data
+    _check(lib().gx_run_batch_host(rt, ptr, n, prog_fd, rptr), "gx_run_batch_host", rt)
+
+
+def gx_get_stats(rt) -> dict:
+    s = gx_batch_stats()
+    _check(lib().gx_get_stats(rt, C.byref(s)), "gx_get_stats", rt)
+    return s.as_dict()
+
+
+def gx_exec_info(rt) -> dict:
+    g, b, s, n = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _check(lib().gx_exec_info(rt, C.byref(g), C.byref(b), C.byref(s), C.byref(n)), "gx_exec_info", rt)
+    return {"grid": g.value, "block": b.value, "smem": s.value, "launches": n.value}
+
+
+def gx_read_map(rt, fd, spec):
+    """Canonical content: ARRAY/PERTHREAD -> bytes (max_entries*value_size); HASH -> sorted (key, value) list."""
+    type_, ks, vs, me = spec
+    n = C.c_uint64()
+    if type_ == GX_MAP_HASH:
+        keys = C.create_string_buffer(ks * me + 8)
+        vals = C.create_string_buffer(vs * me + 8)
+        _check(lib().gx_read_map(rt, fd, keys, vals, me, C.byref(n)), "gx_read_map", rt)
+        return [(int.from_bytes(keys.raw[i * ks:(i + 1) * ks], "little"), vals.raw[i * vs:(i + 1) * vs])
+                for i in range(n.value)]
+    vals = C.create_string_buffer(vs * me)
+    _check(lib().gx_read_map(rt, fd, None, vals, me, C.byref(n)), "gx_read_map", rt)
+    return vals.raw
+
+
+def gx_ringbuf_drain(rt, fd) -> list[bytes]:
+    """Drains a ring buffer; returns the record payloads in buffer order."""
+    n = C.c_uint64()
+    rc = lib().gx_ringbuf_drain(rt, fd, None, 0, C.byref(n))
+    if rc < 0 and -rc != errno.E2BIG:
+        _check(rc, "gx_ringbuf_drain", rt)
+    buf = C.create_string_buffer(max(n.value, 1))
+    _check(lib().gx_ringbuf_drain(rt, fd, buf, n.value, C.byref(n)), "gx_ringbuf_drain", rt)
+    raw, out, o = buf.raw[: n.value], [], 0
+    while o + 8 <= len(raw):
+        ln = int.from_bytes(raw[o:o + 4], "little")
+        out.append(raw[o + 8:o + 8 + ln])
+        o += (8 + ln + 7) & ~7
+    return out
+
+
+def gx_merge_words(rt, fd) -> int:
+    w = C.c_uint64()
+    _check(lib().gx_merge_words(rt, fd, C.byref(w)), "gx_merge_words", rt)
+    return w.value
+
+
+def gx_merge_export(rt, fd, delta, stream=None):
+    _check(lib().gx_merge_export(rt, fd, delta.data_ptr(), _stream_handle(stream)), "gx_merge_export", rt)
+
+
+def gx_merge_apply(rt, fd, total, stream=None):
+    _check(lib().gx_merge_apply(rt, fd, total.data_ptr(), _stream_handle(stream)), "gx_merge_apply", rt)
+
+
+def gx_hash_export(rt, fd, keys, vals) -> int:
+    n = C.c_uint64()
+    _check(lib().gx_hash_export(rt, fd, keys.data_ptr(), vals.data_ptr(), keys.numel(), C.byref(n)),
+           "gx_hash_export", rt)
+    return n.value
+
+
+def gx_hash_apply(rt, fd, keys, vals, n, stream=None):
+    _check(lib().gx_hash_apply(rt, fd, keys.data_ptr() if n else None, vals.data_ptr() if n else None, n,
+                               _stream_handle(stream)), "gx_hash_apply", rt)
+
+
+# ---------------------------------------------------------------- engine object
+
+class Runtime:
+    """One gx_rt.  Engine interface for gxin.configs.setup plus run / read helpers."""
+
+    def __init__(self, device: int = 0, strict: bool = False):
+        self.rt = gx_open(device)
+        self.device = device
+        self.strict = strict
+        self.specs = {}
+        self.reports = {}
+
+    def close(self):
+        if self.rt:
+            gx_close(self.rt)
+            self.rt = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # engine interface
+    def create_map(self, type, key_size, value_size, max_entries) -> int:
+        fd = gx_create_map(self.rt, type, key_size, value_size, max_entries)
+        self.specs[fd] = (type, key_size, value_size, max_entries)
+        return fd
+
+    def update_map(self, fd, key: bytes, val: bytes, flags=0) -> int:
+        return gx_update_map(self.rt, fd, key, val, 1, flags)
+
+    def update_many(self, fd, keys: bytes, vals: bytes, n: int, flags=0) -> int:
+        return gx_update_map(self.rt, fd, keys, vals, n, flags)
+
+    def load_prog(self, slots: bytes, hook: int = 0) -> int:
+        """load + verify; raises GxError on rejection (the report is kept in .reports)."""
+        fd = gx_load_prog(self.rt, hook, slots)
+        v, rep, log = gx_verify(self.rt, fd, strict=self.strict)
+        self.reports[fd] = (v, rep, log)
+        if v != 0:
+            raise GxError(-v, f"verifier rejected program: {rep['rule']} at insn {rep['first_insn']}\n{log}")
+        return fd
+
+    def attach(self, prog, kind, tenant):
+        gx_attach(self.rt, prog, kind, tenant)
+
+    # execution
+    def run(self, events, prog=-1, ret=None, stream=None):
+        gx_run_batch(self.rt, events, prog_fd=prog, ret=ret, stream=stream)
+
+    def stats(self) -> dict:
+        return gx_get_stats(self.rt)
+
+    # reads
+    def dump(self, fd) -> bytes:
+        spec = self.specs[fd]
+        if spec[0] == GX_MAP_HASH:
+            return b"".join(k.to_bytes(spec[1], "little") + v for k, v in gx_read_map(self.rt, fd, spec))
+        return gx_read_map(self.rt, fd, spec)
+
+    def array_u64(self, fd) -> np.ndarray:
+        return np.frombuffer(self.dump(fd), dtype=np.uint64)
+
+    def hash_items(self, fd) -> dict:
+        return {k: np.frombuffer(v, dtype=np.uint64).copy() for k, v in gx_read_map(self.rt, fd, self.specs[fd])}
+
+    def ringbuf_records(self, fd) -> list[bytes]:
+        """Drains; returns the multiset as a sorted list of payloads."""
+        return sorted(gx_ringbuf_drain(self.rt, fd))
+
+
+def gx_last_error(rt) -> str:
+    return lib().gx_last_error(rt).decode(errors="replace")

@@ -1,0 +1,141 @@
+/*
+ * gx_device.cuh -- device-side map primitives shared by the executor (gx_exec.cu) and the map
+ * maintenance kernels (gx_maps.cu).  sm_100a only.
+ */
+#pragma once
+#include <stdint.h>
+
+#include "gx_internal.h"
+
+#define GX_FULL 0xFFFFFFFFu
+
+namespace gxd {
+
+enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_EXIST = 17, E_INVAL = 22 };
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p) {
+    uint64_t r;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+    uint64_t r;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+/* 128-bit compare-and-swap of a {key, value} hash slot (PTX atom.cas.b128, sm_90+): publishes
+ * key and value in one indivisible step so a reader that sees the key sees its value. */
+__device__ __forceinline__ void cas128(uint64_t *a, uint64_t cmp_lo, uint64_t cmp_hi, uint64_t new_lo,
+                                       uint64_t new_hi, uint64_t &old_lo, uint64_t &old_hi) {
+    asm volatile(
+        "{\n\t.reg .b128 d, b, c;\n\t"
+        "mov.b128 b, {%2, %3};\n\t"
+        "mov.b128 c, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], b, c;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(old_lo), "=l"(old_hi)
+        : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(a)
+        : "memory");
+}
+
+/* ---- HASH (open addressing, linear probing; slot = {u64 key, u64 value}; EMPTY key = all-ones;
+ * the all-ones key itself lives in a side slot at index cap whose key word is a present flag) */
+__device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key) {
+    uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
+    const uint64_t cap = (uint64_t)m.cap_mask + 1;
+    if (key == GX_HASH_EMPTY) {
+        uint64_t *side = slots + 2 * cap;
+        return ld_acquire(side) == 1 ? side + 1 : nullptr;
+    }
+    uint64_t h = mix64(key) & m.cap_mask;
+    for (uint64_t i = 0; i < cap; i++) {
+        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+        uint64_t k = ld_acquire(s);
+        if (k == key) return s + 1;
+        if (k == GX_HASH_EMPTY) return nullptr;
+    }
+    return nullptr;
+}
+
+/* bpf_map_update_elem on a HASH with 8-byte values (bpf.h:1762-1776).  Returns 0 or -errno;
+ * *full set when refused for capacity (hash_full). */
+__device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
+                                               bool &full) {
+    full = false;
+    if (flags > 2) return -E_INVAL;
+    uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
+    unsigned long long *count = reinterpret_cast<unsigned long long *>(m.aux);
+    const uint64_t cap = (uint64_t)m.cap_mask + 1;
+    if (key == GX_HASH_EMPTY) {
+        uint64_t *side = slots + 2 * cap;
+        if (ld_acquire(side) == 1) {
+            if (flags == 1) return -E_EXIST;
+            st_relaxed(side + 1, val);
+            return 0;
+        }
+        if (flags == 2) return -E_NOENT;
+        if (atomicAdd(count, 1ull) >= m.max_entries) {
+            atomicAdd(count, ~0ull);
+            full = true;
+            return -E_2BIG;
+        }
+        uint64_t ol, oh;
+        cas128(side, 0, 0, 1, val, ol, oh);
+        if (ol == 0) return 0;
+        atomicAdd(count, ~0ull);
+        if (flags == 1) return -E_EXIST;
+        st_relaxed(side + 1, val);
+        return 0;
+    }
+    uint64_t h = mix64(key) & m.cap_mask;
+    for (uint64_t i = 0; i < cap; i++) {
+        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+        uint64_t k = ld_acquire(s);
+        if (k == key) {
+            if (flags == 1) return -E_EXIST;
+            st_relaxed(s + 1, val);
+            return 0;
+        }
+        if (k != GX_HASH_EMPTY) continue;
+        if (flags == 2) return -E_NOENT;
+        if (atomicAdd(count, 1ull) >= m.max_entries) {
+            atomicAdd(count, ~0ull);
+            full = true;
+            return -E_2BIG;
+        }
+        uint64_t ol, oh;
+        cas128(s, GX_HASH_EMPTY, 0, key, val, ol, oh);
+        if (ol == GX_HASH_EMPTY) return 0;
+        atomicAdd(count, ~0ull); /* lost the slot */
+        if (ol == key) {
+            if (flags == 1) return -E_EXIST;
+            st_relaxed(s + 1, val);
+            return 0;
+        }
+    }
+    full = true;
+    return -E_2BIG;
+}
+
+/* ---- per-thread ARRAY: value pointers are LOGICAL addresses data + key*vs + off; the lane's
+ * word lives at data + ((logical - data)/8 * nshards + shard) * 8 ([key][word][shard] layout,
+ * so the 32 lanes of a warp touching one word are contiguous). */
+__device__ __forceinline__ uint8_t *pt_phys(const GxMapDesc &m, uint64_t logical, uint32_t shard) {
+    uint64_t lo = logical - m.data;
+    return reinterpret_cast<uint8_t *>(m.data) + ((lo >> 3) * m.nshards + shard) * 8 + (lo & 7);
+}
+
+}  // namespace gxd

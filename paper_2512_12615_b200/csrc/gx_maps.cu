@@ -1,0 +1,163 @@
+/*
+ * gx_maps.cu -- map maintenance kernels: per-thread fold, host control-plane writes, hash
+ * initialisation, and the snapshot-and-merge delta/apply kernels.
+ * Not on the per-event hot path; each is a simple grid-stride kernel.
+ */
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gx_device.cuh"
+#include "gx_internal.h"
+
+namespace {
+
+/* canonical per-thread value = SUM over shards of each u64 word (S4); one warp per word,
+ * coalesced over the [word][shard] layout */
+__global__ void pt_fold_kernel(const uint64_t *__restrict__ data, uint32_t nshards, uint64_t nwords,
+                               uint64_t *__restrict__ out) {
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t w = warp; w < nwords; w += nw) {
+        const uint64_t *row = data + w * nshards;
+        uint64_t s = 0;
+        for (uint32_t k = lane; k < nshards; k += 32) s += row[k];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(GX_FULL, s, o);
+        if (lane == 0) out[w] = s;
+    }
+}
+
+/* host write of per-thread key k: shard 0 = value, other shards = 0 */
+__global__ void pt_set_kernel(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)nw * nshards;
+         i += gridDim.x * (uint64_t)blockDim.x) {
+        const uint64_t w = i / nshards, s = i % nshards;
+        data[(word0 + w) * nshards + s] = s == 0 ? vals[w] : 0;
+    }
+}
+
+/* canonical per-thread content -> shard 0, zero the rest (after a merge) */
+__global__ void pt_store_canonical_kernel(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords * nshards;
+         i += gridDim.x * (uint64_t)blockDim.x) {
+        const uint64_t w = i / nshards, s = i % nshards;
+        data[i] = s == 0 ? vals[w] : 0;
+    }
+}
+
+__global__ void hash_init_kernel(uint64_t *slots, uint64_t cap) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
+         i += gridDim.x * (uint64_t)blockDim.x) {
+        slots[2 * i] = i < cap ? GX_HASH_EMPTY : 0; /* side slot: present flag 0 */
+        slots[2 * i + 1] = 0;
+    }
+}
+
+/* host control-plane updates, applied in order by one thread (bpf semantics per call) */
+__global__ void hash_host_update_kernel(GxMapDesc m, const uint64_t *keys, const uint64_t *vals, uint64_t n,
+                                        uint64_t flags, int64_t *rc, unsigned long long *full) {
+    if (blockIdx.x || threadIdx.x) return;
+    for (uint64_t i = 0; i < n; i++) {
+        bool f;
+        rc[i] = gxd::hash_update(m, keys[i], vals[i], flags, f);
+        if (f) atomicAdd(full, 1ull);
+    }
+}
+
+__global__ void sub_kernel(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
+        out[i] = a[i] - b[i];
+}
+__global__ void add_kernel(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
+        out[i] = a[i] + b[i];
+}
+
+/* hash delta export: entries whose value differs from the base copy, or that are new */
+__global__ void hash_export_kernel(GxMapDesc m, GxMapDesc base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
+                                   unsigned long long *count) {
+    const uint64_t *slots = reinterpret_cast<const uint64_t *>(m.data);
+    const uint64_t cap = (uint64_t)m.cap_mask + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
+         i += gridDim.x * (uint64_t)blockDim.x) {
+        uint64_t k = slots[2 * i], v = slots[2 * i + 1];
+        if (i < cap) {
+            if (k == GX_HASH_EMPTY) continue;
+        } else {
+            if (k != 1) continue;
+            k = GX_HASH_EMPTY;
+        }
+        const uint64_t *bv = gxd::hash_find(base, k);
+        const uint64_t d = v - (bv ? *bv : 0);
+        if (bv && d == 0) continue;
+        const unsigned long long o = atomicAdd(count, 1ull);
+        if (o < cap_out) {
+            keys[o] = k;
+            deltas[o] = d;
+        }
+    }
+}
+
+/* hash merge apply: value = base value (0 if absent) + summed delta; inserts new keys */
+__global__ void hash_apply_kernel(GxMapDesc m, GxMapDesc base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                                  unsigned long long *full) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x) {
+        const uint64_t *bv = gxd::hash_find(base, keys[i]);
+        const uint64_t v = (bv ? *bv : 0) + deltas[i];
+        bool f;
+        gxd::hash_update(m, keys[i], v, 0, f);
+        if (f) atomicAdd(full, 1ull);
+    }
+}
+
+inline uint32_t grid_for(uint64_t n, uint32_t block) {
+    uint64_t g = (n + block - 1) / block;
+    if (g > 148 * 8) g = 148 * 8;
+    return g ? (uint32_t)g : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint64_t nwords, uint64_t *out, cudaStream_t s) {
+    pt_fold_kernel<<<grid_for(nwords * 32, 256), 256, 0, s>>>(data, nshards, nwords, out);
+    return (int)cudaGetLastError();
+}
+int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals, cudaStream_t s) {
+    pt_set_kernel<<<grid_for((uint64_t)nw * nshards, 256), 256, 0, s>>>(data, nshards, word0, nw, vals);
+    return (int)cudaGetLastError();
+}
+int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals, cudaStream_t s) {
+    pt_store_canonical_kernel<<<grid_for(nwords * nshards, 256), 256, 0, s>>>(data, nshards, nwords, vals);
+    return (int)cudaGetLastError();
+}
+int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s) {
+    hash_init_kernel<<<grid_for(cap + 1, 256), 256, 0, s>>>(slots, cap);
+    return (int)cudaGetLastError();
+}
+int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t flags,
+                          int64_t *rc, unsigned long long *full, cudaStream_t s) {
+    hash_host_update_kernel<<<1, 1, 0, s>>>(*m, keys, vals, n, flags, rc, full);
+    return (int)cudaGetLastError();
+}
+int gx_k_sub(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s) {
+    sub_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, n);
+    return (int)cudaGetLastError();
+}
+int gx_k_add(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s) {
+    add_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, n);
+    return (int)cudaGetLastError();
+}
+int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
+                     unsigned long long *count, cudaStream_t s) {
+    hash_export_kernel<<<grid_for((uint64_t)m->cap_mask + 2, 256), 256, 0, s>>>(*m, *base, keys, deltas, cap_out, count);
+    return (int)cudaGetLastError();
+}
+int gx_k_hash_apply(const GxMapDesc *m, const GxMapDesc *base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                    unsigned long long *full, cudaStream_t s) {
+    hash_apply_kernel<<<grid_for(n, 256), 256, 0, s>>>(*m, *base, keys, deltas, n, full);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,801 @@
+/*
+ * gx_runtime.cpp -- implementation of the C ABI in include/gx.h (host side).
+ *
+ * Owns the per-device runtime: map memory and descriptors, loaded programs and their verified
+ * pre-decoded images, the attach table, launch descriptors, stats, and the chunked host->device
+ * pipeline of gx_run_batch_host.  Every device-side step is one of the kernels in gx_exec.cu /
+ * gx_maps.cu; nothing here computes on events.
+ */
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/gx.h"
+#include "gx_internal.h"
+#include "gx_verifier.h"
+
+extern "C" {
+int gx_launch_exec(const GxLaunch *d_launch, const void *d_events, uint64_t n, uint64_t *d_ret, uint32_t grid,
+                   uint32_t smem, cudaStream_t stream);
+int gx_exec_occupancy(uint32_t smem, int *blocks_per_sm);
+uint32_t gx_exec_block_threads();
+int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint64_t nwords, uint64_t *out, cudaStream_t s);
+int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals, cudaStream_t s);
+int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals, cudaStream_t s);
+int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s);
+int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t flags,
+                          int64_t *rc, unsigned long long *full, cudaStream_t s);
+int gx_k_sub(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s);
+int gx_k_add(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s);
+int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
+                     unsigned long long *count, cudaStream_t s);
+int gx_k_hash_apply(const GxMapDesc *m, const GxMapDesc *base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                    unsigned long long *full, cudaStream_t s);
+}
+
+namespace {
+
+constexpr uint32_t kBlocksPerSmMax = 4;        /* 4 x 256 threads = 1024 executor lanes per SM */
+constexpr uint32_t kPrivMaxBytes = 16 * 1024;  /* shared-memory privatisation budget per block */
+constexpr uint64_t kHostChunk = 1ull << 22;    /* events per chunk of gx_run_batch_host (128 MiB) */
+
+struct Map {
+    bool valid = false;
+    gx_map_spec spec{};
+    void *data = nullptr;   /* device */
+    void *aux = nullptr;    /* device counters */
+    uint64_t data_bytes = 0;
+    uint32_t nshards = 0;
+    uint64_t cap = 0;       /* HASH slots / RINGBUF bytes */
+    void *base = nullptr;   /* merge snapshot (ARRAY/PT canonical words, HASH slot copy) */
+    void *base_aux = nullptr;
+};
+
+struct Prog {
+    bool valid = false;
+    uint32_t hook = 0;
+    std::vector<uint8_t> slots;
+    bool verified = false;
+    GxVerifyResult vr;
+    GxInsn *d_image = nullptr;
+};
+
+struct LaunchKey {
+    int prog;
+    std::vector<int> attach_progs;
+    uint64_t version;
+    bool operator<(const LaunchKey &o) const {
+        if (prog != o.prog) return prog < o.prog;
+        if (version != o.version) return version < o.version;
+        return attach_progs < o.attach_progs;
+    }
+};
+
+struct LaunchCfg {
+    GxLaunch *d = nullptr;
+    uint32_t smem = 0;
+    uint32_t grid = 0;
+};
+
+}  // namespace
+
+struct gx_rt {
+    int dev = 0;
+    int nsm = 0;
+    uint32_t max_shards = 0;
+    Map maps[GX_MAX_MAPS];
+    Prog progs[GX_MAX_PROGS];
+    int attach[GX_MAX_KINDS][256];
+    uint64_t version = 1;               /* bumps whenever maps / programs / attach change */
+    std::map<LaunchKey, LaunchCfg> launches;
+    unsigned long long *d_stats = nullptr;
+    uint32_t last_grid = 0, last_block = 0, last_smem = 0;
+    uint64_t n_launches = 0;
+    std::string err;
+    /* gx_run_batch_host pipeline */
+    cudaStream_t s_copy = nullptr, s_exec = nullptr;
+    void *d_chunk[2] = {nullptr, nullptr};
+    uint64_t *d_rchunk[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copied[2], ev_done[2];
+    bool pipe_init = false;
+};
+
+namespace {
+
+int set_err(gx_rt *rt, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (rt) rt->err = buf;
+    return code;
+}
+
+int cuda_err(gx_rt *rt, cudaError_t e, const char *what) {
+    return set_err(rt, -EFAULT, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call, what)                                    \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_err(rt, _e, what); \
+    } while (0)
+
+GxMapDesc make_desc(const Map &m) {
+    GxMapDesc d{};
+    d.data = (uint64_t)m.data;
+    d.aux = (uint64_t)m.aux;
+    d.type = m.spec.type;
+    d.key_size = m.spec.key_size;
+    d.value_size = m.spec.value_size;
+    d.max_entries = m.spec.max_entries;
+    d.nshards = m.nshards;
+    d.cap_mask = (uint32_t)(m.cap ? m.cap - 1 : 0);
+    d.priv_off = 0xFFFFFFFFu;
+    d.coherent = 0;
+    return d;
+}
+
+GxMapDesc make_base_desc(const Map &m) {
+    GxMapDesc d = make_desc(m);
+    d.data = (uint64_t)m.base;
+    d.aux = (uint64_t)m.base_aux;
+    return d;
+}
+
+bool check_map(gx_rt *rt, int fd) { return rt && fd >= 0 && fd < GX_MAX_MAPS && rt->maps[fd].valid; }
+bool check_prog(gx_rt *rt, int fd) { return rt && fd >= 0 && fd < GX_MAX_PROGS && rt->progs[fd].valid; }
+
+uint32_t smem_bytes(uint32_t staged, uint32_t stack_slots, uint32_t priv_bytes) {
+    uint32_t per_warp = (GX_NREGS + 4 + stack_slots) * 32 * 8;
+    return staged * (uint32_t)sizeof(GxInsn) + GX_MAX_MAPS * (uint32_t)sizeof(GxMapDesc) + GX_MAX_KINDS * 256 +
+           priv_bytes + 64 + per_warp * (gx_exec_block_threads() / 32);
+}
+
+/* builds (or reuses) the device launch descriptor for one run configuration */
+int get_launch(gx_rt *rt, int prog_fd, LaunchCfg *&out) {
+    LaunchKey key;
+    key.prog = prog_fd;
+    key.version = rt->version;
+    std::vector<int> plist;
+    if (prog_fd >= 0) plist.push_back(prog_fd);
+    else {
+        for (int k = 0; k < GX_MAX_KINDS; k++)
+            for (int t = 0; t < 256; t++)
+                if (rt->attach[k][t] >= 0 && std::find(plist.begin(), plist.end(), rt->attach[k][t]) == plist.end())
+                    plist.push_back(rt->attach[k][t]);
+        key.attach_progs = plist;
+    }
+    auto it = rt->launches.find(key);
+    if (it != rt->launches.end()) {
+        out = &it->second;
+        return 0;
+    }
+    if (plist.size() > GX_MAX_LAUNCH_PROGS) return set_err(rt, -E2BIG, "more than %d programs in one launch", GX_MAX_LAUNCH_PROGS);
+    GxLaunch h;
+    memset(&h, 0, sizeof h);
+    memset(h.attach, -1, sizeof h.attach);
+    for (int i = 0; i < GX_MAX_MAPS; i++)
+        if (rt->maps[i].valid) h.maps[i] = make_desc(rt->maps[i]);
+    uint32_t staged = 0, stack = 8;
+    for (size_t q = 0; q < plist.size(); q++) {
+        Prog &p = rt->progs[plist[q]];
+        if (!p.verified) return set_err(rt, -EPERM, "program %d has not passed gx_verify", plist[q]);
+        h.progs[q].image = (uint64_t)p.d_image;
+        h.progs[q].n = (uint32_t)p.vr.image.size();
+        h.progs[q].smem_off = staged;
+        staged += h.progs[q].n;
+        stack = std::max(stack, p.vr.stack_depth);
+    }
+    if (staged > GX_MAX_STAGED_INSNS) return set_err(rt, -E2BIG, "launch stages %u instructions (max %d)", staged, GX_MAX_STAGED_INSNS);
+    h.n_progs = (uint32_t)plist.size();
+    h.single = prog_fd >= 0 ? 0 : -1;
+    if (prog_fd < 0)
+        for (int k = 0; k < GX_MAX_KINDS; k++)
+            for (int t = 0; t < 256; t++)
+                if (rt->attach[k][t] >= 0)
+                    h.attach[k][t] = (int8_t)(std::find(plist.begin(), plist.end(), rt->attach[k][t]) - plist.begin());
+    h.staged_insns = staged;
+    h.stack_slots = (stack + 7) / 8;
+    /* map facts across the launch: coherent (written by any program) and privatisable
+     * (write-only commutative ADD accumulator in every program that uses it: SURVEY.md §8c c.7) */
+    uint32_t priv = 0;
+    for (int m = 0; m < GX_MAX_MAPS; m++) {
+        if (!rt->maps[m].valid) continue;
+        bool written = false, accum = true, used = false;
+        for (int q : plist) {
+            const GxMapUse &u = rt->progs[q].vr.use[m];
+            if (!u.used) continue;
+            used = true;
+            written |= u.writes;
+            if (u.reads || u.non_add_write || u.fetch_add || u.update_call || u.non_dw_atomic) accum = false;
+        }
+        h.maps[m].coherent = written ? 1 : 0;
+        const Map &mm = rt->maps[m];
+        uint64_t bytes = (uint64_t)mm.spec.max_entries * mm.spec.value_size;
+        if (used && written && accum && mm.spec.type == GX_MAP_ARRAY && h.n_priv < 8 && priv + bytes <= kPrivMaxBytes) {
+            h.maps[m].priv_off = priv;
+            h.priv_maps[h.n_priv++] = m;
+            priv += (uint32_t)((bytes + 15) & ~15ull);
+        }
+    }
+    h.priv_bytes = priv;
+    h.stats = (uint64_t)rt->d_stats;
+    LaunchCfg cfg;
+    cfg.smem = smem_bytes(staged, h.stack_slots, priv);
+    if (cfg.smem > 227 * 1024) return set_err(rt, -E2BIG, "launch needs %u bytes of shared memory", cfg.smem);
+    int bps = 0;
+    int e = gx_exec_occupancy(cfg.smem, &bps);
+    if (e) return cuda_err(rt, (cudaError_t)e, "occupancy");
+    if (bps < 1) return set_err(rt, -E2BIG, "executor does not fit on an SM (%u B shared)", cfg.smem);
+    cfg.grid = (uint32_t)rt->nsm * (uint32_t)std::min<int>(bps, (int)kBlocksPerSmMax);
+    CK(cudaMalloc(&cfg.d, sizeof(GxLaunch)), "cudaMalloc launch");
+    CK(cudaMemcpy(cfg.d, &h, sizeof h, cudaMemcpyHostToDevice), "cudaMemcpy launch");
+    auto res = rt->launches.emplace(key, cfg);
+    out = &res.first->second;
+    return 0;
+}
+
+int sync(gx_rt *rt) {
+    CK(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gx_open(int cuda_device, gx_rt **out) {
+    if (!out) return -EINVAL;
+    *out = nullptr;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, cuda_device);
+    if (e != cudaSuccess) return -EFAULT;
+    if (prop.major != 10) return -EFAULT; /* sm_100a code only */
+    e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return -EFAULT;
+    gx_rt *rt = new gx_rt();
+    rt->dev = cuda_device;
+    rt->nsm = prop.multiProcessorCount;
+    rt->max_shards = (uint32_t)rt->nsm * kBlocksPerSmMax * gx_exec_block_threads();
+    for (auto &row : rt->attach)
+        for (int &x : row) x = -1;
+    if (cudaMalloc(&rt->d_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(rt->d_stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete rt;
+        return -ENOMEM;
+    }
+    *out = rt;
+    return 0;
+}
+
+void gx_close(gx_rt *rt) {
+    if (!rt) return;
+    cudaSetDevice(rt->dev);
+    cudaDeviceSynchronize();
+    for (auto &m : rt->maps) {
+        cudaFree(m.data);
+        cudaFree(m.aux);
+        cudaFree(m.base);
+        cudaFree(m.base_aux);
+    }
+    for (auto &p : rt->progs) cudaFree(p.d_image);
+    for (auto &kv : rt->launches) cudaFree(kv.second.d);
+    cudaFree(rt->d_stats);
+    if (rt->pipe_init) {
+        for (int b = 0; b < 2; b++) {
+            cudaFree(rt->d_chunk[b]);
+            cudaFree(rt->d_rchunk[b]);
+            cudaEventDestroy(rt->ev_copied[b]);
+            cudaEventDestroy(rt->ev_done[b]);
+        }
+        cudaStreamDestroy(rt->s_copy);
+        cudaStreamDestroy(rt->s_exec);
+    }
+    delete rt;
+}
+
+const char *gx_last_error(gx_rt *rt) { return rt ? rt->err.c_str() : "no runtime"; }
+
+int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
+    if (!rt || !spec || !map_fd) return -EINVAL;
+    const gx_map_spec s = *spec;
+    if (s.flags) return set_err(rt, -EINVAL, "map flags must be 0");
+    int fd = -1;
+    for (int i = 0; i < GX_MAX_MAPS; i++)
+        if (!rt->maps[i].valid) {
+            fd = i;
+            break;
+        }
+    if (fd < 0) return set_err(rt, -ENOMEM, "too many maps");
+    Map m;
+    m.spec = s;
+    switch (s.type) {
+    case GX_MAP_ARRAY:
+        if (s.key_size != 4 || !s.value_size || s.value_size % 8 || s.value_size > 65536 || !s.max_entries)
+            return set_err(rt, -EINVAL, "bad ARRAY spec");
+        m.data_bytes = (uint64_t)s.max_entries * s.value_size;
+        break;
+    case GX_MAP_PERTHREAD_ARRAY:
+        if (s.key_size != 4 || !s.value_size || s.value_size % 8 || s.value_size > 256 || !s.max_entries ||
+            (uint64_t)s.max_entries * s.value_size > 4096)
+            return set_err(rt, -EINVAL, "bad PERTHREAD_ARRAY spec (max_entries*value_size <= 4096)");
+        m.nshards = rt->max_shards;
+        m.data_bytes = (uint64_t)s.max_entries * s.value_size * m.nshards;
+        break;
+    case GX_MAP_HASH: {
+        if ((s.key_size != 4 && s.key_size != 8) || s.value_size != 8 || !s.max_entries)
+            return set_err(rt, -EINVAL, "bad HASH spec (key 4 or 8 bytes, value 8 bytes)");
+        uint64_t cap = 16;
+        while (cap < 2ull * s.max_entries) cap <<= 1;
+        m.cap = cap;
+        m.data_bytes = (cap + 1) * 16;
+        break;
+    }
+    case GX_MAP_RINGBUF:
+        if (s.key_size || s.value_size || s.max_entries < 4096 || (s.max_entries & (s.max_entries - 1)))
+            return set_err(rt, -EINVAL, "bad RINGBUF spec (byte capacity: power of two >= 4096)");
+        m.cap = s.max_entries;
+        m.data_bytes = s.max_entries;
+        break;
+    default:
+        return set_err(rt, -EINVAL, "unknown map type %u", s.type);
+    }
+    if (cudaMalloc(&m.data, m.data_bytes) != cudaSuccess) return set_err(rt, -ENOMEM, "cudaMalloc map %llu B", (unsigned long long)m.data_bytes);
+    cudaMalloc(&m.aux, 64);
+    cudaMemset(m.aux, 0, 64);
+    if (s.type == GX_MAP_HASH) {
+        int e = gx_k_hash_init((uint64_t *)m.data, m.cap, 0);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash init");
+    } else {
+        CK(cudaMemset(m.data, 0, m.data_bytes), "cudaMemset map");
+    }
+    CK(cudaDeviceSynchronize(), "map init");
+    m.valid = true;
+    rt->maps[fd] = m;
+    rt->version++;
+    *map_fd = fd;
+    return 0;
+}
+
+int gx_update_map(gx_rt *rt, int fd, const void *keys, const void *vals, uint64_t n, uint64_t flags) {
+    if (!check_map(rt, fd)) return -ENOENT;
+    if (n == 0) return 0;
+    if (!keys || !vals) return -EINVAL;
+    Map &m = rt->maps[fd];
+    const gx_map_spec &s = m.spec;
+    int rc0 = sync(rt);
+    if (rc0) return rc0;
+    const uint8_t *kb = (const uint8_t *)keys, *vb = (const uint8_t *)vals;
+    if (s.type == GX_MAP_RINGBUF) return set_err(rt, -EINVAL, "ring buffers have no keys");
+    if (flags > 2) return -EINVAL;
+    if (s.type == GX_MAP_ARRAY || s.type == GX_MAP_PERTHREAD_ARRAY) {
+        int first = 0;
+        std::vector<uint8_t> img;
+        bool whole = s.type == GX_MAP_ARRAY && n > 8;
+        if (whole) {
+            img.resize(m.data_bytes);
+            CK(cudaMemcpy(img.data(), m.data, m.data_bytes, cudaMemcpyDeviceToHost), "read array");
+        }
+        uint64_t *dv = nullptr;
+        if (s.type == GX_MAP_PERTHREAD_ARRAY) CK(cudaMalloc(&dv, s.value_size), "cudaMalloc");
+        for (uint64_t i = 0; i < n; i++) {
+            uint32_t k;
+            memcpy(&k, kb + 4 * i, 4);
+            int rc = 0;
+            if (k >= s.max_entries) rc = -E2BIG;
+            else if (flags == 1) rc = -EEXIST;
+            if (rc) {
+                if (!first) first = rc;
+                continue;
+            }
+            const uint8_t *v = vb + (uint64_t)s.value_size * i;
+            if (whole) memcpy(img.data() + (uint64_t)k * s.value_size, v, s.value_size);
+            else if (s.type == GX_MAP_ARRAY)
+                CK(cudaMemcpy((uint8_t *)m.data + (uint64_t)k * s.value_size, v, s.value_size, cudaMemcpyHostToDevice), "write array");
+            else {
+                CK(cudaMemcpy(dv, v, s.value_size, cudaMemcpyHostToDevice), "write pt");
+                int e = gx_k_pt_set((uint64_t *)m.data, m.nshards, (uint64_t)k * s.value_size / 8, s.value_size / 8, dv, 0);
+                if (e) return cuda_err(rt, (cudaError_t)e, "pt set");
+                CK(cudaDeviceSynchronize(), "pt set");
+            }
+        }
+        if (whole) CK(cudaMemcpy(m.data, img.data(), m.data_bytes, cudaMemcpyHostToDevice), "write array");
+        cudaFree(dv);
+        return first;
+    }
+    /* HASH */
+    std::vector<uint64_t> hk(n), hv(n);
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t k = 0;
+        memcpy(&k, kb + s.key_size * i, s.key_size);
+        hk[i] = k;
+        memcpy(&hv[i], vb + 8 * i, 8);
+    }
+    uint64_t *dk, *dvv;
+    int64_t *drc;
+    unsigned long long *dfull;
+    CK(cudaMalloc(&dk, 8 * n), "cudaMalloc");
+    CK(cudaMalloc(&dvv, 8 * n), "cudaMalloc");
+    CK(cudaMalloc(&drc, 8 * n), "cudaMalloc");
+    CK(cudaMalloc(&dfull, 8), "cudaMalloc");
+    cudaMemset(dfull, 0, 8);
+    cudaMemcpy(dk, hk.data(), 8 * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dvv, hv.data(), 8 * n, cudaMemcpyHostToDevice);
+    GxMapDesc d = make_desc(m);
+    int e = gx_k_hash_host_update(&d, dk, dvv, n, flags, drc, dfull, 0);
+    if (e) return cuda_err(rt, (cudaError_t)e, "hash update");
+    std::vector<int64_t> rc(n);
+    CK(cudaMemcpy(rc.data(), drc, 8 * n, cudaMemcpyDeviceToHost), "hash update rc");
+    cudaFree(dk);
+    cudaFree(dvv);
+    cudaFree(drc);
+    cudaFree(dfull);
+    for (auto r : rc)
+        if (r) return (int)r;
+    return 0;
+}
+
+int gx_read_map(gx_rt *rt, int fd, void *keys, void *vals, uint64_t cap, uint64_t *n_out) {
+    if (!check_map(rt, fd)) return -ENOENT;
+    if (!vals || !n_out) return -EINVAL;
+    Map &m = rt->maps[fd];
+    const gx_map_spec &s = m.spec;
+    int rc0 = sync(rt);
+    if (rc0) return rc0;
+    if (s.type == GX_MAP_ARRAY || s.type == GX_MAP_PERTHREAD_ARRAY) {
+        if (cap < s.max_entries) return -E2BIG;
+        uint64_t bytes = (uint64_t)s.max_entries * s.value_size;
+        if (s.type == GX_MAP_ARRAY) {
+            CK(cudaMemcpy(vals, m.data, bytes, cudaMemcpyDeviceToHost), "read array");
+        } else {
+            uint64_t *tmp;
+            CK(cudaMalloc(&tmp, bytes), "cudaMalloc");
+            int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, tmp, 0);
+            if (e) return cuda_err(rt, (cudaError_t)e, "pt fold");
+            CK(cudaMemcpy(vals, tmp, bytes, cudaMemcpyDeviceToHost), "read pt");
+            cudaFree(tmp);
+        }
+        if (keys)
+            for (uint32_t k = 0; k < s.max_entries; k++) memcpy((uint8_t *)keys + 4 * k, &k, 4);
+        *n_out = s.max_entries;
+        return 0;
+    }
+    if (s.type == GX_MAP_HASH) {
+        std::vector<uint64_t> slots(2 * (m.cap + 1));
+        CK(cudaMemcpy(slots.data(), m.data, m.data_bytes, cudaMemcpyDeviceToHost), "read hash");
+        std::vector<std::pair<uint64_t, uint64_t>> ent;
+        for (uint64_t i = 0; i < m.cap; i++)
+            if (slots[2 * i] != GX_HASH_EMPTY) ent.push_back({slots[2 * i], slots[2 * i + 1]});
+        if (slots[2 * m.cap] == 1) ent.push_back({GX_HASH_EMPTY, slots[2 * m.cap + 1]});
+        std::sort(ent.begin(), ent.end());
+        if (ent.size() > cap) return -E2BIG;
+        for (size_t i = 0; i < ent.size(); i++) {
+            if (keys) memcpy((uint8_t *)keys + s.key_size * i, &ent[i].first, s.key_size);
+            memcpy((uint8_t *)vals + 8 * i, &ent[i].second, 8);
+        }
+        *n_out = ent.size();
+        return 0;
+    }
+    return -EINVAL;
+}
+
+int gx_ringbuf_drain(gx_rt *rt, int fd, void *buf, uint64_t cap, uint64_t *n_bytes) {
+    if (!check_map(rt, fd)) return -ENOENT;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_RINGBUF || !n_bytes) return -EINVAL;
+    int rc0 = sync(rt);
+    if (rc0) return rc0;
+    uint64_t ctr[2];
+    CK(cudaMemcpy(ctr, m.aux, 16, cudaMemcpyDeviceToHost), "ringbuf counters");
+    uint64_t used = std::min<uint64_t>(ctr[1], m.cap);
+    if (used > cap || (used && !buf)) {
+        *n_bytes = used;
+        return -E2BIG;
+    }
+    if (used) CK(cudaMemcpy(buf, m.data, used, cudaMemcpyDeviceToHost), "ringbuf data");
+    CK(cudaMemset(m.aux, 0, 16), "ringbuf reset");
+    *n_bytes = used;
+    return 0;
+}
+
+int gx_load_prog(gx_rt *rt, uint32_t hook, const void *insn_slots, uint32_t n_slots, int *prog_fd) {
+    if (!rt || !insn_slots || !prog_fd || n_slots == 0) return -EINVAL;
+    if (n_slots > 4096) return set_err(rt, -E2BIG, "program has %u slots (max 4096)", n_slots);
+    int fd = -1;
+    for (int i = 0; i < GX_MAX_PROGS; i++)
+        if (!rt->progs[i].valid) {
+            fd = i;
+            break;
+        }
+    if (fd < 0) return set_err(rt, -ENOMEM, "too many programs");
+    Prog &p = rt->progs[fd];
+    p = Prog();
+    p.valid = true;
+    p.hook = hook;
+    p.slots.assign((const uint8_t *)insn_slots, (const uint8_t *)insn_slots + 8ull * n_slots);
+    *prog_fd = fd;
+    return 0;
+}
+
+int gx_verify(gx_rt *rt, int prog_fd, const gx_verify_opts *opts, gx_verify_report *report, char *log,
+              uint64_t log_len) {
+    if (!check_prog(rt, prog_fd)) return -ENOENT;
+    Prog &p = rt->progs[prog_fd];
+    GxMapInfo mi[GX_MAX_MAPS];
+    for (int i = 0; i < GX_MAX_MAPS; i++) {
+        const Map &m = rt->maps[i];
+        mi[i].valid = m.valid;
+        mi[i].type = m.spec.type;
+        mi[i].key_size = m.spec.key_size;
+        mi[i].value_size = m.spec.value_size;
+        mi[i].max_entries = m.spec.max_entries;
+    }
+    gx_verify_opts o{};
+    if (opts) o = *opts;
+    int v = gx_verify_program(p.slots.data(), (uint32_t)(p.slots.size() / 8), mi, o, p.vr);
+    if (report) *report = p.vr.report;
+    if (log && log_len) {
+        size_t k = std::min<size_t>(log_len - 1, p.vr.log.size());
+        memcpy(log, p.vr.log.data(), k);
+        log[k] = 0;
+    }
+    if (v != 0) {
+        p.verified = false;
+        rt->err = p.vr.log;
+        return v;
+    }
+    cudaFree(p.d_image);
+    p.d_image = nullptr;
+    CK(cudaMalloc(&p.d_image, p.vr.image.size() * sizeof(GxInsn)), "cudaMalloc image");
+    CK(cudaMemcpy(p.d_image, p.vr.image.data(), p.vr.image.size() * sizeof(GxInsn), cudaMemcpyHostToDevice), "upload image");
+    p.verified = true;
+    rt->version++;
+    return 0;
+}
+
+int gx_verify_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *maps, uint32_t n_maps,
+                      const gx_verify_opts *opts, gx_verify_report *report, char *log, uint64_t log_len) {
+    if (!insn_slots || n_maps > GX_MAX_MAPS || (n_maps && !maps)) return -EINVAL;
+    GxMapInfo mi[GX_MAX_MAPS];
+    for (uint32_t i = 0; i < n_maps; i++) {
+        mi[i].valid = maps[i].type != 0;
+        mi[i].type = maps[i].type;
+        mi[i].key_size = maps[i].key_size;
+        mi[i].value_size = maps[i].value_size;
+        mi[i].max_entries = maps[i].max_entries;
+    }
+    gx_verify_opts o{};
+    if (opts) o = *opts;
+    GxVerifyResult vr;
+    int v = gx_verify_program((const uint8_t *)insn_slots, n_slots, mi, o, vr);
+    if (report) *report = vr.report;
+    if (log && log_len) {
+        size_t k = std::min<size_t>(log_len - 1, vr.log.size());
+        memcpy(log, vr.log.data(), k);
+        log[k] = 0;
+    }
+    return v;
+}
+
+int gx_attach(gx_rt *rt, int prog_fd, uint32_t kind, uint32_t tenant) {
+    if (!rt || kind >= GX_MAX_KINDS || tenant > 255) return -EINVAL;
+    if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
+    rt->attach[kind][tenant] = prog_fd < 0 ? -1 : prog_fd;
+    rt->version++;
+    return 0;
+}
+
+int gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, uint64_t *d_ret, void *stream) {
+    if (!rt) return -EINVAL;
+    if (n == 0) return 0;
+    if (!d_events || ((uintptr_t)d_events & 31)) return set_err(rt, -EINVAL, "events must be 32-byte aligned device memory");
+    if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
+    LaunchCfg *cfg;
+    int rc = get_launch(rt, prog_fd, cfg);
+    if (rc) return rc;
+    int e = gx_launch_exec(cfg->d, d_events, n, d_ret, cfg->grid, cfg->smem, (cudaStream_t)stream);
+    if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");
+    rt->last_grid = cfg->grid;
+    rt->last_block = gx_exec_block_threads();
+    rt->last_smem = cfg->smem;
+    rt->n_launches++;
+    return 0;
+}
+
+int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, uint64_t *h_ret) {
+    if (!rt || (!h_events && n)) return -EINVAL;
+    if (n == 0) return 0;
+    if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
+    LaunchCfg *cfg;
+    int rc = get_launch(rt, prog_fd, cfg);
+    if (rc) return rc;
+    if (!rt->pipe_init) {
+        CK(cudaStreamCreateWithFlags(&rt->s_copy, cudaStreamNonBlocking), "stream");
+        CK(cudaStreamCreateWithFlags(&rt->s_exec, cudaStreamNonBlocking), "stream");
+        for (int b = 0; b < 2; b++) {
+            CK(cudaMalloc(&rt->d_chunk[b], kHostChunk * 32), "cudaMalloc chunk");
+            CK(cudaMalloc(&rt->d_rchunk[b], kHostChunk * 8), "cudaMalloc chunk");
+            CK(cudaEventCreateWithFlags(&rt->ev_copied[b], cudaEventDisableTiming), "event");
+            CK(cudaEventCreateWithFlags(&rt->ev_done[b], cudaEventDisableTiming), "event");
+            CK(cudaEventRecord(rt->ev_done[b], rt->s_exec), "event");
+        }
+        rt->pipe_init = true;
+    }
+    /* copies of chunk i+1 overlap the execution of chunk i; kernels stay serialised on s_exec
+     * (per-thread shards are not shared between concurrent launches) */
+    const uint8_t *src = (const uint8_t *)h_events;
+    uint64_t nchunks = (n + kHostChunk - 1) / kHostChunk;
+    for (uint64_t c = 0; c < nchunks; c++) {
+        int b = (int)(c & 1);
+        uint64_t i0 = c * kHostChunk, cnt = std::min(kHostChunk, n - i0);
+        CK(cudaStreamWaitEvent(rt->s_copy, rt->ev_done[b], 0), "wait");
+        CK(cudaMemcpyAsync(rt->d_chunk[b], src + 32 * i0, 32 * cnt, cudaMemcpyHostToDevice, rt->s_copy), "H2D");
+        CK(cudaEventRecord(rt->ev_copied[b], rt->s_copy), "record");
+        CK(cudaStreamWaitEvent(rt->s_exec, rt->ev_copied[b], 0), "wait");
+        int e = gx_launch_exec(cfg->d, rt->d_chunk[b], cnt, h_ret ? rt->d_rchunk[b] : nullptr, cfg->grid, cfg->smem, rt->s_exec);
+        if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");
+        rt->n_launches++;
+        if (h_ret) CK(cudaMemcpyAsync(h_ret + i0, rt->d_rchunk[b], 8 * cnt, cudaMemcpyDeviceToHost, rt->s_exec), "D2H");
+        CK(cudaEventRecord(rt->ev_done[b], rt->s_exec), "record");
+    }
+    CK(cudaStreamSynchronize(rt->s_exec), "sync");
+    rt->last_grid = cfg->grid;
+    rt->last_block = gx_exec_block_threads();
+    rt->last_smem = cfg->smem;
+    return 0;
+}
+
+int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
+    if (!rt || !out) return -EINVAL;
+    int rc0 = sync(rt);
+    if (rc0) return rc0;
+    unsigned long long h[8];
+    CK(cudaMemcpy(h, rt->d_stats, sizeof h, cudaMemcpyDeviceToHost), "stats");
+    CK(cudaMemset(rt->d_stats, 0, sizeof h), "stats reset");
+    out->events_run = h[GXS_RUN];
+    out->events_skipped = h[GXS_SKIP];
+    out->divergent_steps = h[GXS_DIVERGENT];
+    out->helper_errors = h[GXS_HERR];
+    out->ringbuf_bytes = h[GXS_RB_BYTES];
+    out->ringbuf_drops = h[GXS_RB_DROPS];
+    out->hash_full = h[GXS_HFULL];
+    out->warp_steps = h[GXS_STEPS];
+    return 0;
+}
+
+int gx_exec_info(gx_rt *rt, uint32_t *grid, uint32_t *block, uint32_t *smem, uint64_t *launches) {
+    if (!rt) return -EINVAL;
+    if (grid) *grid = rt->last_grid;
+    if (block) *block = rt->last_block;
+    if (smem) *smem = rt->last_smem;
+    if (launches) *launches = rt->n_launches;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ merge (S3) */
+
+int gx_merge_words(gx_rt *rt, int fd, uint64_t *words) {
+    if (!check_map(rt, fd) || !words) return -EINVAL;
+    const Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_ARRAY && m.spec.type != GX_MAP_PERTHREAD_ARRAY) return -EINVAL;
+    *words = (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+    return 0;
+}
+
+static int ensure_base(gx_rt *rt, Map &m) {
+    if (m.base) return 0;
+    if (m.spec.type == GX_MAP_HASH) {
+        CK(cudaMalloc(&m.base, m.data_bytes), "cudaMalloc base");
+        CK(cudaMalloc(&m.base_aux, 64), "cudaMalloc base");
+        CK(cudaMemcpy(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice), "base");
+        CK(cudaMemcpy(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice), "base");
+        return 0;
+    }
+    uint64_t bytes = (uint64_t)m.spec.max_entries * m.spec.value_size;
+    CK(cudaMalloc(&m.base, bytes), "cudaMalloc base");
+    if (m.spec.type == GX_MAP_ARRAY) CK(cudaMemcpy(m.base, m.data, bytes, cudaMemcpyDeviceToDevice), "base");
+    else {
+        int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, (uint64_t *)m.base, 0);
+        if (e) return cuda_err(rt, (cudaError_t)e, "base fold");
+    }
+    CK(cudaDeviceSynchronize(), "base");
+    return 0;
+}
+
+int gx_merge_export(gx_rt *rt, int fd, uint64_t *d_delta, void *stream) {
+    if (!check_map(rt, fd) || !d_delta) return -EINVAL;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_ARRAY && m.spec.type != GX_MAP_PERTHREAD_ARRAY) return -EINVAL;
+    int rc = ensure_base(rt, m);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t words = (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+    int e;
+    if (m.spec.type == GX_MAP_ARRAY) {
+        e = gx_k_sub((const uint64_t *)m.data, (const uint64_t *)m.base, d_delta, words, s);
+    } else {
+        e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, words, d_delta, s);
+        if (!e) e = gx_k_sub(d_delta, (const uint64_t *)m.base, d_delta, words, s);
+    }
+    if (e) return cuda_err(rt, (cudaError_t)e, "merge export");
+    return 0;
+}
+
+int gx_merge_apply(gx_rt *rt, int fd, const uint64_t *d_sum, void *stream) {
+    if (!check_map(rt, fd) || !d_sum) return -EINVAL;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_ARRAY && m.spec.type != GX_MAP_PERTHREAD_ARRAY) return -EINVAL;
+    int rc = ensure_base(rt, m);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t words = (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+    /* base = base + sum; local = base */
+    int e = gx_k_add((const uint64_t *)m.base, d_sum, (uint64_t *)m.base, words, s);
+    if (!e) {
+        if (m.spec.type == GX_MAP_ARRAY) {
+            cudaError_t ce = cudaMemcpyAsync(m.data, m.base, words * 8, cudaMemcpyDeviceToDevice, s);
+            if (ce != cudaSuccess) return cuda_err(rt, ce, "merge apply");
+        } else {
+            e = gx_k_pt_store_canonical((uint64_t *)m.data, m.nshards, words, (const uint64_t *)m.base, s);
+        }
+    }
+    if (e) return cuda_err(rt, (cudaError_t)e, "merge apply");
+    return 0;
+}
+
+int gx_hash_export(gx_rt *rt, int fd, uint64_t *d_keys, uint64_t *d_vals, uint64_t cap, uint64_t *n_out) {
+    if (!check_map(rt, fd) || !n_out) return -EINVAL;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_HASH) return -EINVAL;
+    int rc = ensure_base(rt, m);
+    if (rc) return rc;
+    unsigned long long *cnt;
+    CK(cudaMalloc(&cnt, 8), "cudaMalloc");
+    CK(cudaMemset(cnt, 0, 8), "memset");
+    GxMapDesc d = make_desc(m), b = make_base_desc(m);
+    int e = gx_k_hash_export(&d, &b, d_keys, d_vals, cap, cnt, 0);
+    if (e) return cuda_err(rt, (cudaError_t)e, "hash export");
+    unsigned long long h;
+    CK(cudaMemcpy(&h, cnt, 8, cudaMemcpyDeviceToHost), "hash export count");
+    cudaFree(cnt);
+    *n_out = h;
+    return h > cap ? -E2BIG : 0;
+}
+
+int gx_hash_apply(gx_rt *rt, int fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n, void *stream) {
+    if (!check_map(rt, fd)) return -EINVAL;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_HASH) return -EINVAL;
+    int rc = ensure_base(rt, m);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *full;
+    CK(cudaMalloc(&full, 8), "cudaMalloc");
+    CK(cudaMemset(full, 0, 8), "memset");
+    GxMapDesc d = make_desc(m), b = make_base_desc(m);
+    if (n) {
+        int e = gx_k_hash_apply(&d, &b, d_keys, d_vals, n, full, s);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash apply");
+    }
+    CK(cudaMemcpyAsync(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash base");
+    CK(cudaMemcpyAsync(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice, s), "hash base");
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, full, 8, cudaMemcpyDeviceToHost, s), "hash full");
+    CK(cudaStreamSynchronize(s), "sync");
+    cudaFree(full);
+    if (h) {
+        return set_err(rt, -E2BIG, "merged hash union exceeds max_entries (%llu refused)", h);
+    }
+    return 0;
+}
+
+}  // extern "C"

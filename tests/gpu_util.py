@@ -1,0 +1,49 @@
+"""Shared helpers for the GPU tests: run a config through the C-ABI library and through the
+oracle on the same seeded events, and collect the compared outputs."""
+from __future__ import annotations
+
+import numpy as np
+
+from gxin import configs
+
+RINGBUF = 27
+
+
+def outputs(engine, setup):
+    """Compared outputs: every map's canonical dump; ring buffers as sorted multisets."""
+    out = {}
+    for (tenant, name), fd in sorted(setup.fds.items()):
+        if engine.specs[fd][0] == RINGBUF:
+            out[(tenant, name)] = tuple(engine.ringbuf_records(fd))
+        else:
+            out[(tenant, name)] = engine.dump(fd)
+    return out
+
+
+def oracle_run(config, ev, threshold=None):
+    from oracle.oracle import Oracle
+    env = Oracle()
+    s = configs.setup(env, config, threshold=threshold)
+    r0 = env.run(ev, s.prog_arg)
+    return env, s, r0
+
+
+def gpu_run(config, ev, threshold=None, want_r0=True, runtime=None):
+    import torch
+
+    import paper_2512_12615_b200 as gx
+    rt = runtime or gx.Runtime(0)
+    s = configs.setup(rt, config, threshold=threshold)
+    d_ev = torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda()
+    ret = torch.zeros(len(ev), dtype=torch.int64, device="cuda") if want_r0 else None
+    rt.run(d_ev, s.prog_arg, ret=ret)
+    torch.cuda.synchronize()
+    r0 = ret.cpu().numpy().view(np.uint64) if want_r0 else None
+    return rt, s, r0
+
+
+def first_diff(a: bytes, b: bytes):
+    for i, (x, y) in enumerate(zip(a, b)):
+        if x != y:
+            return i
+    return min(len(a), len(b)) if len(a) != len(b) else -1

@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on the same seeded events (task rule ③; SURVEY.md §8c parity matrix).  Integer work: bit-exact.
+ORDER_INSENSITIVE configs only (c.3 S1): map dumps, ringbuf multisets, R0, stats."""
+import numpy as np
+import pytest
+
+from gxin import asm, configs, gen
+import closed_forms as cf
+from gpu_util import first_diff, gpu_run, oracle_run, outputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(config, ev, threshold=None, check_r0=True):
+    env, so, r0o = oracle_run(config, ev, threshold)
+    rt, sg, r0g = gpu_run(config, ev, threshold)
+    oo, og = outputs(env, so), outputs(rt, sg)
+    for key in oo:
+        a, b = oo[key], og[key]
+        if isinstance(a, tuple):
+            assert a == b, (config, key, "ringbuf multiset differs", len(a), len(b))
+        else:
+            assert a == b, (config, key, "first differing byte", first_diff(a, b))
+    if check_r0:
+        bad = np.nonzero(r0o != r0g)[0]
+        assert bad.size == 0, (config, "R0 differs at", bad[:8], r0o[bad[:8]], r0g[bad[:8]])
+    so_stats, sg_stats = env.stats(), rt.stats()
+    for k in ("events_run", "events_skipped", "ringbuf_drops", "hash_full"):
+        assert so_stats[k] == sg_stats[k], (config, k, so_stats[k], sg_stats[k])
+    return rt, sg, sg_stats
+
+
+@pytest.mark.parametrize("config,n", [("C1", 10 ** 6), ("C1", 1 << 20), ("C1d", 10 ** 6), ("C2", (1 << 18) + 13),
+                                      ("C3", (1 << 18) + 5), ("C4", (1 << 18) + 31), ("C5", (1 << 18) + 1)])
+def test_config_parity(gpu, config, n):
+    ev = configs.events(config, configs.SEEDS[config], n)
+    rt, s, st = _compare(config, ev)
+    if config == "C4":
+        assert st["divergent_steps"] > 0   # straddling records exercise the min-PC path
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 1000])
+@pytest.mark.parametrize("config", ["C1", "C3", "C5"])
+def test_ragged_tails(gpu, config, n):
+    ev = configs.events(config, configs.SEEDS[config], n)
+    _compare(config, ev, threshold=2 if config == "C3" else None)
+
+
+def test_c3_threshold_small(gpu):
+    """Threshold T=2 makes many FETCH-ADD crossings: ringbuf multiset must equal the oracle's."""
+    ev = configs.events("C3", 99, 1 << 16)
+    rt, s, st = _compare("C3", ev, threshold=2)
+    assert st["ringbuf_drops"] == 0
+
+
+def test_empty_batch(gpu):
+    import torch
+    import paper_2512_12615_b200 as gx
+    rt = gx.Runtime(0)
+    s = configs.setup(rt, "C1")
+    rt.run(torch.empty((0, 32), dtype=torch.uint8, device="cuda"), s.prog_arg)
+    assert int(rt.array_u64(s.fds[(0, "counts")]).sum()) == 0
+
+
+def test_fig2_pin_gpu(gpu):
+    sm = np.concatenate([np.full(382, 15), np.full(3, 6)]).astype(np.uint16)
+    ev = gen.records(len(sm), sm_id=sm, warp_id=(np.arange(len(sm)) % 64).astype(np.uint8), size=4)
+    rt, s, _ = gpu_run("C2", ev)
+    hist = rt.array_u64(s.fds[(0, "hist")]).reshape(148, 64).sum(axis=1)
+    assert int(hist[15]) == 382 and int(hist[6]) == 3
+
+
+def test_device_generator(gpu):
+    """The CUDA generator reproduces gxin.gen byte for byte (any shard offset)."""
+    from gxin import gen_gpu
+    for config in gen.CONFIGS:
+        n_total = 1 << 20
+        for i0, n in ((0, 4096), (1 << 19, 4099), (n_total - 777, 777)):
+            want = gen.generate(config, 1234, n, i0, n_total)
+            got = gen_gpu.generate_device(config, 1234, n, i0, n_total).cpu().numpy()
+            assert got.tobytes() == want.tobytes(), (config, i0)
+
+
+PRE = "ldxdw r0, [r1+0]\nldxdw r2, [r1+8]\n"
+
+
+@pytest.mark.parametrize("W", [64, 32])
+def test_isa_parity_alu_jmp(gpu, W):
+    """Every ALU / JMP op over the edge grid: GPU R0 == oracle R0 (and == closed form)."""
+    import itertools
+    import torch
+    import paper_2512_12615_b200 as gx
+    from oracle.oracle import Oracle
+    grid = cf.edge_grid(20)
+    pairs = list(itertools.product(grid, grid))
+    ev = gen.records(len(pairs), addr=np.array([p[0] for p in pairs], dtype=np.uint64),
+                     ts=np.array([p[1] for p in pairs], dtype=np.uint64))
+    d_ev = torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda()
+    rt = gx.Runtime(0)
+    texts = []
+    for name in cf.ALU_NAMES:
+        if name == "movsx32" and W == 32:
+            continue
+        texts.append(f"{name}{W} r0" if name == "neg" else f"{name}{W} r0, r2")
+    sfx = "32" if W == 32 else ""
+    for name in cf.JMP_NAMES:
+        texts.append(f"mov64 r3, r0\nmov64 r0, 0\n{name}{sfx} r3, r2, +1\nja +1\nmov64 r0, 1")
+    for w in (16, 32, 64):
+        texts += [f"le{w} r0", f"be{w} r0", f"bswap{w} r0"]
+    for body in texts:
+        prog = asm.assemble(PRE + body + "\nexit")
+        env = Oracle()
+        want = env.run(ev, env.load_prog(prog))
+        fd = rt.load_prog(prog)
+        ret = torch.zeros(len(ev), dtype=torch.int64, device="cuda")
+        rt.run(d_ev, fd, ret=ret)
+        got = ret.cpu().numpy().view(np.uint64)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (body, [(hex(pairs[i][0]), hex(pairs[i][1]), hex(int(got[i])), hex(int(want[i]))) for i in bad[:4]])
+
+
+def test_micro_pins_gpu(gpu):
+    """The hand-computed micro-pins (tests/golden/micro_pins.txt) on the GPU."""
+    import os
+    import torch
+    import paper_2512_12615_b200 as gx
+    rt = gx.Runtime(0)
+    path = os.path.join(os.path.dirname(__file__), "golden", "micro_pins.txt")
+    for line in open(path):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, ops, d, s, want = [x.strip() for x in line.split("|")]
+        ev = gen.records(32, addr=int(d, 0), ts=int(s, 0))
+        fd = rt.load_prog(asm.assemble(PRE + ops.replace(" / ", "\n") + "\nexit"))
+        ret = torch.zeros(32, dtype=torch.int64, device="cuda")
+        rt.run(torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda(), fd, ret=ret)
+        got = ret.cpu().numpy().view(np.uint64)
+        assert (got == np.uint64(int(want, 0))).all(), (name, hex(int(got[0])))
+
+
+def test_unverified_program_refused(gpu):
+    import torch
+    import paper_2512_12615_b200 as gx
+    rt = gx.Runtime(0)
+    fd = gx.gx_load_prog(rt.rt, 0, asm.assemble("mov64 r0, 0\nexit"))
+    with pytest.raises(gx.GxError):
+        rt.run(torch.zeros((32, 32), dtype=torch.uint8, device="cuda"), fd)
+
+
+def test_run_batch_host_parity(gpu):
+    """gx_run_batch_host (chunked H2D pipeline) gives the oracle's result too."""
+    import paper_2512_12615_b200 as gx
+    ev = configs.events("C2", 7, (1 << 18) + 3)
+    env, so, r0o = oracle_run("C2", ev)
+    rt = gx.Runtime(0)
+    s = configs.setup(rt, "C2")
+    r0 = np.zeros(len(ev), dtype=np.uint64)
+    gx.gx_run_batch_host(rt.rt, ev, prog_fd=s.prog_arg, ret=r0)
+    assert outputs(rt, s) == outputs(env, so)
+    assert (r0 == r0o).all()
