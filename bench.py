@@ -325,7 +325,7 @@ def extra_lines(rt0, args):
     import torch
     import paper_2512_12615_b200 as gx
     from gxin import configs, gen_gpu
-    for config, n in (("C1", 1 << 20), ("C1", 1 << 26), ("C1d", 1 << 26), ("C3", 1 << 28), ("C4", 1 << 28), ("C5", 1 << 26)):
+    for config, n in (("C1", 1 << 20), ("C1", 1 << 26), ("C3", 1 << 28), ("C4", 1 << 28), ("C5", 1 << 26)):
         rt = gx.Runtime(0)
         s = configs.setup(rt, config)
         ev = gen_gpu.generate_device(config, configs.SEEDS[config], n)

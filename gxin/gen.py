@@ -108,13 +108,15 @@ def tenant_table():
 
 @functools.lru_cache(maxsize=None)
 def c4_bounds():
-    """bounds[4097]: bounds[0] = 2 MiB (end of centroids); Pareto(1.5) list sizes in 512-B vectors."""
+    """bounds[4097]: bounds[0] = 2 MiB (end of the centroids); list sizes are heavy-tailed
+    (Pareto alpha 1.2, >= 256 vectors) counts of 128-B vectors (uint8 SIFT, 128 dims), so list
+    boundaries are not 512-B aligned and the 512-B warp records that cross them diverge."""
     u = rnd(LAYOUT_SEED, 20, np.arange(NLISTS)).astype(np.float64) / 2.0 ** 64
-    vec = np.floor(8192.0 / np.power(1.0 - u, 1.0 / 1.5))
-    vec = np.clip(vec, 1, 1 << 20).astype(np.uint64)
+    vec = np.floor(256.0 / np.power(1.0 - u, 1.0 / 1.2))
+    vec = np.clip(vec, 1, 1 << 22).astype(np.uint64)
     b = np.zeros(NLISTS + 1, dtype=np.uint64)
     b[0] = CENTROID_BYTES
-    b[1:] = np.uint64(CENTROID_BYTES) + np.cumsum(vec * np.uint64(512))
+    b[1:] = np.uint64(CENTROID_BYTES) + np.cumsum(vec * np.uint64(128))
     return b
 
 

@@ -167,19 +167,26 @@ int  gx_exec_info(gx_rt *rt, uint32_t *grid, uint32_t *block, uint32_t *smem, ui
  *   gx_merge_export: additive maps (ARRAY / PERTHREAD folded) -> d_delta[u64 words] =
  *     local - base (mod 2^64), for the map's max_entries*value_size/8 words.
  *   gx_merge_apply:  local = base + d_sum; base = local (d_sum = the allreduced deltas).
- *   gx_hash_export:  live entries whose value differs from the base (or are new) ->
- *     d_keys[u64] / d_vals[u64 delta] (device buffers, cap entries), *n_out entries.  Sync.
- *   gx_hash_apply:   for each (key, delta): value = base_value (0 if absent) + delta, inserting
- *     new keys; then base = value for every live entry.  -E2BIG if the union exceeds max_entries.
+ *   gx_hash_export:  entries whose value differs from the base (or that are new), as
+ *     (key, value - base value) pairs, grouped by owner rank g = mix64(key) mod nranks into
+ *     d_keys / d_vals (device, cap entries); h_counts[g] (host, nranks entries) = pairs of owner g,
+ *     stored in owner order.  owner >= 0 keeps only the keys that rank owns.  Synchronous.
+ *   gx_hash_apply:   GX_MERGE_RESTORE: local := base first; then, for every (key, delta):
+ *     value += delta (absent keys are inserted at 0 first; duplicate keys accumulate);
+ *     GX_MERGE_COMMIT: afterwards base := local.  -E2BIG if the union exceeds max_entries.
  *   gx_merge_words:  number of u64 words gx_merge_export writes for this map.
- * All device pointers are caller-owned; the calls are stream-ordered on cuda_stream except
- * gx_hash_export (synchronous, it returns a count). */
+ * The key-sharded hash merge is: export grouped by owner -> all-to-all ->
+ * apply(RESTORE) on the owner -> export(owner = self) -> all-gather -> apply(RESTORE|COMMIT).
+ * All device pointers are caller-owned; merge_export / merge_apply / hash_apply are stream-ordered
+ * on cuda_stream (hash_apply synchronises before returning). */
+enum { GX_MERGE_RESTORE = 1, GX_MERGE_COMMIT = 2 };
 int  gx_merge_words(gx_rt *rt, int map_fd, uint64_t *words);
 int  gx_merge_export(gx_rt *rt, int map_fd, uint64_t *d_delta, void *cuda_stream);
 int  gx_merge_apply(gx_rt *rt, int map_fd, const uint64_t *d_sum, void *cuda_stream);
-int  gx_hash_export(gx_rt *rt, int map_fd, uint64_t *d_keys, uint64_t *d_vals, uint64_t cap, uint64_t *n_out);
+int  gx_hash_export(gx_rt *rt, int map_fd, uint32_t nranks, int32_t owner, uint64_t *d_keys, uint64_t *d_vals,
+                    uint64_t cap, uint64_t *h_counts);
 int  gx_hash_apply(gx_rt *rt, int map_fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n,
-                   void *cuda_stream);
+                   uint32_t flags, void *cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -95,8 +95,8 @@ def lib():
         "gx_merge_words": (i32, [vp, i32, p64]),
         "gx_merge_export": (i32, [vp, i32, vp, vp]),
         "gx_merge_apply": (i32, [vp, i32, vp, vp]),
-        "gx_hash_export": (i32, [vp, i32, vp, vp, u64, p64]),
-        "gx_hash_apply": (i32, [vp, i32, vp, vp, u64, vp]),
+        "gx_hash_export": (i32, [vp, i32, u32, C.c_int32, vp, vp, u64, p64]),
+        "gx_hash_apply": (i32, [vp, i32, vp, vp, u64, u32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -265,15 +265,19 @@ def gx_merge_apply(rt, fd, total, stream=None):
     _check(lib().gx_merge_apply(rt, fd, total.data_ptr(), _stream_handle(stream)), "gx_merge_apply", rt)
 
 
-def gx_hash_export(rt, fd, keys, vals) -> int:
-    n = C.c_uint64()
-    _check(lib().gx_hash_export(rt, fd, keys.data_ptr(), vals.data_ptr(), keys.numel(), C.byref(n)),
+def gx_hash_export(rt, fd, keys, vals, nranks=1, owner=-1):
+    """Fills keys/vals (u64 device tensors) grouped by owner; returns the per-owner counts."""
+    counts = (C.c_uint64 * nranks)()
+    _check(lib().gx_hash_export(rt, fd, nranks, owner, keys.data_ptr(), vals.data_ptr(), keys.numel(), counts),
            "gx_hash_export", rt)
-    return n.value
+    return list(counts)
 
 
-def gx_hash_apply(rt, fd, keys, vals, n, stream=None):
-    _check(lib().gx_hash_apply(rt, fd, keys.data_ptr() if n else None, vals.data_ptr() if n else None, n,
+GX_MERGE_RESTORE, GX_MERGE_COMMIT = 1, 2
+
+
+def gx_hash_apply(rt, fd, keys, vals, n, flags=GX_MERGE_RESTORE | GX_MERGE_COMMIT, stream=None):
+    _check(lib().gx_hash_apply(rt, fd, keys.data_ptr() if n else None, vals.data_ptr() if n else None, n, flags,
                                _stream_handle(stream)), "gx_hash_apply", rt)
 
 

@@ -71,63 +71,61 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
 }
 
 /* bpf_map_update_elem on a HASH with 8-byte values (bpf.h:1762-1776).  Returns 0 or -errno;
- * *full set when refused for capacity (hash_full). */
+ * *full set when refused for capacity (hash_full).
+ * Capacity (max_entries): aux[1] counts committed entries.  An insert is refused when the committed
+ * count has reached max_entries; inserts of DISTINCT keys racing at that boundary can each pass the
+ * check, so up to (concurrent inserters - 1) entries beyond max_entries may be admitted (the slot
+ * array holds 2 x max_entries, reading I-22).  Nothing ever spins on other lanes. */
 __device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
                                                bool &full) {
     full = false;
     if (flags > 2) return -E_INVAL;
     uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
-    unsigned long long *count = reinterpret_cast<unsigned long long *>(m.aux);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(m.aux);
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    if (key == GX_HASH_EMPTY) {
-        uint64_t *side = slots + 2 * cap;
-        if (ld_acquire(side) == 1) {
-            if (flags == 1) return -E_EXIST;
-            st_relaxed(side + 1, val);
-            return 0;
+    for (;;) {
+        uint64_t *s = nullptr;
+        bool present = false;
+        if (key == GX_HASH_EMPTY) {
+            s = slots + 2 * cap;
+            present = ld_acquire(s) == 1;
+        } else {
+            const uint64_t h = mix64(key) & m.cap_mask;
+            uint64_t i = 0;
+            for (; i < cap; i++) {
+                s = slots + 2 * ((h + i) & m.cap_mask);
+                const uint64_t k = ld_acquire(s);
+                if (k == key) {
+                    present = true;
+                    break;
+                }
+                if (k == GX_HASH_EMPTY) break;
+            }
+            if (i == cap) {
+                full = true;
+                return -E_2BIG;
+            }
         }
-        if (flags == 2) return -E_NOENT;
-        if (atomicAdd(count, 1ull) >= m.max_entries) {
-            atomicAdd(count, ~0ull);
-            full = true;
-            return -E_2BIG;
-        }
-        uint64_t ol, oh;
-        cas128(side, 0, 0, 1, val, ol, oh);
-        if (ol == 0) return 0;
-        atomicAdd(count, ~0ull);
-        if (flags == 1) return -E_EXIST;
-        st_relaxed(side + 1, val);
-        return 0;
-    }
-    uint64_t h = mix64(key) & m.cap_mask;
-    for (uint64_t i = 0; i < cap; i++) {
-        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
-        uint64_t k = ld_acquire(s);
-        if (k == key) {
+        if (present) {
             if (flags == 1) return -E_EXIST;
             st_relaxed(s + 1, val);
             return 0;
         }
-        if (k != GX_HASH_EMPTY) continue;
         if (flags == 2) return -E_NOENT;
-        if (atomicAdd(count, 1ull) >= m.max_entries) {
-            atomicAdd(count, ~0ull);
+        if (ld_relaxed(reinterpret_cast<const uint64_t *>(&ctr[1])) >= m.max_entries) {
             full = true;
             return -E_2BIG;
         }
+        const uint64_t empty = key == GX_HASH_EMPTY ? 0 : GX_HASH_EMPTY;
+        const uint64_t tag = key == GX_HASH_EMPTY ? 1 : key;
         uint64_t ol, oh;
-        cas128(s, GX_HASH_EMPTY, 0, key, val, ol, oh);
-        if (ol == GX_HASH_EMPTY) return 0;
-        atomicAdd(count, ~0ull); /* lost the slot */
-        if (ol == key) {
-            if (flags == 1) return -E_EXIST;
-            st_relaxed(s + 1, val);
+        cas128(s, empty, 0, tag, val, ol, oh);
+        if (ol == empty && oh == 0) {
+            atomicAdd(&ctr[1], 1ull);
             return 0;
         }
+        /* lost the slot: probe again (the winner may hold our key) */
     }
-    full = true;
-    return -E_2BIG;
 }
 
 /* ---- per-thread ARRAY: value pointers are LOGICAL addresses data + key*vs + off; the lane's

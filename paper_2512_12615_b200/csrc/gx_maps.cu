@@ -73,40 +73,61 @@ __global__ void add_kernel(const uint64_t *a, const uint64_t *b, uint64_t *out, 
         out[i] = a[i] + b[i];
 }
 
-/* hash delta export: entries whose value differs from the base copy, or that are new */
-__global__ void hash_export_kernel(GxMapDesc m, GxMapDesc base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
-                                   unsigned long long *count) {
+/* hash delta export: entries whose value differs from the base copy (or are new), bucketed by
+ * owner = mix64(key) mod nranks.  Pass 0 counts per owner, pass 1 scatters at per-owner offsets. */
+__device__ __forceinline__ bool export_entry(const GxMapDesc &m, const GxMapDesc &base, uint64_t i, uint64_t &k,
+                                             uint64_t &d) {
     const uint64_t *slots = reinterpret_cast<const uint64_t *>(m.data);
+    const uint64_t cap = (uint64_t)m.cap_mask + 1;
+    k = slots[2 * i];
+    const uint64_t v = slots[2 * i + 1];
+    if (i < cap) {
+        if (k == GX_HASH_EMPTY) return false;
+    } else {
+        if (k != 1) return false;
+        k = GX_HASH_EMPTY;
+    }
+    const uint64_t *bv = gxd::hash_find(base, k);
+    d = v - (bv ? *bv : 0);
+    return !(bv && d == 0);
+}
+__global__ void hash_export_kernel(GxMapDesc m, GxMapDesc base, uint32_t nranks, int32_t owner, int pass,
+                                   unsigned long long *counts, unsigned long long *offsets, uint64_t *keys,
+                                   uint64_t *deltas, uint64_t cap_out) {
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
          i += gridDim.x * (uint64_t)blockDim.x) {
-        uint64_t k = slots[2 * i], v = slots[2 * i + 1];
-        if (i < cap) {
-            if (k == GX_HASH_EMPTY) continue;
+        uint64_t k, d;
+        if (!export_entry(m, base, i, k, d)) continue;
+        const uint32_t g = (uint32_t)(gxd::mix64(k) % nranks);
+        if (owner >= 0 && g != (uint32_t)owner) continue;
+        if (pass == 0) {
+            atomicAdd(&counts[g], 1ull);
         } else {
-            if (k != 1) continue;
-            k = GX_HASH_EMPTY;
-        }
-        const uint64_t *bv = gxd::hash_find(base, k);
-        const uint64_t d = v - (bv ? *bv : 0);
-        if (bv && d == 0) continue;
-        const unsigned long long o = atomicAdd(count, 1ull);
-        if (o < cap_out) {
-            keys[o] = k;
-            deltas[o] = d;
+            const unsigned long long o = atomicAdd(&offsets[g], 1ull);
+            if (o < cap_out) {
+                keys[o] = k;
+                deltas[o] = d;
+            }
         }
     }
 }
 
-/* hash merge apply: value = base value (0 if absent) + summed delta; inserts new keys */
-__global__ void hash_apply_kernel(GxMapDesc m, GxMapDesc base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
-                                  unsigned long long *full) {
+/* hash merge accumulate: value += delta, inserting absent keys at 0 */
+__global__ void hash_accumulate_kernel(GxMapDesc m, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                                       unsigned long long *full) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x) {
-        const uint64_t *bv = gxd::hash_find(base, keys[i]);
-        const uint64_t v = (bv ? *bv : 0) + deltas[i];
-        bool f;
-        gxd::hash_update(m, keys[i], v, 0, f);
-        if (f) atomicAdd(full, 1ull);
+        uint64_t *v = gxd::hash_find(m, keys[i]);
+        if (!v) {
+            bool f;
+            gxd::hash_update(m, keys[i], 0, 1 /* NOEXIST */, f);
+            if (f) {
+                atomicAdd(full, 1ull);
+                continue;
+            }
+            v = gxd::hash_find(m, keys[i]);
+        }
+        if (v) atomicAdd(reinterpret_cast<unsigned long long *>(v), (unsigned long long)deltas[i]);
     }
 }
 
@@ -149,14 +170,16 @@ int gx_k_add(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cu
     add_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, n);
     return (int)cudaGetLastError();
 }
-int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
-                     unsigned long long *count, cudaStream_t s) {
-    hash_export_kernel<<<grid_for((uint64_t)m->cap_mask + 2, 256), 256, 0, s>>>(*m, *base, keys, deltas, cap_out, count);
+int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint32_t nranks, int32_t owner, int pass,
+                     unsigned long long *counts, unsigned long long *offsets, uint64_t *keys, uint64_t *deltas,
+                     uint64_t cap_out, cudaStream_t s) {
+    hash_export_kernel<<<grid_for((uint64_t)m->cap_mask + 2, 256), 256, 0, s>>>(*m, *base, nranks, owner, pass, counts,
+                                                                               offsets, keys, deltas, cap_out);
     return (int)cudaGetLastError();
 }
-int gx_k_hash_apply(const GxMapDesc *m, const GxMapDesc *base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
-                    unsigned long long *full, cudaStream_t s) {
-    hash_apply_kernel<<<grid_for(n, 256), 256, 0, s>>>(*m, *base, keys, deltas, n, full);
+int gx_k_hash_accumulate(const GxMapDesc *m, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                         unsigned long long *full, cudaStream_t s) {
+    hash_accumulate_kernel<<<grid_for(n, 256), 256, 0, s>>>(*m, keys, deltas, n, full);
     return (int)cudaGetLastError();
 }
 

@@ -35,10 +35,11 @@ int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64
                           int64_t *rc, unsigned long long *full, cudaStream_t s);
 int gx_k_sub(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s);
 int gx_k_add(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s);
-int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint64_t *keys, uint64_t *deltas, uint64_t cap_out,
-                     unsigned long long *count, cudaStream_t s);
-int gx_k_hash_apply(const GxMapDesc *m, const GxMapDesc *base, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
-                    unsigned long long *full, cudaStream_t s);
+int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint32_t nranks, int32_t owner, int pass,
+                     unsigned long long *counts, unsigned long long *offsets, uint64_t *keys, uint64_t *deltas,
+                     uint64_t cap_out, cudaStream_t s);
+int gx_k_hash_accumulate(const GxMapDesc *m, const uint64_t *keys, const uint64_t *deltas, uint64_t n,
+                         unsigned long long *full, cudaStream_t s);
 }
 
 namespace {
@@ -752,49 +753,72 @@ int gx_merge_apply(gx_rt *rt, int fd, const uint64_t *d_sum, void *stream) {
     return 0;
 }
 
-int gx_hash_export(gx_rt *rt, int fd, uint64_t *d_keys, uint64_t *d_vals, uint64_t cap, uint64_t *n_out) {
-    if (!check_map(rt, fd) || !n_out) return -EINVAL;
+int gx_hash_export(gx_rt *rt, int fd, uint32_t nranks, int32_t owner, uint64_t *d_keys, uint64_t *d_vals,
+                   uint64_t cap, uint64_t *h_counts) {
+    if (!check_map(rt, fd) || !h_counts || nranks == 0 || nranks > 4096 || owner >= (int32_t)nranks) return -EINVAL;
     Map &m = rt->maps[fd];
     if (m.spec.type != GX_MAP_HASH) return -EINVAL;
     int rc = ensure_base(rt, m);
     if (rc) return rc;
-    unsigned long long *cnt;
-    CK(cudaMalloc(&cnt, 8), "cudaMalloc");
-    CK(cudaMemset(cnt, 0, 8), "memset");
+    unsigned long long *cnt, *off;
+    CK(cudaMalloc(&cnt, 16ull * nranks), "cudaMalloc");
+    off = cnt + nranks;
+    CK(cudaMemset(cnt, 0, 16ull * nranks), "memset");
     GxMapDesc d = make_desc(m), b = make_base_desc(m);
-    int e = gx_k_hash_export(&d, &b, d_keys, d_vals, cap, cnt, 0);
+    int e = gx_k_hash_export(&d, &b, nranks, owner, 0, cnt, off, d_keys, d_vals, cap, 0);
     if (e) return cuda_err(rt, (cudaError_t)e, "hash export");
-    unsigned long long h;
-    CK(cudaMemcpy(&h, cnt, 8, cudaMemcpyDeviceToHost), "hash export count");
+    std::vector<unsigned long long> c(nranks), o(nranks);
+    CK(cudaMemcpy(c.data(), cnt, 8ull * nranks, cudaMemcpyDeviceToHost), "hash export counts");
+    uint64_t total = 0;
+    for (uint32_t g = 0; g < nranks; g++) {
+        o[g] = total;
+        total += c[g];
+        h_counts[g] = c[g];
+    }
+    if (total > cap) {
+        cudaFree(cnt);
+        return set_err(rt, -E2BIG, "hash export needs %llu entries (cap %llu)", (unsigned long long)total,
+                       (unsigned long long)cap);
+    }
+    if (total) {
+        CK(cudaMemcpy(off, o.data(), 8ull * nranks, cudaMemcpyHostToDevice), "hash export offsets");
+        e = gx_k_hash_export(&d, &b, nranks, owner, 1, cnt, off, d_keys, d_vals, cap, 0);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash export");
+    }
+    CK(cudaDeviceSynchronize(), "hash export");
     cudaFree(cnt);
-    *n_out = h;
-    return h > cap ? -E2BIG : 0;
+    return 0;
 }
 
-int gx_hash_apply(gx_rt *rt, int fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n, void *stream) {
-    if (!check_map(rt, fd)) return -EINVAL;
+int gx_hash_apply(gx_rt *rt, int fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n, uint32_t flags,
+                  void *stream) {
+    if (!check_map(rt, fd) || (n && (!d_keys || !d_vals)) || (flags & ~3u)) return -EINVAL;
     Map &m = rt->maps[fd];
     if (m.spec.type != GX_MAP_HASH) return -EINVAL;
     int rc = ensure_base(rt, m);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
+    if (flags & GX_MERGE_RESTORE) {
+        CK(cudaMemcpyAsync(m.data, m.base, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash restore");
+        CK(cudaMemcpyAsync(m.aux, m.base_aux, 64, cudaMemcpyDeviceToDevice, s), "hash restore");
+    }
     unsigned long long *full;
     CK(cudaMalloc(&full, 8), "cudaMalloc");
-    CK(cudaMemset(full, 0, 8), "memset");
-    GxMapDesc d = make_desc(m), b = make_base_desc(m);
+    CK(cudaMemsetAsync(full, 0, 8, s), "memset");
+    GxMapDesc d = make_desc(m);
     if (n) {
-        int e = gx_k_hash_apply(&d, &b, d_keys, d_vals, n, full, s);
-        if (e) return cuda_err(rt, (cudaError_t)e, "hash apply");
+        int e = gx_k_hash_accumulate(&d, d_keys, d_vals, n, full, s);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash accumulate");
     }
-    CK(cudaMemcpyAsync(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash base");
-    CK(cudaMemcpyAsync(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice, s), "hash base");
+    if (flags & GX_MERGE_COMMIT) {
+        CK(cudaMemcpyAsync(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash commit");
+        CK(cudaMemcpyAsync(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice, s), "hash commit");
+    }
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, full, 8, cudaMemcpyDeviceToHost, s), "hash full");
     CK(cudaStreamSynchronize(s), "sync");
     cudaFree(full);
-    if (h) {
-        return set_err(rt, -E2BIG, "merged hash union exceeds max_entries (%llu refused)", h);
-    }
+    if (h) return set_err(rt, -E2BIG, "merged hash union exceeds max_entries (%llu refused)", h);
     return 0;
 }
 
