@@ -180,6 +180,9 @@ int  gx_exec_info(gx_rt *rt, uint32_t *grid, uint32_t *block, uint32_t *smem, ui
  * All device pointers are caller-owned; merge_export / merge_apply / hash_apply are stream-ordered
  * on cuda_stream (hash_apply synchronises before returning). */
 enum { GX_MERGE_RESTORE = 1, GX_MERGE_COMMIT = 2 };
+/* (Re)takes the base snapshot of a map = the state every rank agrees on.  Call it on every rank
+ * after identical initialisation and before the first batch; each merge then advances it. */
+int  gx_merge_snapshot(gx_rt *rt, int map_fd);
 int  gx_merge_words(gx_rt *rt, int map_fd, uint64_t *words);
 int  gx_merge_export(gx_rt *rt, int map_fd, uint64_t *d_delta, void *cuda_stream);
 int  gx_merge_apply(gx_rt *rt, int map_fd, const uint64_t *d_sum, void *cuda_stream);

@@ -28,7 +28,7 @@ RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", 
          "MIXED_PTR")
 EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_map", "gx_read_map",
            "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_attach", "gx_run_batch", "gx_run_batch_host",
-           "gx_get_stats", "gx_exec_info", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
+           "gx_get_stats", "gx_exec_info", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply")
 
 
@@ -92,6 +92,7 @@ def lib():
         "gx_run_batch_host": (i32, [vp, vp, u64, i32, vp]),
         "gx_get_stats": (i32, [vp, C.POINTER(gx_batch_stats)]),
         "gx_exec_info": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), p64]),
+        "gx_merge_snapshot": (i32, [vp, i32]),
         "gx_merge_words": (i32, [vp, i32, p64]),
         "gx_merge_export": (i32, [vp, i32, vp, vp]),
         "gx_merge_apply": (i32, [vp, i32, vp, vp]),
@@ -249,6 +250,10 @@ def gx_ringbuf_drain(rt, fd) -> list[bytes]:
         out.append(raw[o + 8:o + 8 + ln])
         o += (8 + ln + 7) & ~7
     return out
+
+
+def gx_merge_snapshot(rt, fd):
+    _check(lib().gx_merge_snapshot(rt, fd), "gx_merge_snapshot", rt)
 
 
 def gx_merge_words(rt, fd) -> int:

@@ -692,8 +692,25 @@ int gx_merge_words(gx_rt *rt, int fd, uint64_t *words) {
     return 0;
 }
 
-static int ensure_base(gx_rt *rt, Map &m) {
-    if (m.base) return 0;
+static int ensure_base(gx_rt *rt, Map &m, bool retake = false) {
+    if (m.base && !retake) return 0;
+    if (m.base && retake) {
+        CK(cudaDeviceSynchronize(), "snapshot");
+        if (m.spec.type == GX_MAP_HASH) {
+            CK(cudaMemcpy(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice), "base");
+            CK(cudaMemcpy(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice), "base");
+        } else {
+            uint64_t bytes = (uint64_t)m.spec.max_entries * m.spec.value_size;
+            if (m.spec.type == GX_MAP_ARRAY) CK(cudaMemcpy(m.base, m.data, bytes, cudaMemcpyDeviceToDevice), "base");
+            else {
+                int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, (uint64_t *)m.base, 0);
+                if (e) return cuda_err(rt, (cudaError_t)e, "base fold");
+            }
+        }
+        CK(cudaDeviceSynchronize(), "snapshot");
+        return 0;
+    }
+    CK(cudaDeviceSynchronize(), "snapshot");
     if (m.spec.type == GX_MAP_HASH) {
         CK(cudaMalloc(&m.base, m.data_bytes), "cudaMalloc base");
         CK(cudaMalloc(&m.base_aux, 64), "cudaMalloc base");
@@ -710,6 +727,13 @@ static int ensure_base(gx_rt *rt, Map &m) {
     }
     CK(cudaDeviceSynchronize(), "base");
     return 0;
+}
+
+int gx_merge_snapshot(gx_rt *rt, int fd) {
+    if (!check_map(rt, fd)) return -ENOENT;
+    Map &m = rt->maps[fd];
+    if (m.spec.type == GX_MAP_RINGBUF) return -EINVAL;
+    return ensure_base(rt, m, true);
 }
 
 int gx_merge_export(gx_rt *rt, int fd, uint64_t *d_delta, void *stream) {

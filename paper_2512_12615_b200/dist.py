@@ -44,6 +44,9 @@ class GxEngine:
     def spec(self, fd):
         return self.rt.specs[fd]
 
+    def merge_snapshot(self, fd):
+        self.gx.gx_merge_snapshot(self.rt.rt, fd)
+
     def merge_words(self, fd) -> int:
         return self.gx.gx_merge_words(self.rt.rt, fd)
 
@@ -74,6 +77,8 @@ class Merger:
         self.rank = dist.get_rank(group)
         self.additive = [fd for fd in fds if self.eng.spec(fd)[0] in (ARRAY, PERTHREAD_ARRAY)]
         self.hashes = [fd for fd in fds if self.eng.spec(fd)[0] == HASH]
+        for fd in self.additive + self.hashes:   # the agreed initial state
+            self.eng.merge_snapshot(fd)
         self.words = [self.eng.merge_words(fd) for fd in self.additive]
         self.packed = torch.zeros(sum(self.words), dtype=torch.int64, device=self.eng.device)
         self.merges = 0

@@ -40,6 +40,9 @@ class OracleEngine:
             return None
         return self.env.array_u64(fd).copy()
 
+    def merge_snapshot(self, fd):
+        self.base[fd] = self._read(fd)
+
     def merge_words(self, fd):
         return self.spec(fd)[2] * self.spec(fd)[3] // 8
 
