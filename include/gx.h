@@ -90,7 +90,10 @@ typedef struct {
     uint32_t stack_depth;      /* bytes, rounded up to 8 */
     uint32_t all_uniform;      /* 1 if no conditional branch depends on a LANE_VARYING value */
     uint32_t commutative;      /* 1 if shared maps change only through commutative updates */
-    uint32_t n_insns;
+    uint32_t n_insns;          /* input slots */
+    uint32_t image_insns;      /* executor instructions after pre-decoding (dead helper-argument
+                                  set-up removed, superinstructions fused, ldimm64 pairs merged) */
+    uint32_t reserved;
 } gx_verify_report;
 
 typedef struct {

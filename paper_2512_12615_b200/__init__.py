@@ -46,7 +46,8 @@ class gx_verify_report(C.Structure):
     _fields_ = [("verdict", C.c_int32), ("n_violations", C.c_uint32), ("first_insn", C.c_uint32),
                 ("first_rule", C.c_uint32), ("worst_insns", C.c_uint64), ("worst_helpers", C.c_uint64),
                 ("worst_memops", C.c_uint64), ("processed_insns", C.c_uint64), ("stack_depth", C.c_uint32),
-                ("all_uniform", C.c_uint32), ("commutative", C.c_uint32), ("n_insns", C.c_uint32)]
+                ("all_uniform", C.c_uint32), ("commutative", C.c_uint32), ("n_insns", C.c_uint32),
+                ("image_insns", C.c_uint32), ("reserved", C.c_uint32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

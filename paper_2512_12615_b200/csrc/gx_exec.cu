@@ -296,8 +296,13 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                 }
                 c_steps++;
                 const bool me = (exec >> lane) & 1;
-                const GxInsn in = P[pc];
-                uint32_t npc = pc + 1;
+                GxInsn in;
+                {   /* one 16-B broadcast LDS per instruction */
+                    const uint4 w = reinterpret_cast<const uint4 *>(P)[pc];
+                    in = *reinterpret_cast<const GxInsn *>(&w);
+                }
+                uint32_t npc = pc + 1, tgt = 0;
+                bool taken = false;
                 uint64_t *const RD = &R[in.dst * 32 + lane];
                 const uint64_t S = (in.flags & GXF_X) ? R[in.src * 32 + lane] : in.imm;
                 switch (in.op) {
@@ -357,9 +362,8 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                 case GX_MOVSX32: if (me) *RD = (uint32_t)sext(S, in.aux); break;
                 case GX_LE: if (me && in.aux < 64) *RD = *RD & ((1ull << in.aux) - 1); break;
                 case GX_BE: if (me) *RD = bswap_w(*RD, in.aux); break;
-                case GX_LDIMM:
+                case GX_LDIMM: /* the pre-decoder dropped the second slot */
                     if (me) *RD = (in.flags & GXF_VAL_MAPV) ? M[in.aux].data + in.imm : in.imm;
-                    npc = pc + 2;
                     break;
 
                 /* ---------------- memory */
@@ -405,10 +409,11 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     break;
                 case GX_ATOM_STACK:
                     if (me) {
-                        uint64_t nv, s = R[in.src * 32 + lane];
+                        const uint32_t op = (uint32_t)(in.imm & 0xFF);
+                        uint64_t nv, s = (in.flags & GXF_PRIV) ? (uint64_t)(int64_t)(int32_t)(in.imm >> 32) : R[in.src * 32 + lane];
                         uint64_t old = rmw_private(&K[(in.off >> 3) * 32 + lane], in.off & 7, (in.aux & 15) == 2,
-                                                   (uint32_t)in.imm, s, R[lane], nv);
-                        if (in.imm == 0xF1) R[lane] = old;
+                                                   op, s, R[lane], nv);
+                        if (op == 0xF1) R[lane] = old;
                         else if (in.flags & GXF_FETCH) R[in.src * 32 + lane] = old;
                     }
                     break;
@@ -416,20 +421,22 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     if (me) {
                         const uint64_t a = (uint64_t)gxd::pt_phys(M[in.aux >> 4], R[in.dst * 32 + lane] + in.off, shard);
                         const bool w32 = (in.aux & 15) == 2;
-                        uint64_t nv, s = R[in.src * 32 + lane];
+                        const uint32_t op = (uint32_t)(in.imm & 0xFF);
+                        uint64_t nv, s = (in.flags & GXF_PRIV) ? (uint64_t)(int64_t)(int32_t)(in.imm >> 32) : R[in.src * 32 + lane];
                         uint64_t *w = reinterpret_cast<uint64_t *>(a & ~7ull);
-                        uint64_t old = rmw_private(w, a & 7, w32, (uint32_t)in.imm, s, R[lane], nv);
-                        if (in.imm == 0xF1) R[lane] = old;
+                        uint64_t old = rmw_private(w, a & 7, w32, op, s, R[lane], nv);
+                        if (op == 0xF1) R[lane] = old;
                         else if (in.flags & GXF_FETCH) R[in.src * 32 + lane] = old;
                     }
                     break;
                 case GX_ATOM_MAP: {
                     /* a7: warp-aggregated atomics on shared map values */
-                    const uint32_t op = (uint32_t)in.imm;
+                    const uint32_t op = (uint32_t)(in.imm & 0xFF);
                     const bool w32 = (in.aux & 15) == 2;
                     const GxMapDesc &md = M[in.aux >> 4];
                     const uint64_t addr = me ? R[in.dst * 32 + lane] + in.off : 0;
-                    const uint64_t sv = me ? R[in.src * 32 + lane] : 0;
+                    const uint64_t sv = !me ? 0 : (in.flags & GXF_PRIV) ? (uint64_t)(int64_t)(int32_t)(in.imm >> 32)
+                                                                       : R[in.src * 32 + lane];
                     if (op == 0xE1 || op == 0xF1) { /* XCHG / CMPXCHG: per lane */
                         if (me) {
                             if (op == 0xE1) {
@@ -530,6 +537,7 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                                                                       : (uint32_t)(K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7)));
                         R[lane] = k < md.max_entries ? md.data + (uint64_t)k * md.value_size : 0;
                     }
+                    if (in.flags & (GXF_FETCH | GXF_W32)) goto lookup_branch;
                     break;
                 case GX_CALL_LOOKUP_HASH:
                     if (me) {
@@ -542,6 +550,7 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         uint64_t *v = gxd::hash_find(md, k);
                         R[lane] = (uint64_t)v;
                     }
+                    if (in.flags & (GXF_FETCH | GXF_W32)) goto lookup_branch;
                     break;
                 case GX_CALL_UPDATE_ARRAY:
                 case GX_CALL_UPDATE_PT:
@@ -635,7 +644,7 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     npc = in.aux;
                     break;
                 case GX_EXIT:
-                    if (me && ret) ret[idx] = R[lane];
+                    if (me && ret) ret[idx] = (in.flags & GXF_SX) ? in.imm : R[lane];
                     active &= ~exec;
                     npc = 0xFFFFFFFFu;
                     break;
@@ -651,32 +660,21 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                             sd = (int32_t)d;
                             ss = (int32_t)s;
                         }
-                        bool t;
                         switch (cop) {
-                        case GX_JEQ: t = d == s; break;
-                        case GX_JNE: t = d != s; break;
-                        case GX_JGT: t = d > s; break;
-                        case GX_JGE: t = d >= s; break;
-                        case GX_JLT: t = d < s; break;
-                        case GX_JLE: t = d <= s; break;
-                        case GX_JSGT: t = sd > ss; break;
-                        case GX_JSGE: t = sd >= ss; break;
-                        case GX_JSLT: t = sd < ss; break;
-                        case GX_JSLE: t = sd <= ss; break;
-                        default: t = (d & s) != 0; break;
+                        case GX_JEQ: taken = d == s; break;
+                        case GX_JNE: taken = d != s; break;
+                        case GX_JGT: taken = d > s; break;
+                        case GX_JGE: taken = d >= s; break;
+                        case GX_JLT: taken = d < s; break;
+                        case GX_JLE: taken = d <= s; break;
+                        case GX_JSGT: taken = sd > ss; break;
+                        case GX_JSGE: taken = sd >= ss; break;
+                        case GX_JSLT: taken = sd < ss; break;
+                        case GX_JSLE: taken = sd <= ss; break;
+                        default: taken = (d & s) != 0; break;
                         }
-                        t = t && me;
-                        const unsigned tb = __ballot_sync(GX_FULL, t);
-                        if (uni) {
-                            if (tb == exec) npc = in.aux;
-                            else if (tb != 0) {
-                                uni = false;
-                                mypc = t ? in.aux : pc + 1;
-                                goto next_step;
-                            }
-                        } else {
-                            npc = t ? in.aux : pc + 1;
-                        }
+                        tgt = in.aux;
+                        goto do_branch;
                     } else {
                         /* GX_OP_NOP: an instruction the verifier proved unreachable -- trap */
                         active &= ~exec;
@@ -684,6 +682,24 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         npc = 0xFFFFFFFFu;
                     }
                     break;
+                }
+                if (false) {
+                lookup_branch:
+                    taken = (in.flags & GXF_FETCH) ? R[lane] == 0 : R[lane] != 0;
+                    tgt = (uint32_t)in.imm;
+                do_branch:
+                    taken = taken && me;
+                    const unsigned tb = __ballot_sync(GX_FULL, taken);
+                    if (uni) {
+                        if (tb == exec) npc = tgt;
+                        else if (tb != 0) {
+                            uni = false;
+                            mypc = taken ? tgt : pc + 1;
+                            goto next_step;
+                        }
+                    } else {
+                        npc = taken ? tgt : pc + 1;
+                    }
                 }
                 if (uni) pc = npc;
                 else if (me) mypc = npc;

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -1784,6 +1785,195 @@ struct Verifier {
         }
     }
     std::vector<uint8_t> hint_uniform;
+
+    /* ---------------------------------------------------------------- stage 6: image optimisation
+     * Liveness-based removal of instructions whose only effect is a register nobody reads (the
+     * helper-argument set-up `lddw r1, map; mov r2, r10; add r2, -k` that the pre-decoded call
+     * resolved statically), three superinstructions, and compaction (ldimm64 second slots go).
+     * Pure re-encoding of the verified program: same per-event semantics (tests compare with the
+     * oracle). */
+    struct UD {
+        uint16_t use = 0, def = 0;
+        bool effect = false;
+    };
+    static UD ud_of(const GxInsn &g) {
+        UD u;
+        auto R = [](int r) { return (uint16_t)(1u << r); };
+        const bool x = g.flags & GXF_X;
+        switch (g.op) {
+        case GX_MOV64: case GX_MOV32:
+            u.use = x ? R(g.src) : 0;
+            u.def = R(g.dst);
+            break;
+        case GX_MOVSX64: case GX_MOVSX32:
+            u.use = R(g.src);
+            u.def = R(g.dst);
+            break;
+        case GX_NEG64: case GX_NEG32: case GX_LE: case GX_BE:
+            u.use = R(g.dst);
+            u.def = R(g.dst);
+            break;
+        case GX_LDIMM: u.def = R(g.dst); break;
+        case GX_JA: break;
+        case GX_EXIT: u.use = R(0); u.effect = true; break;
+        case GX_LDX_CTX: case GX_LDX_STACK: u.def = R(g.dst); break;
+        case GX_LDX_MAP: case GX_LDX_PT: u.use = R(g.src); u.def = R(g.dst); break;
+        case GX_ST_STACK: u.use = x ? R(g.src) : 0; u.effect = true; break;
+        case GX_ST_MAP: case GX_ST_PT: u.use = R(g.dst) | (x ? R(g.src) : 0); u.effect = true; break;
+        case GX_ATOM_STACK: case GX_ATOM_MAP: case GX_ATOM_PT: {
+            const uint32_t op = (uint32_t)(g.imm & 0xFF);
+            u.use = R(g.src) | (g.op != GX_ATOM_STACK ? R(g.dst) : 0) | (op == 0xF1 ? R(0) : 0);
+            if (op == 0xF1) u.def = R(0);
+            else if (op & 1) u.def = R(g.src);
+            u.effect = true;
+            break;
+        }
+        case GX_CALL_LOOKUP_ARRAY: case GX_CALL_LOOKUP_PT: case GX_CALL_LOOKUP_HASH:
+            u.use = (g.flags & GXF_KEY_MAPV) ? R(2) : 0;
+            u.def = 0x3F;
+            u.effect = true;
+            break;
+        case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: case GX_CALL_UPDATE_HASH:
+            u.use = R(4) | ((g.flags & GXF_KEY_MAPV) ? R(2) : 0) | ((g.flags & GXF_VAL_MAPV) ? R(3) : 0);
+            u.def = 0x3F;
+            u.effect = true;
+            break;
+        case GX_CALL_RINGBUF_OUTPUT:
+            u.use = (g.flags & GXF_VAL_MAPV) ? R(2) : 0;
+            u.def = 0x3F;
+            u.effect = true;
+            break;
+        case GX_OP_NOP: u.effect = true; break;
+        default:
+            if (g.op >= GX_JEQ && g.op <= GX_JSET32) {
+                u.use = R(g.dst) | (x ? R(g.src) : 0);
+            } else { /* binary ALU */
+                u.use = R(g.dst) | (x ? R(g.src) : 0);
+                u.def = R(g.dst);
+            }
+        }
+        return u;
+    }
+    static bool is_jcc(uint8_t op) { return op >= GX_JEQ && op <= GX_JSET32; }
+
+    void optimize(bool full) {
+        std::vector<GxInsn> &im = out.image;
+        const uint32_t N = (uint32_t)im.size();
+        std::vector<uint8_t> removed(N, 0), target(N, 0);
+        for (uint32_t i = 0; i < N; i++)
+            if (is_second[i]) removed[i] = 1;
+        auto succs = [&](uint32_t i, uint32_t *s) -> int {
+            const GxInsn &g = im[i];
+            if (g.op == GX_EXIT || g.op == GX_OP_NOP) return 0;
+            uint32_t nx = i + (g.op == GX_LDIMM ? 2 : 1);
+            if (g.op == GX_JA) { s[0] = g.aux; return 1; }
+            if (is_jcc(g.op)) { s[0] = g.aux; s[1] = nx; return 2; }
+            s[0] = nx;
+            return 1;
+        };
+        for (uint32_t i = 0; i < N; i++)
+            if (!removed[i] && (im[i].op == GX_JA || is_jcc(im[i].op))) target[im[i].aux] = 1;
+        /* dead-definition elimination to a fixpoint (removed insns become pass-throughs) */
+        for (int round = 0; round < (full ? 16 : 0); round++) {
+            std::vector<uint16_t> live_in(N, 0), live_out(N, 0);
+            bool ch = true;
+            while (ch) {
+                ch = false;
+                for (int i = (int)N - 1; i >= 0; i--) {
+                    if (is_second[i]) continue;
+                    uint32_t sv[2];
+                    int ns = succs(i, sv);
+                    uint16_t lo = 0;
+                    for (int k = 0; k < ns; k++)
+                        if (sv[k] < N) lo |= live_in[sv[k]];
+                    uint16_t li;
+                    if (removed[i]) li = lo;
+                    else {
+                        UD u = ud_of(im[i]);
+                        li = (uint16_t)(u.use | (lo & ~u.def));
+                    }
+                    if (lo != live_out[i] || li != live_in[i]) {
+                        live_out[i] = lo;
+                        live_in[i] = li;
+                        ch = true;
+                    }
+                }
+            }
+            bool any = false;
+            for (uint32_t i = 0; i < N; i++) {
+                if (removed[i] || is_second[i]) continue;
+                UD u = ud_of(im[i]);
+                if (!u.effect && u.def && !(u.def & live_out[i]) && im[i].op != GX_JA && !is_jcc(im[i].op)) {
+                    removed[i] = 1;
+                    any = true;
+                }
+            }
+            if (!any) {
+                live = live_out;
+                break;
+            }
+        }
+        if (live.size() != N) live.assign(N, 0x7FF);
+        /* superinstructions over adjacent surviving instructions */
+        auto next_kept = [&](uint32_t i) {
+            uint32_t j = i + 1;
+            while (j < N && removed[j]) j++;
+            return j;
+        };
+        for (uint32_t i = 0; i < N && full; i++) {
+            if (removed[i]) continue;
+            GxInsn &a = im[i];
+            uint32_t j = next_kept(i);
+            if (j >= N || target[j]) continue;
+            /* all removed insns between i and j must not be jump targets either */
+            bool clean = true;
+            for (uint32_t k = i + 1; k < j; k++)
+                if (target[k]) clean = false;
+            if (!clean) continue;
+            GxInsn &b = im[j];
+            if (a.op == GX_MOV64 && !(a.flags & GXF_X) && a.dst == 0 && b.op == GX_EXIT) {
+                b = a;
+                b.op = GX_EXIT;
+                b.flags = GXF_SX; /* exit with r0 = imm */
+                std::swap(a, b);
+                removed[j] = 1;
+            } else if ((a.op == GX_CALL_LOOKUP_ARRAY || a.op == GX_CALL_LOOKUP_PT || a.op == GX_CALL_LOOKUP_HASH) &&
+                       (b.op == GX_JEQ || b.op == GX_JNE) && b.dst == 0 && !(b.flags & GXF_X) && b.imm == 0) {
+                a.flags |= b.op == GX_JEQ ? GXF_FETCH /* jump if NULL */ : GXF_W32 /* jump if not NULL */;
+                a.imm = b.aux;
+                removed[j] = 1;
+            } else if (a.op == GX_MOV64 && !(a.flags & GXF_X) &&
+                       (b.op == GX_ATOM_MAP || b.op == GX_ATOM_PT || b.op == GX_ATOM_STACK) && b.src == a.dst &&
+                       !(b.imm & 1) && (b.imm & 0xFF) != 0xE1 && !(live[j] & (1u << a.dst))) {
+                GxInsn f = b;
+                f.flags |= GXF_PRIV; /* constant operand in imm[63:32] */
+                f.imm = (b.imm & 0xFF) | ((uint64_t)(uint32_t)(int32_t)(int64_t)a.imm << 32);
+                a = f;
+                removed[j] = 1;
+            }
+        }
+        /* compaction */
+        std::vector<uint32_t> map(N + 1, 0);
+        uint32_t np = 0;
+        for (uint32_t i = 0; i < N; i++) {
+            map[i] = np;
+            if (!removed[i]) np++;
+        }
+        map[N] = np;
+        std::vector<GxInsn> c;
+        c.reserve(np);
+        for (uint32_t i = 0; i < N; i++) {
+            if (removed[i]) continue;
+            GxInsn g = im[i];
+            if (g.op == GX_JA || is_jcc(g.op)) g.aux = (uint16_t)map[g.aux];
+            if ((g.op == GX_CALL_LOOKUP_ARRAY || g.op == GX_CALL_LOOKUP_PT || g.op == GX_CALL_LOOKUP_HASH) &&
+                (g.flags & (GXF_FETCH | GXF_W32)))
+                g.imm = map[g.imm];
+            c.push_back(g);
+        }
+        im.swap(c);
+    }
+    std::vector<uint16_t> live;
 };
 
 }  // namespace
@@ -1847,6 +2037,8 @@ int gx_verify_program(const uint8_t *slots, uint32_t n, const GxMapInfo *maps, c
     rep.commutative = comm;
     out.stack_depth = rep.stack_depth;
     v.predecode();
+    v.optimize(getenv("GX_NO_OPT") == nullptr);
+    rep.image_insns = (uint32_t)out.image.size();
     rep.verdict = 0;
     return 0;
 }
