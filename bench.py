@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--extra", action="store_true", help="also time C1/C3/C4 single-GPU lines (stderr)")
+    p.add_argument("--engine", default="jit", choices=["jit", "interp"],
+                   help="headline engine (the other one is timed too and reported under 'engines')")
     return p.parse_args()
 
 
@@ -195,7 +197,8 @@ def main():
     seed = configs.SEEDS[config]
     stream = torch.cuda.current_stream()
 
-    rt = gx.Runtime(local)
+    engine_id = gx.GX_ENGINE_JIT if args.engine == "jit" else gx.GX_ENGINE_INTERP
+    rt = gx.Runtime(local, engine=engine_id)
     s = configs.setup(rt, config)
     events = gen_gpu.generate_device(config, seed, n, i0=rank * n, n_total=n_total, device=local)
     torch.cuda.synchronize()
@@ -210,9 +213,11 @@ def main():
         if merger is not None:
             merger.merge()
 
+    t_compile = time.perf_counter()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    t_compile = time.perf_counter() - t_compile
     launches0 = gx.gx_exec_info(rt.rt)["launches"]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     per_launch = []
@@ -247,7 +252,7 @@ def main():
     alg_bytes = EVENT_BYTES * n
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{config}_{args.engine}.json")
     if os.path.exists(tfile):
         try:
             traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
@@ -262,13 +267,33 @@ def main():
                    "parallelism": f"dp{world}" if world > 1 else "dp1"},
         "ns_per_event": t_ms * 1e6 / (n_total * args.steps) * world,
         "gpu_launches": int(launches),
+        "engine": args.engine,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
-                     "kernel": "gx_exec_kernel", "alg_bytes_per_launch": alg_bytes,
-                     "peak_kind": peak_kind, "kernel_ms": kernel_ms},
+                     "kernel": "gx_jit_kernel" if args.engine == "jit" else "gx_exec_kernel",
+                     "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind, "kernel_ms": kernel_ms},
+        "warmup_incl_jit_s": t_compile,
         "stats": {k: int(v) // max(1, args.steps + args.warmup) for k, v in st.items()},
         "clocks": clk.summary(),
     }
+
+    # the other engine on the same events (same maps semantics; reported, not the headline)
+    if world == 1:
+        other = "interp" if args.engine == "jit" else "jit"
+        gx.gx_set_engine(rt.rt, gx.GX_ENGINE_INTERP if other == "interp" else gx.GX_ENGINE_JIT)
+        for _ in range(2):
+            rt.run(events, s.prog_arg, stream=stream)
+        a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            rt.run(events, s.prog_arg, stream=stream)
+        b2.record(stream)
+        torch.cuda.synchronize()
+        oms = a.elapsed_time(b2) / args.steps
+        line["engines"] = {other: {"value": n / (oms / 1e3), "kernel_ms": oms,
+                                   "hbm_frac": EVENT_BYTES * n / (oms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}}
+        gx.gx_set_engine(rt.rt, engine_id)
+        rt.stats()
 
     # end-to-end through the public API from pinned host memory (H2D inside the timed region)
     if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
@@ -325,8 +350,9 @@ def extra_lines(rt0, args):
     import torch
     import paper_2512_12615_b200 as gx
     from gxin import configs, gen_gpu
-    for config, n in (("C1", 1 << 20), ("C1", 1 << 26), ("C3", 1 << 28), ("C4", 1 << 28), ("C5", 1 << 26)):
-        rt = gx.Runtime(0)
+    for config, n, eng in [(c, n, e) for c, n in (("C1", 1 << 20), ("C1", 1 << 26), ("C1d", 1 << 26), ("C3", 1 << 28),
+                                                   ("C4", 1 << 28), ("C5", 1 << 26)) for e in ("jit", "interp")]:
+        rt = gx.Runtime(0, engine=gx.GX_ENGINE_JIT if eng == "jit" else gx.GX_ENGINE_INTERP)
         s = configs.setup(rt, config)
         ev = gen_gpu.generate_device(config, configs.SEEDS[config], n)
         for _ in range(3):
@@ -340,7 +366,7 @@ def extra_lines(rt0, args):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 5
         st = rt.stats()
-        print(json.dumps({"config": config, "events": n, "ms": ms, "events_per_s": n / ms * 1e3,
+        print(json.dumps({"config": config, "engine": eng, "events": n, "ms": ms, "events_per_s": n / ms * 1e3,
                           "hbm_frac": n * 32 / (ms / 1e3) / 1e9 / measured_peaks()[0]["hbm_gbs"],
                           "warp_steps_per_record": st["warp_steps"] / 8 / (n / 32),
                           "divergent_frac": st["divergent_steps"] / max(1, st["warp_steps"])}), file=sys.stderr, flush=True)

@@ -104,7 +104,7 @@ typedef struct {
     uint64_t ringbuf_bytes;    /* bytes committed to ring buffers */
     uint64_t ringbuf_drops;    /* ringbuf_output calls dropped (-EAGAIN) */
     uint64_t hash_full;        /* hash inserts refused because max_entries was reached */
-    uint64_t warp_steps;       /* interpreted warp-instructions (all paths) */
+    uint64_t warp_steps;       /* interpreted warp-instructions (all paths; 0 for the JIT engine) */
 } gx_batch_stats;
 
 /* ---------------------------------------------------------------- runtime */
@@ -143,6 +143,12 @@ int  gx_verify(gx_rt *rt, int prog_fd, const gx_verify_opts *opts, gx_verify_rep
  * report->verdict. */
 int  gx_verify_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *maps, uint32_t n_maps,
                        const gx_verify_opts *opts, gx_verify_report *report, char *log, uint64_t log_len);
+/* Generates and compiles (NVRTC, sm_100a) the JIT kernel of one program against map specs, with
+ * placeholder map addresses, without a runtime or device -- for tooling and CPU-side tests.
+ * src (nullable) receives the generated CUDA C++; log the compiler log.  Returns 0, the
+ * verifier's -errno, or -ENOSYS if NVRTC is unavailable / compilation failed. */
+int  gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *maps, uint32_t n_maps,
+                    char *src, uint64_t src_len, char *log, uint64_t log_len);
 /* Attach table entry (hook kind, tenant) -> program.  prog_fd = -1 detaches. */
 int  gx_attach(gx_rt *rt, int prog_fd, uint32_t hook_kind, uint32_t tenant);
 
@@ -158,6 +164,16 @@ int  gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n_events, int prog_f
  * on the runtime's own streams, overlapping copies with execution; h_ret (nullable) receives R0.
  * Synchronous.  This is the end-to-end path bench.py times as "e2e". */
 int  gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n_events, int prog_fd, uint64_t *h_ret);
+/* Execution engine for subsequent batches (default GX_ENGINE_JIT):
+ *   GX_ENGINE_INTERP  the warp-cooperative interpreter (uniform-PC fast path, min-PC divergent
+ *                     path);
+ *   GX_ENGINE_JIT     the verified, pre-decoded programs of a launch configuration compiled to
+ *                     sm_100a code by NVRTC, cached
+ *                     per configuration; -ENOSYS if libnvrtc cannot be loaded.
+ * Both engines compute the same results (parity-tested against the oracle). */
+enum { GX_ENGINE_INTERP = 0, GX_ENGINE_JIT = 1 };
+int  gx_set_engine(gx_rt *rt, int engine);
+int  gx_get_engine(gx_rt *rt);
 /* Cumulative stats since the last call (then reset).  Synchronous. */
 int  gx_get_stats(gx_rt *rt, gx_batch_stats *out);
 /* Launch geometry of the executor: grid blocks, threads per block, dynamic shared bytes of the

@@ -27,8 +27,8 @@ RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", 
          "COMPLEXITY", "BUDGET", "UNIFORM_BRANCH", "UNIFORM_LOOP_BOUND", "UNIFORM_MAP_KEY", "NON_UNIFORM_ATOMIC",
          "MIXED_PTR")
 EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_map", "gx_read_map",
-           "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_attach", "gx_run_batch", "gx_run_batch_host",
-           "gx_get_stats", "gx_exec_info", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
+           "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_jit_offline", "gx_attach", "gx_run_batch", "gx_run_batch_host",
+           "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply")
 
 
@@ -88,6 +88,9 @@ def lib():
         "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
         "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
                                     C.c_char_p, u64]),
+        "gx_jit_offline": (i32, [vp, u32, vp, u32, C.c_char_p, u64, C.c_char_p, u64]),
+        "gx_set_engine": (i32, [vp, i32]),
+        "gx_get_engine": (i32, [vp]),
         "gx_attach": (i32, [vp, i32, u32, u32]),
         "gx_run_batch": (i32, [vp, vp, u64, i32, vp, vp]),
         "gx_run_batch_host": (i32, [vp, vp, u64, i32, vp]),
@@ -170,6 +173,30 @@ def gx_verify_offline(slots: bytes, maps: dict, strict=False, max_insns=0, max_h
     log = C.create_string_buffer(1 << 16)
     v = lib().gx_verify_offline(slots, len(slots) // 8, arr, n, C.byref(opts), C.byref(rep), log, len(log))
     return v, rep.as_dict(), log.value.decode(errors="replace")
+
+
+def gx_jit_offline(slots: bytes, maps: dict):
+    """Generates + NVRTC-compiles the JIT kernel of one program without a device.
+    Returns (rc, generated source, compiler log)."""
+    n = max(maps) + 1 if maps else 0
+    arr = (gx_map_spec * max(n, 1))()
+    for fd, (t, ks, vs, me) in maps.items():
+        arr[fd] = gx_map_spec(t, ks, vs, me, 0)
+    src = C.create_string_buffer(1 << 20)
+    log = C.create_string_buffer(1 << 16)
+    rc = lib().gx_jit_offline(slots, len(slots) // 8, arr, n, src, len(src), log, len(log))
+    return rc, src.value.decode(errors="replace"), log.value.decode(errors="replace")
+
+
+GX_ENGINE_INTERP, GX_ENGINE_JIT = 0, 1
+
+
+def gx_set_engine(rt, engine):
+    _check(lib().gx_set_engine(rt, engine), "gx_set_engine", rt)
+
+
+def gx_get_engine(rt) -> int:
+    return lib().gx_get_engine(rt)
 
 
 def gx_attach(rt, prog_fd, kind, tenant):
@@ -292,8 +319,10 @@ def gx_hash_apply(rt, fd, keys, vals, n, flags=GX_MERGE_RESTORE | GX_MERGE_COMMI
 class Runtime:
     """One gx_rt.  Engine interface for gxin.configs.setup plus run / read helpers."""
 
-    def __init__(self, device: int = 0, strict: bool = False):
+    def __init__(self, device: int = 0, strict: bool = False, engine: int | None = None):
         self.rt = gx_open(device)
+        if engine is not None:
+            gx_set_engine(self.rt, engine)
         self.device = device
         self.strict = strict
         self.specs = {}

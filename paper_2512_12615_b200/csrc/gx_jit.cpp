@@ -1,0 +1,493 @@
+/*
+ * gx_jit.cpp -- per-launch JIT of verified programs to sm_100a machine code.
+ *
+ * "Verified programs are JIT-compiled into native host code or GPU-compatible instructions (e.g.,
+ * PTX)" (§4.2); "an LLVM-based backend translates the restricted gpu_ext eBPF
+ * instruction subset into GPU device code (PTX)" (§5.1); helpers and map accesses are
+ * inlined.  Here the verifier's pre-decoded image (every memory access already
+ * resolved to ctx / stack / map / per-thread kind, every helper to its map and argument slots) is
+ * translated to straight-line CUDA C++ and compiled by NVRTC for sm_100a; the cubin is loaded with
+ * cudaLibraryLoadData.  One kernel per launch configuration (programs + attach table + map
+ * descriptors, which are baked in as constants); cached by the runtime.
+ *
+ * NVRTC is loaded with dlopen so libgx.so has no link-time dependency on it.
+ */
+#include "gx_jit.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "gx_jit_headers.inc"  /* kJitHeaders[]: {name, text} of the device headers */
+
+namespace {
+
+struct Nvrtc {
+    bool ok = false;
+    std::string err;
+    decltype(&nvrtcCreateProgram) create;
+    decltype(&nvrtcCompileProgram) compile;
+    decltype(&nvrtcGetCUBINSize) cubin_size;
+    decltype(&nvrtcGetCUBIN) cubin;
+    decltype(&nvrtcGetProgramLogSize) log_size;
+    decltype(&nvrtcGetProgramLog) log;
+    decltype(&nvrtcDestroyProgram) destroy;
+    decltype(&nvrtcGetErrorString) errstr;
+};
+
+Nvrtc &nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *cands[] = {getenv("GX_NVRTC"), "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                               "/usr/local/cuda/lib64/libnvrtc.so", "libnvrtc.so"};
+        void *h = nullptr;
+        for (const char *c : cands)
+            if (c && (h = dlopen(c, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!h) {
+            n.err = "cannot dlopen libnvrtc.so.12";
+            return;
+        }
+#define LOAD(f, name)                                              \
+    n.f = (decltype(n.f))dlsym(h, name);                           \
+    if (!n.f) {                                                    \
+        n.err = std::string("libnvrtc lacks ") + name;             \
+        return;                                                    \
+    }
+        LOAD(create, "nvrtcCreateProgram");
+        LOAD(compile, "nvrtcCompileProgram");
+        LOAD(cubin_size, "nvrtcGetCUBINSize");
+        LOAD(cubin, "nvrtcGetCUBIN");
+        LOAD(log_size, "nvrtcGetProgramLogSize");
+        LOAD(log, "nvrtcGetProgramLog");
+        LOAD(destroy, "nvrtcDestroyProgram");
+        LOAD(errstr, "nvrtcGetErrorString");
+#undef LOAD
+        n.ok = true;
+    });
+    return n;
+}
+
+std::string hex(uint64_t v) {
+    char b[32];
+    snprintf(b, sizeof b, "0x%llxull", (unsigned long long)v);
+    return b;
+}
+
+struct Gen {
+    std::ostringstream o;
+    const GxLaunch &L;
+    explicit Gen(const GxLaunch &l) : L(l) {}
+
+    std::string md(int fd) {
+        const GxMapDesc &d = L.maps[fd];
+        std::ostringstream s;
+        s << "GxMapDesc{" << hex(d.data) << ", " << hex(d.aux) << ", " << d.type << "u, " << d.key_size << "u, "
+          << d.value_size << "u, " << d.max_entries << "u, " << d.nshards << "u, " << d.cap_mask << "u, "
+          << d.priv_off << "u, " << d.coherent << "u}";
+        return s.str();
+    }
+
+    static std::string R(int r) { return "r" + std::to_string(r); }
+    static std::string slot(int addr) { return "s" + std::to_string(addr >> 3); }
+
+    void program(int q, const GxInsn *im, uint32_t n) {
+        std::set<uint32_t> targets;
+        std::set<int> slots;
+        for (uint32_t i = 0; i < n; i++) {
+            const GxInsn &g = im[i];
+            if (g.op == GX_JA || (g.op >= GX_JEQ && g.op <= GX_JSET32)) targets.insert(g.aux);
+            if ((g.op == GX_CALL_LOOKUP_ARRAY || g.op == GX_CALL_LOOKUP_PT || g.op == GX_CALL_LOOKUP_HASH) &&
+                (g.flags & (GXF_FETCH | GXF_W32)))
+                targets.insert((uint32_t)g.imm);
+            switch (g.op) {
+            case GX_LDX_STACK: case GX_ST_STACK: case GX_ATOM_STACK: slots.insert(g.off >> 3); break;
+            case GX_CALL_LOOKUP_ARRAY: case GX_CALL_LOOKUP_PT: case GX_CALL_LOOKUP_HASH:
+                if (!(g.flags & GXF_KEY_MAPV)) slots.insert(g.off >> 3);
+                break;
+            case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: case GX_CALL_UPDATE_HASH: {
+                if (!(g.flags & GXF_KEY_MAPV)) slots.insert(g.off >> 3);
+                if (!(g.flags & GXF_VAL_MAPV)) {
+                    const uint32_t vs = L.maps[g.aux].value_size;
+                    for (uint32_t w = 0; w < vs / 8; w++) slots.insert((int)((uint32_t)g.imm / 8 + w));
+                }
+                break;
+            }
+            case GX_CALL_RINGBUF_OUTPUT:
+                if (!(g.flags & GXF_VAL_MAPV)) {
+                    const uint32_t size = (uint32_t)g.imm;
+                    for (uint32_t w = 0; w < (size + 7) / 8; w++) slots.insert((int)((uint16_t)g.off / 8 + w));
+                }
+                break;
+            default: break;
+            }
+        }
+        o << "__device__ __forceinline__ uint64_t prog" << q
+          << "(const Ctx &c, const uint32_t shard, uint32_t *spriv, unsigned long long &c_herr, "
+             "unsigned long long &c_drop, unsigned long long &c_rbb, unsigned long long &c_hfull) {\n";
+        o << "  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0, r8 = 0, r9 = 0;\n"
+             "  const uint64_t r10 = 512;\n  (void)r10; (void)spriv; (void)shard;\n";
+        for (int s : slots) o << "  uint64_t s" << s << " = 0;\n";
+        for (uint32_t i = 0; i < n; i++) {
+            if (targets.count(i)) o << " L" << i << ":\n";
+            insn(im[i], i);
+        }
+        o << "  return r0;\n}\n\n";
+    }
+
+    std::string src_operand(const GxInsn &g, bool is64) {
+        if (g.flags & GXF_X) return is64 ? R(g.src) : "(uint32_t)" + R(g.src);
+        return is64 ? hex(g.imm) : hex((uint32_t)g.imm);
+    }
+
+    void insn(const GxInsn &g, uint32_t i) {
+        const std::string d = R(g.dst), s = R(g.src);
+        const std::string S64 = src_operand(g, true), S32 = src_operand(g, false);
+        auto st = [&](const std::string &x) { o << "  " << x << "\n"; };
+        const bool sxf = g.flags & GXF_SX;
+        const unsigned lg = g.aux & 15;
+        auto ld_fix = [&](const std::string &v) {
+            return sxf ? "sx(" + v + ", " + std::to_string(8u << lg) + ")" : v;
+        };
+        auto branch_cond = [&](const std::string &cond, uint32_t tgt) { st("if (" + cond + ") goto L" + std::to_string(tgt) + ";"); };
+        switch (g.op) {
+        case GX_ADD64: st(d + " += " + S64 + ";"); break;
+        case GX_SUB64: st(d + " -= " + S64 + ";"); break;
+        case GX_MUL64: st(d + " *= " + S64 + ";"); break;
+        case GX_DIV64: st("{ const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " / t : 0; }"); break;
+        case GX_MOD64: st("{ const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " % t : " + d + "; }"); break;
+        case GX_SDIV64:
+            st("{ const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
+               " = t == 0 ? 0 : (a == (int64_t)0x8000000000000000ll && t == -1) ? (uint64_t)a : (uint64_t)(a / t); }");
+            break;
+        case GX_SMOD64:
+            st("{ const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
+               " = t == 0 ? (uint64_t)a : t == -1 ? 0 : (uint64_t)(a % t); }");
+            break;
+        case GX_OR64: st(d + " |= " + S64 + ";"); break;
+        case GX_AND64: st(d + " &= " + S64 + ";"); break;
+        case GX_XOR64: st(d + " ^= " + S64 + ";"); break;
+        case GX_LSH64: st(d + " <<= (" + S64 + " & 63);"); break;
+        case GX_RSH64: st(d + " >>= (" + S64 + " & 63);"); break;
+        case GX_ARSH64: st(d + " = (uint64_t)((int64_t)" + d + " >> (" + S64 + " & 63));"); break;
+        case GX_NEG64: st(d + " = 0 - " + d + ";"); break;
+        case GX_MOV64: st(d + " = " + S64 + ";"); break;
+        case GX_MOVSX64: st(d + " = sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_ADD32: st(d + " = (uint32_t)((uint32_t)" + d + " + " + S32 + ");"); break;
+        case GX_SUB32: st(d + " = (uint32_t)((uint32_t)" + d + " - " + S32 + ");"); break;
+        case GX_MUL32: st(d + " = (uint32_t)((uint32_t)" + d + " * " + S32 + ");"); break;
+        case GX_DIV32: st("{ const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " / t : 0; }"); break;
+        case GX_MOD32: st("{ const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " % t : (uint32_t)" + d + "; }"); break;
+        case GX_SDIV32:
+            st("{ const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
+               " = (uint32_t)(t == 0 ? 0 : (a == (int32_t)0x80000000 && t == -1) ? a : a / t); }");
+            break;
+        case GX_SMOD32:
+            st("{ const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
+               " = (uint32_t)(t == 0 ? a : t == -1 ? 0 : a % t); }");
+            break;
+        case GX_OR32: st(d + " = (uint32_t)" + d + " | " + S32 + ";"); break;
+        case GX_AND32: st(d + " = (uint32_t)" + d + " & " + S32 + ";"); break;
+        case GX_XOR32: st(d + " = (uint32_t)" + d + " ^ " + S32 + ";"); break;
+        case GX_LSH32: st(d + " = (uint32_t)((uint32_t)" + d + " << (" + S32 + " & 31));"); break;
+        case GX_RSH32: st(d + " = (uint32_t)" + d + " >> (" + S32 + " & 31);"); break;
+        case GX_ARSH32: st(d + " = (uint32_t)((int32_t)" + d + " >> (" + S32 + " & 31));"); break;
+        case GX_NEG32: st(d + " = (uint32_t)(0u - (uint32_t)" + d + ");"); break;
+        case GX_MOV32: st(d + " = (uint32_t)(" + S32 + ");"); break;
+        case GX_MOVSX32: st(d + " = (uint32_t)sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_LE:
+            if (g.aux < 64) st(d + " &= " + hex((1ull << g.aux) - 1) + ";");
+            break;
+        case GX_BE: st(d + " = bswap_w(" + d + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_LDIMM:
+            if (g.flags & GXF_VAL_MAPV) st(d + " = " + hex(L.maps[g.aux].data + g.imm) + ";");
+            else st(d + " = " + hex(g.imm) + ";");
+            break;
+        case GX_JA: st("goto L" + std::to_string(g.aux) + ";"); break;
+        case GX_EXIT: st(std::string("return ") + ((g.flags & GXF_SX) ? hex(g.imm) : "r0") + ";"); break;
+        case GX_LDX_CTX: st(d + " = " + ld_fix("ctx_ld(c, " + std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";"); break;
+        case GX_LDX_STACK:
+            st(d + " = " + ld_fix("zx(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ", " + std::to_string(lg) + ")") + ";");
+            break;
+        case GX_LDX_MAP: {
+            const bool coh = L.maps[g.imm].coherent;
+            st(d + " = " + ld_fix(std::string("gload<") + (coh ? "true" : "false") + ">(" + s + " + (int64_t)" +
+                                  std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";");
+            break;
+        }
+        case GX_LDX_PT:
+            st(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
+                                  std::to_string(g.off) + ", shard), " + std::to_string(lg) + ")") + ";");
+            break;
+        case GX_ST_STACK: {
+            const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
+            st(slot(g.off) + " = word_set(" + slot(g.off) + ", " + std::to_string(g.off & 7) + ", " + std::to_string(lg) + ", " + v + ");");
+            break;
+        }
+        case GX_ST_MAP: {
+            const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
+            st("gstore(" + d + " + (int64_t)" + std::to_string(g.off) + ", " + std::to_string(lg) + ", " + v + ");");
+            break;
+        }
+        case GX_ST_PT: {
+            const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
+            st("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
+               ", shard), " + std::to_string(lg) + ", " + v + ");");
+            break;
+        }
+        case GX_ATOM_STACK: case GX_ATOM_PT: case GX_ATOM_MAP: atomic(g); break;
+        case GX_CALL_LOOKUP_ARRAY: case GX_CALL_LOOKUP_PT: case GX_CALL_LOOKUP_HASH: {
+            const GxMapDesc &m = L.maps[g.aux];
+            std::string key;
+            if (g.op == GX_CALL_LOOKUP_HASH) {
+                key = (g.flags & GXF_KEY_MAPV)
+                          ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
+                          : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+                if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
+                st("r0 = (uint64_t)gxd::hash_find(" + md(g.aux) + ", " + key + ");");
+            } else {
+                key = (g.flags & GXF_KEY_MAPV) ? "*(const uint32_t *)r2"
+                                               : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+                st("{ const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
+                   " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0; }");
+            }
+            if (g.flags & GXF_FETCH) branch_cond("r0 == 0", (uint32_t)g.imm);
+            if (g.flags & GXF_W32) branch_cond("r0 != 0", (uint32_t)g.imm);
+            break;
+        }
+        case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: {
+            const GxMapDesc &m = L.maps[g.aux];
+            const std::string key = (g.flags & GXF_KEY_MAPV)
+                                        ? "*(const uint32_t *)r2"
+                                        : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+            std::ostringstream b;
+            b << "{ const uint32_t k = " << key << "; int64_t rc = 0;\n"
+              << "    if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17;\n"
+              << "    else {\n";
+            for (uint32_t w = 0; w < m.value_size / 8; w++) {
+                const std::string v = (g.flags & GXF_VAL_MAPV) ? "((const uint64_t *)r3)[" + std::to_string(w) + "]"
+                                                               : "s" + std::to_string((uint32_t)g.imm / 8 + w);
+                const std::string logical = hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u + " +
+                                            std::to_string(8 * w);
+                if (g.op == GX_CALL_UPDATE_ARRAY) b << "      *(uint64_t *)(" << logical << ") = " << v << ";\n";
+                else b << "      *(uint64_t *)gxd::pt_phys(" << md(g.aux) << ", " << logical << ", shard) = " << v << ";\n";
+            }
+            b << "    }\n    if (rc) c_herr++; r0 = (uint64_t)rc; }";
+            st(b.str());
+            break;
+        }
+        case GX_CALL_UPDATE_HASH: {
+            const GxMapDesc &m = L.maps[g.aux];
+            std::string key = (g.flags & GXF_KEY_MAPV)
+                                  ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
+                                  : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+            if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
+            const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
+            st("{ bool full; const int64_t rc = gxd::hash_update(" + md(g.aux) + ", " + key + ", " + v +
+               ", r4, full); if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
+            break;
+        }
+        case GX_CALL_RINGBUF_OUTPUT: {
+            const uint32_t size = (uint32_t)g.imm, flags = (uint32_t)(g.imm >> 32);
+            if (flags > 2) {
+                st("r0 = (uint64_t)(int64_t)-22; c_herr++;");
+                break;
+            }
+            std::ostringstream b;
+            b << "{ ";
+            if (g.flags & GXF_VAL_MAPV) b << "const uint64_t *w = (const uint64_t *)r2;";
+            else {
+                b << "const uint64_t w[" << (size + 7) / 8 << "] = {";
+                for (uint32_t k = 0; k < (size + 7) / 8; k++) b << (k ? ", " : "") << "s" << ((uint16_t)g.off / 8 + k);
+                b << "};";
+            }
+            b << " r0 = (uint64_t)ringbuf_output(" << md(g.aux) << ", w, " << size << "u, c_drop, c_rbb);"
+              << " if (r0) c_herr++; }";
+            st(b.str());
+            break;
+        }
+        case GX_OP_NOP: st("{ c_herr++; return 0; }"); break;
+        default:
+            if (g.op >= GX_JEQ && g.op <= GX_JSET32) {
+                const bool is32 = g.op >= GX_JEQ32;
+                const int cop = is32 ? g.op - (GX_JEQ32 - GX_JEQ) : g.op;
+                std::string a = is32 ? "(uint32_t)" + d : d;
+                std::string b = is32 ? S32 : S64;
+                std::string sa = is32 ? "(int32_t)" + d : "(int64_t)" + d;
+                std::string sb = is32 ? "(int32_t)(" + S32 + ")" : "(int64_t)(" + S64 + ")";
+                std::string c;
+                switch (cop) {
+                case GX_JEQ: c = a + " == " + b; break;
+                case GX_JNE: c = a + " != " + b; break;
+                case GX_JGT: c = a + " > " + b; break;
+                case GX_JGE: c = a + " >= " + b; break;
+                case GX_JLT: c = a + " < " + b; break;
+                case GX_JLE: c = a + " <= " + b; break;
+                case GX_JSGT: c = sa + " > " + sb; break;
+                case GX_JSGE: c = sa + " >= " + sb; break;
+                case GX_JSLT: c = sa + " < " + sb; break;
+                case GX_JSLE: c = sa + " <= " + sb; break;
+                default: c = "(" + a + " & " + b + ") != 0"; break;
+                }
+                branch_cond(c, g.aux);
+            } else {
+                st("{ c_herr++; return 0; }");
+            }
+        }
+        (void)i;
+    }
+
+    void atomic(const GxInsn &g) {
+        const uint32_t op = (uint32_t)(g.imm & 0xFF);
+        const bool w32 = (g.aux & 15) == 2, fetch = op & 1, kop = g.flags & GXF_PRIV;
+        const std::string v = kop ? hex((uint64_t)(int64_t)(int32_t)(g.imm >> 32)) : R(g.src);
+        const std::string ret = op == 0xF1 ? "r0" : R(g.src);
+        auto st = [&](const std::string &x) { o << "  " << x << "\n"; };
+        if (g.op == GX_ATOM_STACK) {
+            std::string e = "rmw_word(" + slot(g.off) + ", " + std::to_string(g.off & 7) + ", " + (w32 ? "true" : "false") +
+                            ", " + std::to_string(op) + "u, " + v + ", r0)";
+            st(fetch ? "{ const uint64_t old = " + e + "; " + ret + " = old; }" : "(void)" + e + ";");
+            return;
+        }
+        const int fd = g.aux >> 4;
+        const std::string addr = R(g.dst) + " + (int64_t)" + std::to_string(g.off);
+        if (g.op == GX_ATOM_PT) {
+            std::string e = "rmw_global_private((uint64_t)gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
+                            (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
+            st(fetch ? "{ const uint64_t old = " + e + "; " + ret + " = old; }" : "(void)" + e + ";");
+            return;
+        }
+        /* shared map value */
+        if (op == 0xE1) {
+            st(R(g.src) + " = " + (w32 ? "atomicExch((unsigned *)(" + addr + "), (uint32_t)" + v + ")"
+                                       : "atomicExch((unsigned long long *)(" + addr + "), " + v + ")") + ";");
+            return;
+        }
+        if (op == 0xF1) {
+            st("r0 = " + (w32 ? "atomicCAS((unsigned *)(" + addr + "), (uint32_t)r0, (uint32_t)" + v + ")"
+                               : "atomicCAS((unsigned long long *)(" + addr + "), r0, " + v + ")") + ";");
+            return;
+        }
+        const GxMapDesc &m = L.maps[fd];
+        if (m.priv_off != 0xFFFFFFFFu && !fetch && (op & 0xF0) == 0 && !w32) {
+            const uint32_t nw = m.max_entries * m.value_size / 8;
+            st("priv_add(spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
+               ", (uint32_t)((" + addr + " - " + hex(m.data) + ") >> 3), " + v + ");");
+            return;
+        }
+        std::string e = "warp_atomic<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
+                        (fetch ? "true" : "false") + ">(" + addr + ", " + v + ")";
+        st(fetch ? R(g.src) + " = " + e + ";" : "(void)" + e + ";");
+    }
+
+    void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+        o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
+        for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
+        const uint32_t priv_words = (L.priv_bytes + 3) / 4;
+        o << "extern \"C\" __global__ void __launch_bounds__(256) gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
+             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
+        o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
+             "  __shared__ unsigned long long sstats[8];\n"
+             "  for (uint32_t k = threadIdx.x; k < " << priv_words << "u; k += 256) spriv[k] = 0;\n"
+             "  if (threadIdx.x < 8) sstats[threadIdx.x] = 0;\n"
+             "  __syncthreads();\n"
+             "  const uint32_t shard = blockIdx.x * 256 + threadIdx.x;\n"
+             "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
+             "  const uint64_t stride = (uint64_t)gridDim.x * 256;\n"
+             "  uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;\n"
+             "  uint4 na = make_uint4(0, 0, 0, 0), nb = na;\n"
+             "  if (i < n) { na = ldg_stream(ev + 2 * i); nb = ldg_stream(ev + 2 * i + 1); }\n"
+             "  for (; i < n; i += stride) {\n"
+             "    const uint4 a = na, b = nb;\n"
+             "    if (i + stride < n) { na = ldg_stream(ev + 2 * (i + stride)); nb = ldg_stream(ev + 2 * (i + stride) + 1); }\n"
+             "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n";
+        if (L.single >= 0) {
+            o << "    const int p = 0;\n";
+        } else {
+            o << "    int p = -1;\n    { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
+            for (int k = 0; k < GX_MAX_KINDS; k++)
+                for (int t = 0; t < 256; t++)
+                    if (L.attach[k][t] >= 0) o << "      case " << k * 256 + t << ": p = " << (int)L.attach[k][t] << "; break;\n";
+            o << "      default: break;\n      }\n    }\n";
+        }
+        o << "    uint64_t r = 0;\n    switch (p) {\n";
+        for (size_t q = 0; q < images.size(); q++)
+            o << "    case " << q << ": r = prog" << q << "(c, shard, spriv, c_herr, c_drop, c_rbb, c_hfull); c_run++; break;\n";
+        o << "    default: c_skip++; break;\n    }\n"
+             "    if (ret) ret[i] = r;\n  }\n";
+        o << "  for (int s = 16; s; s >>= 1) {\n"
+             "    c_run += __shfl_xor_sync(0xFFFFFFFFu, c_run, s); c_skip += __shfl_xor_sync(0xFFFFFFFFu, c_skip, s);\n"
+             "    c_herr += __shfl_xor_sync(0xFFFFFFFFu, c_herr, s); c_drop += __shfl_xor_sync(0xFFFFFFFFu, c_drop, s);\n"
+             "    c_rbb += __shfl_xor_sync(0xFFFFFFFFu, c_rbb, s); c_hfull += __shfl_xor_sync(0xFFFFFFFFu, c_hfull, s);\n"
+             "  }\n"
+             "  if ((threadIdx.x & 31) == 0) {\n"
+             "    if (c_run) atomicAdd(&sstats[" << GXS_RUN << "], c_run);\n"
+             "    if (c_skip) atomicAdd(&sstats[" << GXS_SKIP << "], c_skip);\n"
+             "    if (c_herr) atomicAdd(&sstats[" << GXS_HERR << "], c_herr);\n"
+             "    if (c_drop) atomicAdd(&sstats[" << GXS_RB_DROPS << "], c_drop);\n"
+             "    if (c_rbb) atomicAdd(&sstats[" << GXS_RB_BYTES << "], c_rbb);\n"
+             "    if (c_hfull) atomicAdd(&sstats[" << GXS_HFULL << "], c_hfull);\n"
+             "  }\n"
+             "  __syncthreads();\n";
+        for (uint32_t k = 0; k < L.n_priv; k++) {
+            const GxMapDesc &m = L.maps[L.priv_maps[k]];
+            const uint32_t nw = m.max_entries * m.value_size / 8;
+            o << "  for (uint32_t w = threadIdx.x; w < " << nw << "u; w += 256) {\n"
+              << "    const uint64_t v = (uint64_t)spriv[" << m.priv_off / 4 << " + w] | ((uint64_t)spriv["
+              << m.priv_off / 4 + nw << " + w] << 32);\n"
+              << "    if (v) atomicAdd((unsigned long long *)" << hex(m.data) << " + w, (unsigned long long)v);\n  }\n";
+        }
+        o << "  if (threadIdx.x < 8 && sstats[threadIdx.x]) atomicAdd(&gstats[threadIdx.x], sstats[threadIdx.x]);\n}\n";
+    }
+};
+
+}  // namespace
+
+std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+    Gen g(L);
+    g.kernel(images, sizes);
+    return g.o.str();
+}
+
+int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
+    Nvrtc &nv = nvrtc();
+    if (!nv.ok) {
+        log = nv.err;
+        return -1;
+    }
+    std::vector<const char *> names, texts;
+    for (int k = 0; kJitHeaders[k].name; k++) {
+        names.push_back(kJitHeaders[k].name);
+        texts.push_back(kJitHeaders[k].text);
+    }
+    nvrtcProgram prog;
+    nvrtcResult r = nv.create(&prog, src.c_str(), "gx_jit.cu", (int)names.size(), texts.data(), names.data());
+    if (r != NVRTC_SUCCESS) {
+        log = nv.errstr(r);
+        return -1;
+    }
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DGX_JIT=1", "-w"};
+    r = nv.compile(prog, (int)(sizeof opts / sizeof *opts), opts);
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    log.assign(ls, 0);
+    if (ls) nv.log(prog, &log[0]);
+    if (r != NVRTC_SUCCESS) {
+        nv.destroy(&prog);
+        return -1;
+    }
+    size_t cs = 0;
+    nv.cubin_size(prog, &cs);
+    cubin.resize(cs);
+    nv.cubin(prog, cubin.data());
+    nv.destroy(&prog);
+    return 0;
+}

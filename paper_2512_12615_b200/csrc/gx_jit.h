@@ -1,0 +1,12 @@
+/* gx_jit.h -- internal interface of the per-launch JIT (gx_jit.cpp). */
+#pragma once
+#include <string>
+#include <vector>
+
+#include "gx_internal.h"
+
+/* CUDA C++ source of one launch configuration (programs in launch-slot order). */
+std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images,
+                          const std::vector<uint32_t> &sizes);
+/* NVRTC -> sm_100a cubin.  Returns 0, or -1 with the compiler log. */
+int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string &log);

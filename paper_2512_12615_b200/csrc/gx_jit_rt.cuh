@@ -1,0 +1,236 @@
+/*
+ * gx_jit_rt.cuh -- device runtime for JIT-compiled gx programs.
+ *
+ * "Verified programs are JIT-compiled into ... GPU-compatible instructions (e.g., PTX)"
+ * (§4.2); "we inline helper functions and map accesses to reduce call overhead"
+ * (§5.3).  gx_jit.cpp translates the verifier's pre-decoded image into straight-line
+ * CUDA C++ (eBPF registers become SSA values in GPU registers, the stack becomes constant-indexed
+ * registers, branches become branches) and NVRTC compiles it for sm_100a together with this
+ * header.  One thread runs one event; SIMT divergence is the hardware's (independent thread
+ * scheduling reconverges at post-dominators), so the interpreter's uniform-PC / min-PC machinery
+ * is not needed here.  Helpers keep the interpreter's semantics: warp-aggregated map atomics over
+ * the lanes that execute the atomic together (__activemask + __match_any_sync + __reduce_*_sync),
+ * shared-memory privatised ADD accumulators, one ringbuf reservation per converged warp.
+ * Included only by NVRTC-compiled sources.
+ */
+#pragma once
+#include "gx_device.cuh"
+#include "gx_internal.h"
+
+namespace gxj {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t sx(uint64_t v, unsigned bits) {
+    if (bits >= 64) return v;
+    const uint64_t m = 1ull << (bits - 1);
+    v &= (1ull << bits) - 1;
+    return (v ^ m) - m;
+}
+__device__ __forceinline__ uint64_t zx(uint64_t v, unsigned lg) { return lg >= 3 ? v : v & ((1ull << (8u << lg)) - 1); }
+
+/* the 32-B event record lives in 8 u32 registers; offsets are compile-time constants */
+struct Ctx {
+    uint32_t w[8];
+};
+__device__ __forceinline__ uint64_t ctx_ld(const Ctx &c, int off, unsigned lg) {
+    const int wi = off >> 2;
+    uint64_t v = (uint64_t)c.w[wi] | (wi + 1 < 8 ? (uint64_t)c.w[wi + 1] << 32 : 0ull);
+    return zx(v >> (8 * (off & 3)), lg);
+}
+
+__device__ __forceinline__ uint64_t bswap_w(uint64_t v, unsigned w) {
+    uint64_t r = __byte_perm((uint32_t)(v >> 32), 0, 0x0123) | ((uint64_t)__byte_perm((uint32_t)v, 0, 0x0123) << 32);
+    return w == 64 ? r : (r >> (64 - w));
+}
+
+__device__ __forceinline__ uint64_t word_set(uint64_t w, unsigned byte, unsigned lg, uint64_t v) {
+    if (lg >= 3) return v;
+    const uint64_t msk = ((1ull << (8u << lg)) - 1) << (8 * byte);
+    return (w & ~msk) | ((v << (8 * byte)) & msk);
+}
+
+template <bool COHERENT>
+__device__ __forceinline__ uint64_t gload(uint64_t a, unsigned lg) {
+    switch (lg) {
+    case 0: return *reinterpret_cast<const volatile uint8_t *>(a);
+    case 1: return *reinterpret_cast<const volatile uint16_t *>(a);
+    case 2: return COHERENT ? *reinterpret_cast<const volatile uint32_t *>(a) : *reinterpret_cast<const uint32_t *>(a);
+    default: return COHERENT ? gxd::ld_relaxed(reinterpret_cast<const uint64_t *>(a)) : *reinterpret_cast<const uint64_t *>(a);
+    }
+}
+__device__ __forceinline__ void gstore(uint64_t a, unsigned lg, uint64_t v) {
+    switch (lg) {
+    case 0: *reinterpret_cast<uint8_t *>(a) = (uint8_t)v; break;
+    case 1: *reinterpret_cast<uint16_t *>(a) = (uint16_t)v; break;
+    case 2: *reinterpret_cast<uint32_t *>(a) = (uint32_t)v; break;
+    default: *reinterpret_cast<uint64_t *>(a) = v; break;
+    }
+}
+
+/* plain RMW of a private word (stack slot or per-thread shard): returns old, stores new */
+__device__ __forceinline__ uint64_t rmw_word(uint64_t &w, unsigned byte, bool w32, uint32_t op, uint64_t s, uint64_t r0) {
+    const uint64_t old = w32 ? (w >> (8 * byte)) & 0xFFFFFFFFull : w;
+    const uint64_t m = w32 ? 0xFFFFFFFFull : ~0ull;
+    s &= m;
+    uint64_t nv;
+    switch (op) {
+    case 0x00: case 0x01: nv = old + s; break;
+    case 0x40: case 0x41: nv = old | s; break;
+    case 0x50: case 0x51: nv = old & s; break;
+    case 0xA0: case 0xA1: nv = old ^ s; break;
+    case 0xE1: nv = s; break;
+    default: nv = (old == (r0 & m)) ? s : old; break;
+    }
+    nv &= m;
+    w = w32 ? ((w & ~(0xFFFFFFFFull << (8 * byte))) | (nv << (8 * byte))) : nv;
+    return old;
+}
+__device__ __forceinline__ uint64_t rmw_global_private(uint64_t a, bool w32, uint32_t op, uint64_t s, uint64_t r0) {
+    uint64_t *w = reinterpret_cast<uint64_t *>(a & ~7ull);
+    uint64_t v = *w;
+    const uint64_t old = rmw_word(v, (unsigned)(a & 7), w32, op, s, r0);
+    *w = v;
+    return old;
+}
+
+__device__ __forceinline__ uint64_t apply_op(uint32_t op, uint64_t a, uint64_t b) {
+    switch (op & 0xF0) {
+    case 0x00: return a + b;
+    case 0x40: return a | b;
+    case 0x50: return a & b;
+    default: return a ^ b;
+    }
+}
+__device__ __forceinline__ uint64_t group_sum64(unsigned mask, uint64_t v) {
+    if (__all_sync(mask, v < (1ull << 27))) return __reduce_add_sync(mask, (uint32_t)v);
+    uint64_t s0 = __reduce_add_sync(mask, (uint32_t)(v & 0xFFFF));
+    uint64_t s1 = __reduce_add_sync(mask, (uint32_t)((v >> 16) & 0xFFFF));
+    uint64_t s2 = __reduce_add_sync(mask, (uint32_t)((v >> 32) & 0xFFFF));
+    uint64_t s3 = __reduce_add_sync(mask, (uint32_t)(v >> 48));
+    return s0 + (s1 << 16) + (s2 << 32) + (s3 << 48);
+}
+__device__ __forceinline__ uint64_t group_reduce(unsigned mask, uint32_t op, uint64_t v, bool w32) {
+    if (w32) {
+        const uint32_t x = (uint32_t)v;
+        switch (op & 0xF0) {
+        case 0x00: return __reduce_add_sync(mask, x);
+        case 0x40: return __reduce_or_sync(mask, x);
+        case 0x50: return __reduce_and_sync(mask, x);
+        default: return __reduce_xor_sync(mask, x);
+        }
+    }
+    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+    switch (op & 0xF0) {
+    case 0x00: return group_sum64(mask, v);
+    case 0x40: return __reduce_or_sync(mask, lo) | ((uint64_t)__reduce_or_sync(mask, hi) << 32);
+    case 0x50: return __reduce_and_sync(mask, lo) | ((uint64_t)__reduce_and_sync(mask, hi) << 32);
+    default: return __reduce_xor_sync(mask, lo) | ((uint64_t)__reduce_xor_sync(mask, hi) << 32);
+    }
+}
+__device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, uint64_t v, bool w32, bool fetch) {
+    if (w32) {
+        unsigned *p = reinterpret_cast<unsigned *>(addr);
+        const uint32_t x = (uint32_t)v;
+        switch (op & 0xF0) {
+        case 0x00: if (!fetch) { atomicAdd(p, x); return 0; } return atomicAdd(p, x);
+        case 0x40: return atomicOr(p, x);
+        case 0x50: return atomicAnd(p, x);
+        default: return atomicXor(p, x);
+        }
+    }
+    unsigned long long *p = reinterpret_cast<unsigned long long *>(addr);
+    switch (op & 0xF0) {
+    case 0x00: if (!fetch) { atomicAdd(p, v); return 0; } return atomicAdd(p, v);
+    case 0x40: return atomicOr(p, v);
+    case 0x50: return atomicAnd(p, v);
+    default: return atomicXor(p, v);
+    }
+}
+
+/* Warp-aggregated atomic on a shared map value (ADD/OR/AND/XOR, +-FETCH) among the lanes that
+ * execute it together: one L2 atomic per distinct address; FETCH lanes get old + the exclusive
+ * prefix of their address group in lane order (a valid linearisation). */
+template <uint32_t OP, bool W32, bool FETCH>
+__device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
+    const unsigned act = __activemask();
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(act, addr);
+    const unsigned leader = __ffs(peers) - 1;
+    if (!FETCH) {
+        const uint64_t agg = group_reduce(peers, OP, v, W32);
+        if (lane == leader) global_atomic(OP, addr, agg, W32, false);
+        return 0;
+    }
+    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    uint64_t pre = ident, tot = ident;
+    for (unsigned m = peers; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const uint64_t vj = __shfl_sync(peers, v, j);
+        if (j < (int)lane) pre = apply_op(OP, pre, vj);
+        tot = apply_op(OP, tot, vj);
+    }
+    uint64_t old = 0;
+    if (lane == leader) old = global_atomic(OP, addr, tot, W32, true);
+    old = __shfl_sync(peers, old, leader);
+    const uint64_t r = apply_op(OP, old, pre);
+    return W32 ? (uint32_t)r : r;
+}
+
+/* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory */
+__device__ __forceinline__ void priv_add(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, w);
+    const uint64_t agg = group_sum64(peers, v);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) {
+        const uint32_t old = atomicAdd(&lo[w], (uint32_t)agg);
+        const uint32_t carry = ((uint32_t)(old + (uint32_t)agg) < old) ? 1u : 0u;
+        const uint32_t h = (uint32_t)(agg >> 32) + carry;
+        if (h) atomicAdd(&hi[w], h);
+    }
+}
+
+/* one ringbuf reservation per converged group of lanes; returns 0 or -EAGAIN */
+__device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uint64_t *words, uint32_t size,
+                                                  unsigned long long &drops, unsigned long long &bytes) {
+    const unsigned act = __activemask();
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t recb = (8 + size + 7) & ~7u;
+    const uint32_t cnt = __popc(act), rank = __popc(act & ((1u << lane) - 1));
+    const uint32_t leader = __ffs(act) - 1;
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(md.aux);
+    uint64_t base = 0;
+    if (lane == leader) base = atomicAdd(&ctr[0], (unsigned long long)(cnt * recb));
+    base = __shfl_sync(act, base, leader);
+    const uint64_t o = base + rank * recb;
+    const bool ok = o + recb <= (uint64_t)md.cap_mask + 1;
+    if (ok) {
+        uint64_t *dst = reinterpret_cast<uint64_t *>(md.data + o);
+        dst[0] = (uint64_t)size | ((o >> 12) << 32);
+        const uint32_t nw = (size + 7) / 8;
+        for (uint32_t w = 0; w < nw; w++) {
+            uint64_t v = words[w];
+            if (w == nw - 1 && (size & 7)) v &= (1ull << (8 * (size & 7))) - 1;
+            dst[1 + w] = v;
+        }
+    } else {
+        drops++;
+    }
+    const uint32_t nok = __popc(__ballot_sync(act, ok));
+    if (nok && lane == leader) {
+        atomicAdd(&ctr[1], (unsigned long long)(nok * recb));
+        bytes += nok * recb;
+    }
+    return ok ? 0 : -(int64_t)gxd::E_AGAIN;
+}
+
+}  // namespace gxj

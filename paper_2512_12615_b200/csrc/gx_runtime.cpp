@@ -20,7 +20,11 @@
 
 #include "../../include/gx.h"
 #include "gx_internal.h"
+#include "gx_jit.h"
 #include "gx_verifier.h"
+
+#include <cuda.h>
+#include <chrono>
 
 extern "C" {
 int gx_launch_exec(const GxLaunch *d_launch, const void *d_events, uint64_t n, uint64_t *d_ret, uint32_t grid,
@@ -82,9 +86,46 @@ struct LaunchKey {
 
 struct LaunchCfg {
     GxLaunch *d = nullptr;
+    GxLaunch h;              /* host copy (the JIT bakes it into the generated kernel) */
+    std::vector<int> progs;  /* launch slot -> prog fd */
     uint32_t smem = 0;
     uint32_t grid = 0;
+    /* JIT engine */
+    bool jit_tried = false;
+    CUmodule jmod = nullptr;
+    CUfunction jfunc = nullptr;
+    uint32_t jgrid = 0;
+    std::string jit_log;
+    double jit_ms = 0;
 };
+
+/* driver entry points through the runtime (no link-time dependency on libcuda) */
+struct Drv {
+    bool ok = false;
+    CUresult (*moduleLoadData)(CUmodule *, const void *) = nullptr;
+    CUresult (*moduleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
+    CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void **, void **) = nullptr;
+    CUresult (*occupancy)(int *, CUfunction, int, size_t) = nullptr;
+    CUresult (*moduleUnload)(CUmodule) = nullptr;
+};
+Drv &drv() {
+    static Drv d;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        cudaDriverEntryPointQueryResult q;
+        bool ok = true;
+        ok &= cudaGetDriverEntryPoint("cuModuleLoadData", (void **)&d.moduleLoadData, cudaEnableDefault, &q) == cudaSuccess;
+        ok &= cudaGetDriverEntryPoint("cuModuleGetFunction", (void **)&d.moduleGetFunction, cudaEnableDefault, &q) == cudaSuccess;
+        ok &= cudaGetDriverEntryPoint("cuLaunchKernel", (void **)&d.launchKernel, cudaEnableDefault, &q) == cudaSuccess;
+        ok &= cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void **)&d.occupancy,
+                                      cudaEnableDefault, &q) == cudaSuccess;
+        ok &= cudaGetDriverEntryPoint("cuModuleUnload", (void **)&d.moduleUnload, cudaEnableDefault, &q) == cudaSuccess;
+        d.ok = ok && d.moduleLoadData && d.moduleGetFunction && d.launchKernel;
+    }
+    return d;
+}
 
 }  // namespace
 
@@ -99,6 +140,7 @@ struct gx_rt {
     std::map<LaunchKey, LaunchCfg> launches;
     unsigned long long *d_stats = nullptr;
     uint32_t last_grid = 0, last_block = 0, last_smem = 0;
+    int engine = GX_ENGINE_JIT;
     uint64_t n_launches = 0;
     std::string err;
     /* gx_run_batch_host pipeline */
@@ -238,10 +280,73 @@ int get_launch(gx_rt *rt, int prog_fd, LaunchCfg *&out) {
     if (e) return cuda_err(rt, (cudaError_t)e, "occupancy");
     if (bps < 1) return set_err(rt, -E2BIG, "executor does not fit on an SM (%u B shared)", cfg.smem);
     cfg.grid = (uint32_t)rt->nsm * (uint32_t)std::min<int>(bps, (int)kBlocksPerSmMax);
+    cfg.h = h;
+    cfg.progs = plist;
     CK(cudaMalloc(&cfg.d, sizeof(GxLaunch)), "cudaMalloc launch");
     CK(cudaMemcpy(cfg.d, &h, sizeof h, cudaMemcpyHostToDevice), "cudaMemcpy launch");
     auto res = rt->launches.emplace(key, cfg);
     out = &res.first->second;
+    return 0;
+}
+
+/* compiles (once) the JIT kernel of a launch configuration */
+int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
+    if (cfg.jfunc) return 0;
+    if (cfg.jit_tried) return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
+    cfg.jit_tried = true;
+    Drv &d = drv();
+    if (!d.ok) {
+        cfg.jit_log = "driver entry points unavailable";
+        return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<const GxInsn *> images;
+    std::vector<uint32_t> sizes;
+    for (int q : cfg.progs) {
+        images.push_back(rt->progs[q].vr.image.data());
+        sizes.push_back((uint32_t)rt->progs[q].vr.image.size());
+    }
+    std::string src = gx_jit_source(cfg.h, images, sizes);
+    if (const char *dump = getenv("GX_JIT_DUMP")) {
+        if (FILE *f = fopen(dump, "w")) {
+            fputs(src.c_str(), f);
+            fclose(f);
+        }
+    }
+    std::vector<char> cubin;
+    if (gx_jit_compile(src, cubin, cfg.jit_log)) return set_err(rt, -ENOSYS, "JIT compile failed: %s", cfg.jit_log.c_str());
+    if (d.moduleLoadData(&cfg.jmod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
+    if (d.moduleGetFunction(&cfg.jfunc, cfg.jmod, "gx_jit_kernel") != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
+    int bps = 0;
+    if (!d.occupancy || d.occupancy(&bps, cfg.jfunc, 256, 0) != CUDA_SUCCESS || bps < 1) bps = 4;
+    bps = std::min(bps, 8);
+    cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
+    cfg.jit_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+}
+
+int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream) {
+    if (rt->engine == GX_ENGINE_JIT) {
+        int rc = jit_prepare(rt, cfg);
+        if (rc) return rc;
+        const void *ev = d_events;
+        uint64_t nn = n;
+        uint64_t *rp = d_ret;
+        unsigned long long *st = rt->d_stats;
+        void *args[] = {(void *)&ev, (void *)&nn, (void *)&rp, (void *)&st};
+        if (drv().launchKernel(cfg.jfunc, cfg.jgrid, 1, 1, 256, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
+            return set_err(rt, -EFAULT, "JIT kernel launch failed");
+        rt->last_grid = cfg.jgrid;
+        rt->last_block = 256;
+        rt->last_smem = 0;
+    } else {
+        int e = gx_launch_exec(cfg.d, d_events, n, d_ret, cfg.grid, cfg.smem, stream);
+        if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");
+        rt->last_grid = cfg.grid;
+        rt->last_block = gx_exec_block_threads();
+        rt->last_smem = cfg.smem;
+    }
+    rt->n_launches++;
     return 0;
 }
 
@@ -266,7 +371,8 @@ int gx_open(int cuda_device, gx_rt **out) {
     gx_rt *rt = new gx_rt();
     rt->dev = cuda_device;
     rt->nsm = prop.multiProcessorCount;
-    rt->max_shards = (uint32_t)rt->nsm * kBlocksPerSmMax * gx_exec_block_threads();
+    rt->max_shards = (uint32_t)rt->nsm * 2048; /* one shard per resident thread slot (2048 / SM) */
+    if (const char *e = getenv("GX_ENGINE")) rt->engine = strcmp(e, "interp") == 0 ? GX_ENGINE_INTERP : GX_ENGINE_JIT;
     for (auto &row : rt->attach)
         for (int &x : row) x = -1;
     if (cudaMalloc(&rt->d_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -289,7 +395,10 @@ void gx_close(gx_rt *rt) {
         cudaFree(m.base_aux);
     }
     for (auto &p : rt->progs) cudaFree(p.d_image);
-    for (auto &kv : rt->launches) cudaFree(kv.second.d);
+    for (auto &kv : rt->launches) {
+        cudaFree(kv.second.d);
+        if (kv.second.jmod && drv().moduleUnload) drv().moduleUnload(kv.second.jmod);
+    }
     cudaFree(rt->d_stats);
     if (rt->pipe_init) {
         for (int b = 0; b < 2; b++) {
@@ -587,6 +696,56 @@ int gx_verify_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spe
     return v;
 }
 
+int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *maps, uint32_t n_maps, char *src,
+                   uint64_t src_len, char *log, uint64_t log_len) {
+    if (!insn_slots || n_maps > GX_MAX_MAPS || (n_maps && !maps)) return -EINVAL;
+    GxMapInfo mi[GX_MAX_MAPS];
+    GxLaunch h;
+    memset(&h, 0, sizeof h);
+    memset(h.attach, -1, sizeof h.attach);
+    for (uint32_t i = 0; i < n_maps; i++) {
+        mi[i].valid = maps[i].type != 0;
+        mi[i].type = maps[i].type;
+        mi[i].key_size = maps[i].key_size;
+        mi[i].value_size = maps[i].value_size;
+        mi[i].max_entries = maps[i].max_entries;
+        GxMapDesc &d = h.maps[i];
+        d.data = 0x7f0000000000ull + ((uint64_t)i << 32);
+        d.aux = d.data - 4096;
+        d.type = maps[i].type;
+        d.key_size = maps[i].key_size;
+        d.value_size = maps[i].value_size;
+        d.max_entries = maps[i].max_entries;
+        d.nshards = 303104;
+        d.cap_mask = maps[i].type == GX_MAP_RINGBUF ? maps[i].max_entries - 1 : 2 * maps[i].max_entries - 1;
+        d.priv_off = 0xFFFFFFFFu;
+        d.coherent = 1;
+    }
+    gx_verify_opts o{};
+    GxVerifyResult vr;
+    int v = gx_verify_program((const uint8_t *)insn_slots, n_slots, mi, o, vr);
+    if (v) return v;
+    h.n_progs = 1;
+    h.single = 0;
+    std::vector<const GxInsn *> images{vr.image.data()};
+    std::vector<uint32_t> sizes{(uint32_t)vr.image.size()};
+    std::string s = gx_jit_source(h, images, sizes);
+    if (src && src_len) {
+        size_t k = std::min<size_t>(src_len - 1, s.size());
+        memcpy(src, s.data(), k);
+        src[k] = 0;
+    }
+    std::vector<char> cubin;
+    std::string lg;
+    int rc = gx_jit_compile(s, cubin, lg);
+    if (log && log_len) {
+        size_t k = std::min<size_t>(log_len - 1, lg.size());
+        memcpy(log, lg.data(), k);
+        log[k] = 0;
+    }
+    return rc ? -ENOSYS : 0;
+}
+
 int gx_attach(gx_rt *rt, int prog_fd, uint32_t kind, uint32_t tenant) {
     if (!rt || kind >= GX_MAX_KINDS || tenant > 255) return -EINVAL;
     if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
@@ -603,13 +762,7 @@ int gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, uint6
     LaunchCfg *cfg;
     int rc = get_launch(rt, prog_fd, cfg);
     if (rc) return rc;
-    int e = gx_launch_exec(cfg->d, d_events, n, d_ret, cfg->grid, cfg->smem, (cudaStream_t)stream);
-    if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");
-    rt->last_grid = cfg->grid;
-    rt->last_block = gx_exec_block_threads();
-    rt->last_smem = cfg->smem;
-    rt->n_launches++;
-    return 0;
+    return launch_cfg(rt, *cfg, d_events, n, d_ret, (cudaStream_t)stream);
 }
 
 int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, uint64_t *h_ret) {
@@ -642,16 +795,12 @@ int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, 
         CK(cudaMemcpyAsync(rt->d_chunk[b], src + 32 * i0, 32 * cnt, cudaMemcpyHostToDevice, rt->s_copy), "H2D");
         CK(cudaEventRecord(rt->ev_copied[b], rt->s_copy), "record");
         CK(cudaStreamWaitEvent(rt->s_exec, rt->ev_copied[b], 0), "wait");
-        int e = gx_launch_exec(cfg->d, rt->d_chunk[b], cnt, h_ret ? rt->d_rchunk[b] : nullptr, cfg->grid, cfg->smem, rt->s_exec);
-        if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");
-        rt->n_launches++;
+        rc = launch_cfg(rt, *cfg, rt->d_chunk[b], cnt, h_ret ? rt->d_rchunk[b] : nullptr, rt->s_exec);
+        if (rc) return rc;
         if (h_ret) CK(cudaMemcpyAsync(h_ret + i0, rt->d_rchunk[b], 8 * cnt, cudaMemcpyDeviceToHost, rt->s_exec), "D2H");
         CK(cudaEventRecord(rt->ev_done[b], rt->s_exec), "record");
     }
     CK(cudaStreamSynchronize(rt->s_exec), "sync");
-    rt->last_grid = cfg->grid;
-    rt->last_block = gx_exec_block_threads();
-    rt->last_smem = cfg->smem;
     return 0;
 }
 
@@ -672,6 +821,14 @@ int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
     out->warp_steps = h[GXS_STEPS];
     return 0;
 }
+
+int gx_set_engine(gx_rt *rt, int engine) {
+    if (!rt || (engine != GX_ENGINE_INTERP && engine != GX_ENGINE_JIT)) return -EINVAL;
+    rt->engine = engine;
+    return 0;
+}
+
+int gx_get_engine(gx_rt *rt) { return rt ? rt->engine : -EINVAL; }
 
 int gx_exec_info(gx_rt *rt, uint32_t *grid, uint32_t *block, uint32_t *smem, uint64_t *launches) {
     if (!rt) return -EINVAL;

@@ -1989,11 +1989,21 @@ int gx_verify_program(const uint8_t *slots, uint32_t n, const GxMapInfo *maps, c
     if (!opts.complexity_limit) opts.complexity_limit = 1000000;
     out = GxVerifyResult{};
     Verifier v(slots, n, maps, opts, out);
-    bool ok = v.structural() && v.explore();
+    bool st_ok = v.structural();
+    bool ok = st_ok && v.explore();
     uint32_t all_uniform = 0;
     if (ok) {
         v.hint_uniform.assign(n, 1);
         ok = v.simt(opts.simt_strict != 0, all_uniform);
+    } else if (st_ok && opts.simt_strict && !v.viol.empty() &&
+               (v.viol[0].rule == GX_BUDGET || v.viol[0].rule == GX_COMPLEXITY || v.viol[0].rule == GX_UNBOUNDED_LOOP)) {
+        /* strict mode: a loop that never terminates in exploration is usually a lane-varying loop
+         * bound; report the SIMT rule first when the uniformity pass finds one */
+        std::vector<Violation> first = v.viol;
+        v.viol.clear();
+        v.hint_uniform.assign(n, 1);
+        v.simt(true, all_uniform);
+        for (auto &x : first) v.viol.push_back(x);
     }
     gx_verify_report &rep = out.report;
     rep.n_insns = n;

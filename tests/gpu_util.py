@@ -28,11 +28,18 @@ def oracle_run(config, ev, threshold=None):
     return env, s, r0
 
 
-def gpu_run(config, ev, threshold=None, want_r0=True, runtime=None):
+ENGINES = ("interp", "jit")
+
+
+def make_runtime(engine="jit"):
+    import paper_2512_12615_b200 as gx
+    return gx.Runtime(0, engine=gx.GX_ENGINE_JIT if engine == "jit" else gx.GX_ENGINE_INTERP)
+
+
+def gpu_run(config, ev, threshold=None, want_r0=True, runtime=None, engine="jit"):
     import torch
 
-    import paper_2512_12615_b200 as gx
-    rt = runtime or gx.Runtime(0)
+    rt = runtime or make_runtime(engine)
     s = configs.setup(rt, config, threshold=threshold)
     d_ev = torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda()
     ret = torch.zeros(len(ev), dtype=torch.int64, device="cuda") if want_r0 else None

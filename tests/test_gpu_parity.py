@@ -6,14 +6,14 @@ import pytest
 
 from gxin import asm, configs, gen
 import closed_forms as cf
-from gpu_util import first_diff, gpu_run, oracle_run, outputs
+from gpu_util import ENGINES, first_diff, gpu_run, make_runtime, oracle_run, outputs
 
 pytestmark = pytest.mark.gpu
 
 
-def _compare(config, ev, threshold=None, check_r0=True):
+def _compare(config, ev, threshold=None, check_r0=True, engine="jit"):
     env, so, r0o = oracle_run(config, ev, threshold)
-    rt, sg, r0g = gpu_run(config, ev, threshold)
+    rt, sg, r0g = gpu_run(config, ev, threshold, engine=engine)
     oo, og = outputs(env, so), outputs(rt, sg)
     for key in oo:
         a, b = oo[key], og[key]
@@ -30,26 +30,29 @@ def _compare(config, ev, threshold=None, check_r0=True):
     return rt, sg, sg_stats
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("config,n", [("C1", 10 ** 6), ("C1", 1 << 20), ("C1d", 10 ** 6), ("C2", (1 << 18) + 13),
                                       ("C3", (1 << 18) + 5), ("C4", (1 << 18) + 31), ("C5", (1 << 18) + 1)])
-def test_config_parity(gpu, config, n):
+def test_config_parity(gpu, config, n, engine):
     ev = configs.events(config, configs.SEEDS[config], n)
-    rt, s, st = _compare(config, ev)
-    if config == "C4":
+    rt, s, st = _compare(config, ev, engine=engine)
+    if config == "C4" and engine == "interp":
         assert st["divergent_steps"] > 0   # straddling records exercise the min-PC path
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 1000])
 @pytest.mark.parametrize("config", ["C1", "C3", "C5"])
-def test_ragged_tails(gpu, config, n):
+def test_ragged_tails(gpu, config, n, engine):
     ev = configs.events(config, configs.SEEDS[config], n)
-    _compare(config, ev, threshold=2 if config == "C3" else None)
+    _compare(config, ev, threshold=2 if config == "C3" else None, engine=engine)
 
 
-def test_c3_threshold_small(gpu):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c3_threshold_small(gpu, engine):
     """Threshold T=2 makes many FETCH-ADD crossings: ringbuf multiset must equal the oracle's."""
     ev = configs.events("C3", 99, 1 << 16)
-    rt, s, st = _compare("C3", ev, threshold=2)
+    rt, s, st = _compare("C3", ev, threshold=2, engine=engine)
     assert st["ringbuf_drops"] == 0
 
 
@@ -84,8 +87,9 @@ def test_device_generator(gpu):
 PRE = "ldxdw r0, [r1+0]\nldxdw r2, [r1+8]\n"
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("W", [64, 32])
-def test_isa_parity_alu_jmp(gpu, W):
+def test_isa_parity_alu_jmp(gpu, W, engine):
     """Every ALU / JMP op over the edge grid: GPU R0 == oracle R0 (and == closed form)."""
     import itertools
     import torch
@@ -96,7 +100,7 @@ def test_isa_parity_alu_jmp(gpu, W):
     ev = gen.records(len(pairs), addr=np.array([p[0] for p in pairs], dtype=np.uint64),
                      ts=np.array([p[1] for p in pairs], dtype=np.uint64))
     d_ev = torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda()
-    rt = gx.Runtime(0)
+    rt = make_runtime(engine)
     texts = []
     for name in cf.ALU_NAMES:
         if name == "movsx32" and W == 32:
@@ -119,12 +123,12 @@ def test_isa_parity_alu_jmp(gpu, W):
         assert bad.size == 0, (body, [(hex(pairs[i][0]), hex(pairs[i][1]), hex(int(got[i])), hex(int(want[i]))) for i in bad[:4]])
 
 
-def test_micro_pins_gpu(gpu):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_micro_pins_gpu(gpu, engine):
     """The hand-computed micro-pins (tests/golden/micro_pins.txt) on the GPU."""
     import os
     import torch
-    import paper_2512_12615_b200 as gx
-    rt = gx.Runtime(0)
+    rt = make_runtime(engine)
     path = os.path.join(os.path.dirname(__file__), "golden", "micro_pins.txt")
     for line in open(path):
         if line.startswith("#") or not line.strip():
@@ -147,12 +151,13 @@ def test_unverified_program_refused(gpu):
         rt.run(torch.zeros((32, 32), dtype=torch.uint8, device="cuda"), fd)
 
 
-def test_run_batch_host_parity(gpu):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_run_batch_host_parity(gpu, engine):
     """gx_run_batch_host (chunked H2D pipeline) gives the oracle's result too."""
     import paper_2512_12615_b200 as gx
     ev = configs.events("C2", 7, (1 << 18) + 3)
     env, so, r0o = oracle_run("C2", ev)
-    rt = gx.Runtime(0)
+    rt = make_runtime(engine)
     s = configs.setup(rt, "C2")
     r0 = np.zeros(len(ev), dtype=np.uint64)
     gx.gx_run_batch_host(rt.rt, ev, prog_fd=s.prog_arg, ret=r0)
