@@ -489,5 +489,11 @@ int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string
     cubin.resize(cs);
     nv.cubin(prog, cubin.data());
     nv.destroy(&prog);
+    if (const char *dump = getenv("GX_JIT_DUMP_CUBIN")) {
+        if (FILE *f = fopen(dump, "wb")) {
+            fwrite(cubin.data(), 1, cubin.size(), f);
+            fclose(f);
+        }
+    }
     return 0;
 }
