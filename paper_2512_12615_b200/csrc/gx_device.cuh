@@ -128,12 +128,24 @@ __device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key,
     }
 }
 
-/* ---- per-thread ARRAY: value pointers are LOGICAL addresses data + key*vs + off; the lane's
- * word lives at data + ((logical - data)/8 * nshards + shard) * 8 ([key][word][shard] layout,
- * so the 32 lanes of a warp touching one word are contiguous). */
+/* ---- per-thread ARRAY (S4): one private copy per executor thread ("shard").  Value pointers a
+ * program holds are LOGICAL addresses data + key*vs + off; the physical word is
+ *     pt_word_index(K, W, k, w, shard) = ((q*K*W) + ((k - r) mod K)*W + w) * 32 + l
+ * with shard = 32q + l, r = l mod K, K = max_entries, W = value_size/8 (a power of two).
+ * Lanes are innermost and the key index is rotated by the lane, so a warp whose lane l touches
+ * key l (C2's per-lane statistics) -- and any warp when K == 1 -- touches 256 contiguous bytes. */
+__device__ __forceinline__ uint64_t pt_word_index(uint32_t K, uint32_t W, uint32_t k, uint32_t w, uint32_t shard) {
+    const uint32_t q = shard >> 5, l = shard & 31;
+    const uint32_t r = l < K ? l : l % K;
+    const uint32_t kk = k >= r ? k - r : k + K - r;
+    return ((uint64_t)q * K * W + (uint64_t)kk * W + w) * 32 + l;
+}
 __device__ __forceinline__ uint8_t *pt_phys(const GxMapDesc &m, uint64_t logical, uint32_t shard) {
-    uint64_t lo = logical - m.data;
-    return reinterpret_cast<uint8_t *>(m.data) + ((lo >> 3) * m.nshards + shard) * 8 + (lo & 7);
+    const uint64_t lo = logical - m.data;
+    const uint32_t W = m.value_size >> 3, sh = __popc(W - 1);
+    const uint32_t wi = (uint32_t)(lo >> 3);
+    const uint64_t idx = pt_word_index(m.max_entries, W, wi >> sh, wi & (W - 1), shard);
+    return reinterpret_cast<uint8_t *>(m.data) + idx * 8 + (lo & 7);
 }
 
 }  // namespace gxd

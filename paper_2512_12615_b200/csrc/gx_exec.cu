@@ -503,27 +503,26 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         }
                         break;
                     }
-                    /* general case: group lanes by target address */
+                    /* mixed addresses: per-lane atomics for plain ops; address groups for FETCH */
+                    if (!fetch) {
+                        if (me) global_atomic(op, addr, sv, w32, false);
+                        break;
+                    }
                     const unsigned peers = __match_any_sync(GX_FULL, me ? addr : 0ull);
                     if (me) {
                         const uint32_t gl = __ffs(peers) - 1;
-                        if (!fetch) {
-                            const uint64_t agg = group_reduce(peers, op, sv, w32);
-                            if (lane == gl) global_atomic(op, addr, agg, w32, false);
-                        } else {
-                            uint64_t pre = (op & 0xF0) == 0x50 ? ~0ull : 0, tot = pre;
-                            for (unsigned m = peers; m; m &= m - 1) {
-                                const int j = __ffs(m) - 1;
-                                const uint64_t vj = __shfl_sync(peers, sv, j);
-                                if (j < (int)lane) pre = apply_op(op, pre, vj);
-                                tot = apply_op(op, tot, vj);
-                            }
-                            uint64_t old = 0;
-                            if (lane == gl) old = global_atomic(op, addr, tot, w32, true);
-                            old = __shfl_sync(peers, old, gl);
-                            uint64_t res = apply_op(op, old, pre);
-                            R[in.src * 32 + lane] = w32 ? (uint32_t)res : res;
+                        uint64_t pre = (op & 0xF0) == 0x50 ? ~0ull : 0, tot = pre;
+                        for (unsigned m = peers; m; m &= m - 1) {
+                            const int j = __ffs(m) - 1;
+                            const uint64_t vj = __shfl_sync(peers, sv, j);
+                            if (j < (int)lane) pre = apply_op(op, pre, vj);
+                            tot = apply_op(op, tot, vj);
                         }
+                        uint64_t old = 0;
+                        if (lane == gl) old = global_atomic(op, addr, tot, w32, true);
+                        old = __shfl_sync(peers, old, gl);
+                        uint64_t res = apply_op(op, old, pre);
+                        R[in.src * 32 + lane] = w32 ? (uint32_t)res : res;
                     }
                     break;
                 }

@@ -99,6 +99,64 @@ struct Gen {
     static std::string R(int r) { return "r" + std::to_string(r); }
     static std::string slot(int addr) { return "s" + std::to_string(addr >> 3); }
 
+    /* Load hoisting inside basic blocks: a map / per-thread load moves above earlier instructions
+     * that neither touch its registers nor may write the bytes it reads (stores through the same
+     * base register to disjoint offsets, stores to another memory kind), so the dependent L2 round
+     * trips of read-modify-write sequences overlap (P2 issues both per-thread loads back to back).
+     * Never crosses a jump target, branch, helper call, atomic or exit. */
+    static bool barrier(const GxInsn &h) {
+        return h.op == GX_JA || h.op == GX_EXIT || h.op == GX_OP_NOP || (h.op >= GX_JEQ && h.op <= GX_JSET32) ||
+               h.op >= GX_CALL_LOOKUP_ARRAY || h.op == GX_ATOM_STACK || h.op == GX_ATOM_MAP || h.op == GX_ATOM_PT;
+    }
+    static uint16_t reads(const GxInsn &h) {
+        auto R = [](int r) { return (uint16_t)(1u << r); };
+        const bool x = h.flags & GXF_X;
+        switch (h.op) {
+        case GX_MOV64: case GX_MOV32: return x ? R(h.src) : 0;
+        case GX_MOVSX64: case GX_MOVSX32: return R(h.src);
+        case GX_LDIMM: case GX_LDX_CTX: case GX_LDX_STACK: return 0;
+        case GX_LDX_MAP: case GX_LDX_PT: return R(h.src);
+        case GX_ST_STACK: return x ? R(h.src) : 0;
+        case GX_ST_MAP: case GX_ST_PT: return R(h.dst) | (x ? R(h.src) : 0);
+        default: return R(h.dst) | (x ? R(h.src) : 0);
+        }
+    }
+    static uint16_t writes(const GxInsn &h) {
+        switch (h.op) {
+        case GX_ST_STACK: case GX_ST_MAP: case GX_ST_PT: return 0;
+        default: return (uint16_t)(1u << h.dst);
+        }
+    }
+    static std::vector<GxInsn> hoist_loads(const GxInsn *im, uint32_t n, const std::set<uint32_t> &targets) {
+        std::vector<GxInsn> v(im, im + n);
+        for (uint32_t j = 0; j < n; j++) {
+            const GxInsn g = v[j];
+            if ((g.op != GX_LDX_MAP && g.op != GX_LDX_PT) || targets.count(j)) continue;
+            const uint16_t gd = (uint16_t)(1u << g.dst), gs = (uint16_t)(1u << g.src);
+            const uint32_t gsz = 1u << (g.aux & 15);
+            uint32_t p = j;
+            while (p > 0) {
+                const uint32_t i = p - 1;
+                const GxInsn &h = v[i];
+                if (barrier(h) || targets.count(i)) break;
+                if ((reads(h) | writes(h)) & gd) break;
+                if (writes(h) & gs) break;
+                if (h.op == GX_ST_MAP || h.op == GX_ST_PT) {
+                    const bool other_kind = (h.op == GX_ST_MAP) != (g.op == GX_LDX_MAP);
+                    const uint32_t hsz = 1u << (h.aux & 15);
+                    const bool disjoint = h.dst == g.src && (h.off + (int)hsz <= g.off || g.off + (int)gsz <= h.off);
+                    if (!other_kind && !disjoint) break;
+                }
+                p = i;
+            }
+            if (p < j) {
+                for (uint32_t k = j; k > p; k--) v[k] = v[k - 1];
+                v[p] = g;
+            }
+        }
+        return v;
+    }
+
     void program(int q, const GxInsn *im, uint32_t n) {
         std::set<uint32_t> targets;
         std::set<int> slots;
@@ -130,6 +188,8 @@ struct Gen {
             default: break;
             }
         }
+        std::vector<GxInsn> sched = hoist_loads(im, n, targets);
+        im = sched.data();
         o << "__device__ __forceinline__ uint64_t prog" << q
           << "(const Ctx &c, const uint32_t shard, uint32_t *spriv, unsigned long long &c_herr, "
              "unsigned long long &c_drop, unsigned long long &c_rbb, unsigned long long &c_hfull) {\n";

@@ -158,44 +158,77 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
 }
 
 /* Warp-aggregated atomic on a shared map value (ADD/OR/AND/XOR, +-FETCH) among the lanes that
- * execute it together: one L2 atomic per distinct address; FETCH lanes get old + the exclusive
- * prefix of their address group in lane order (a valid linearisation). */
+ * execute it together.  All lanes on one address (record-uniform keys): one REDUX + one L2 atomic
+ * for the warp.  Mixed addresses: plain per-lane atomics for non-FETCH ops (the L2 serialises
+ * per address; a match_any/segmented-reduce costs more than it saves on random keys), and
+ * __match_any_sync groups for FETCH ops, whose lanes get old + their exclusive group prefix in
+ * lane order (a valid linearisation). */
 template <uint32_t OP, bool W32, bool FETCH>
 __device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
     const unsigned act = __activemask();
     const unsigned lane = threadIdx.x & 31;
-    const unsigned peers = __match_any_sync(act, addr);
-    const unsigned leader = __ffs(peers) - 1;
-    if (!FETCH) {
-        const uint64_t agg = group_reduce(peers, OP, v, W32);
-        if (lane == leader) global_atomic(OP, addr, agg, W32, false);
+    const unsigned leader = __ffs(act) - 1;
+    const uint64_t a0 = __shfl_sync(act, addr, leader);
+    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    if (__all_sync(act, addr == a0)) {
+        if (!FETCH) {
+            const uint64_t agg = group_reduce(act, OP, v, W32);
+            if (lane == leader) global_atomic(OP, addr, agg, W32, false);
+            return 0;
+        }
+        if (act == 0xFFFFFFFFu) {
+            uint64_t inc = W32 ? (uint32_t)v : v;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t o = __shfl_up_sync(act, inc, d);
+                if ((int)lane >= d) inc = apply_op(OP, inc, o);
+            }
+            if (W32) inc = (uint32_t)inc;
+            const uint64_t tot = __shfl_sync(act, inc, 31);
+            uint64_t old = 0;
+            if (lane == leader) old = global_atomic(OP, addr, tot, W32, true);
+            old = __shfl_sync(act, old, leader);
+            uint64_t exc = __shfl_up_sync(act, inc, 1);
+            if (lane == 0) exc = ident;
+            const uint64_t r = apply_op(OP, old, exc);
+            return W32 ? (uint32_t)r : r;
+        }
+    } else if (!FETCH) {
+        global_atomic(OP, addr, v, W32, false);
         return 0;
     }
-    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    const unsigned peers = __match_any_sync(act, addr);
+    const unsigned gl = __ffs(peers) - 1;
     uint64_t pre = ident, tot = ident;
     for (unsigned m = peers; m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const uint64_t vj = __shfl_sync(peers, v, j);
-        if (j < (int)lane) pre = apply_op(OP, pre, vj);
+        const int jl = __ffs(m) - 1;
+        const uint64_t vj = __shfl_sync(peers, v, jl);
+        if (jl < (int)lane) pre = apply_op(OP, pre, vj);
         tot = apply_op(OP, tot, vj);
     }
     uint64_t old = 0;
-    if (lane == leader) old = global_atomic(OP, addr, tot, W32, true);
-    old = __shfl_sync(peers, old, leader);
+    if (lane == gl) old = global_atomic(OP, addr, tot, W32, true);
+    old = __shfl_sync(peers, old, gl);
     const uint64_t r = apply_op(OP, old, pre);
     return W32 ? (uint32_t)r : r;
 }
 
-/* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory */
+/* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory; one atomic per warp
+ * when every converged lane adds to the same word, else one per lane */
+__device__ __forceinline__ void priv_one(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
+    const uint32_t old = atomicAdd(&lo[w], (uint32_t)v);
+    const uint32_t carry = ((uint32_t)(old + (uint32_t)v) < old) ? 1u : 0u;
+    const uint32_t h = (uint32_t)(v >> 32) + carry;
+    if (h) atomicAdd(&hi[w], h);
+}
 __device__ __forceinline__ void priv_add(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
     const unsigned act = __activemask();
-    const unsigned peers = __match_any_sync(act, w);
-    const uint64_t agg = group_sum64(peers, v);
-    if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) {
-        const uint32_t old = atomicAdd(&lo[w], (uint32_t)agg);
-        const uint32_t carry = ((uint32_t)(old + (uint32_t)agg) < old) ? 1u : 0u;
-        const uint32_t h = (uint32_t)(agg >> 32) + carry;
-        if (h) atomicAdd(&hi[w], h);
+    const unsigned leader = __ffs(act) - 1;
+    const uint32_t w0 = __shfl_sync(act, w, leader);
+    if (__all_sync(act, w == w0)) {
+        const uint64_t agg = group_sum64(act, v);
+        if ((threadIdx.x & 31) == leader) priv_one(lo, hi, w0, agg);
+    } else {
+        priv_one(lo, hi, w, v);
     }
 }
 

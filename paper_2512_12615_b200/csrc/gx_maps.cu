@@ -11,37 +11,38 @@
 
 namespace {
 
-/* canonical per-thread value = SUM over shards of each u64 word (S4); one warp per word,
- * coalesced over the [word][shard] layout */
-__global__ void pt_fold_kernel(const uint64_t *__restrict__ data, uint32_t nshards, uint64_t nwords,
+/* canonical per-thread value = SUM over shards of each u64 word (S4); one warp per canonical word,
+ * coalesced over the lane-innermost layout (gxd::pt_word_index) */
+__global__ void pt_fold_kernel(const uint64_t *__restrict__ data, uint32_t nshards, uint32_t K, uint32_t W,
                                uint64_t *__restrict__ out) {
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t w = warp; w < nwords; w += nw) {
-        const uint64_t *row = data + w * nshards;
+    for (uint64_t j = warp; j < (uint64_t)K * W; j += nw) {
+        const uint32_t k = (uint32_t)(j / W), w = (uint32_t)(j % W);
         uint64_t s = 0;
-        for (uint32_t k = lane; k < nshards; k += 32) s += row[k];
+        for (uint32_t sh = lane; sh < nshards; sh += 32) s += data[gxd::pt_word_index(K, W, k, w, sh)];
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(GX_FULL, s, o);
-        if (lane == 0) out[w] = s;
+        if (lane == 0) out[j] = s;
     }
 }
 
-/* host write of per-thread key k: shard 0 = value, other shards = 0 */
-__global__ void pt_set_kernel(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)nw * nshards;
+/* host write of key k: shard 0 = value, every other shard's copy of key k = 0 */
+__global__ void pt_set_kernel(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)W * nshards;
          i += gridDim.x * (uint64_t)blockDim.x) {
-        const uint64_t w = i / nshards, s = i % nshards;
-        data[(word0 + w) * nshards + s] = s == 0 ? vals[w] : 0;
+        const uint32_t w = (uint32_t)(i / nshards), s = (uint32_t)(i % nshards);
+        data[gxd::pt_word_index(K, W, k, w, s)] = s == 0 ? vals[w] : 0;
     }
 }
 
-/* canonical per-thread content -> shard 0, zero the rest (after a merge) */
-__global__ void pt_store_canonical_kernel(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords * nshards;
+/* canonical content -> shard 0, zero the rest (after a merge) */
+__global__ void pt_store_canonical_kernel(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, const uint64_t *vals) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)K * W * nshards;
          i += gridDim.x * (uint64_t)blockDim.x) {
-        const uint64_t w = i / nshards, s = i % nshards;
-        data[i] = s == 0 ? vals[w] : 0;
+        const uint64_t j = i / nshards;
+        const uint32_t s = (uint32_t)(i % nshards);
+        data[gxd::pt_word_index(K, W, (uint32_t)(j / W), (uint32_t)(j % W), s)] = s == 0 ? vals[j] : 0;
     }
 }
 
@@ -141,16 +142,18 @@ inline uint32_t grid_for(uint64_t n, uint32_t block) {
 
 extern "C" {
 
-int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint64_t nwords, uint64_t *out, cudaStream_t s) {
-    pt_fold_kernel<<<grid_for(nwords * 32, 256), 256, 0, s>>>(data, nshards, nwords, out);
+int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint64_t *out, cudaStream_t s) {
+    pt_fold_kernel<<<grid_for((uint64_t)K * W * 32, 256), 256, 0, s>>>(data, nshards, K, W, out);
     return (int)cudaGetLastError();
 }
-int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals, cudaStream_t s) {
-    pt_set_kernel<<<grid_for((uint64_t)nw * nshards, 256), 256, 0, s>>>(data, nshards, word0, nw, vals);
+int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals,
+                cudaStream_t s) {
+    pt_set_kernel<<<grid_for((uint64_t)W * nshards, 256), 256, 0, s>>>(data, nshards, K, W, k, vals);
     return (int)cudaGetLastError();
 }
-int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals, cudaStream_t s) {
-    pt_store_canonical_kernel<<<grid_for(nwords * nshards, 256), 256, 0, s>>>(data, nshards, nwords, vals);
+int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, const uint64_t *vals,
+                            cudaStream_t s) {
+    pt_store_canonical_kernel<<<grid_for((uint64_t)K * W * nshards, 256), 256, 0, s>>>(data, nshards, K, W, vals);
     return (int)cudaGetLastError();
 }
 int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s) {

@@ -31,9 +31,11 @@ int gx_launch_exec(const GxLaunch *d_launch, const void *d_events, uint64_t n, u
                    uint32_t smem, cudaStream_t stream);
 int gx_exec_occupancy(uint32_t smem, int *blocks_per_sm);
 uint32_t gx_exec_block_threads();
-int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint64_t nwords, uint64_t *out, cudaStream_t s);
-int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint64_t word0, uint32_t nw, const uint64_t *vals, cudaStream_t s);
-int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint64_t nwords, const uint64_t *vals, cudaStream_t s);
+int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint64_t *out, cudaStream_t s);
+int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals,
+                cudaStream_t s);
+int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, const uint64_t *vals,
+                            cudaStream_t s);
 int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s);
 int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t flags,
                           int64_t *rc, unsigned long long *full, cudaStream_t s);
@@ -435,9 +437,10 @@ int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
         m.data_bytes = (uint64_t)s.max_entries * s.value_size;
         break;
     case GX_MAP_PERTHREAD_ARRAY:
-        if (s.key_size != 4 || !s.value_size || s.value_size % 8 || s.value_size > 256 || !s.max_entries ||
-            (uint64_t)s.max_entries * s.value_size > 4096)
-            return set_err(rt, -EINVAL, "bad PERTHREAD_ARRAY spec (max_entries*value_size <= 4096)");
+        if (s.key_size != 4 || s.value_size < 8 || s.value_size > 256 || (s.value_size & (s.value_size - 1)) ||
+            !s.max_entries || (uint64_t)s.max_entries * s.value_size > 4096)
+            return set_err(rt, -EINVAL, "bad PERTHREAD_ARRAY spec (value_size a power of two in [8,256], "
+                                        "max_entries*value_size <= 4096)");
         m.nshards = rt->max_shards;
         m.data_bytes = (uint64_t)s.max_entries * s.value_size * m.nshards;
         break;
@@ -513,7 +516,7 @@ int gx_update_map(gx_rt *rt, int fd, const void *keys, const void *vals, uint64_
                 CK(cudaMemcpy((uint8_t *)m.data + (uint64_t)k * s.value_size, v, s.value_size, cudaMemcpyHostToDevice), "write array");
             else {
                 CK(cudaMemcpy(dv, v, s.value_size, cudaMemcpyHostToDevice), "write pt");
-                int e = gx_k_pt_set((uint64_t *)m.data, m.nshards, (uint64_t)k * s.value_size / 8, s.value_size / 8, dv, 0);
+                int e = gx_k_pt_set((uint64_t *)m.data, m.nshards, s.max_entries, s.value_size / 8, k, dv, 0);
                 if (e) return cuda_err(rt, (cudaError_t)e, "pt set");
                 CK(cudaDeviceSynchronize(), "pt set");
             }
@@ -569,7 +572,7 @@ int gx_read_map(gx_rt *rt, int fd, void *keys, void *vals, uint64_t cap, uint64_
         } else {
             uint64_t *tmp;
             CK(cudaMalloc(&tmp, bytes), "cudaMalloc");
-            int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, tmp, 0);
+            int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, s.max_entries, s.value_size / 8, tmp, 0);
             if (e) return cuda_err(rt, (cudaError_t)e, "pt fold");
             CK(cudaMemcpy(vals, tmp, bytes, cudaMemcpyDeviceToHost), "read pt");
             cudaFree(tmp);
@@ -860,7 +863,8 @@ static int ensure_base(gx_rt *rt, Map &m, bool retake = false) {
             uint64_t bytes = (uint64_t)m.spec.max_entries * m.spec.value_size;
             if (m.spec.type == GX_MAP_ARRAY) CK(cudaMemcpy(m.base, m.data, bytes, cudaMemcpyDeviceToDevice), "base");
             else {
-                int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, (uint64_t *)m.base, 0);
+                int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, m.spec.max_entries, m.spec.value_size / 8,
+                                     (uint64_t *)m.base, 0);
                 if (e) return cuda_err(rt, (cudaError_t)e, "base fold");
             }
         }
@@ -879,7 +883,8 @@ static int ensure_base(gx_rt *rt, Map &m, bool retake = false) {
     CK(cudaMalloc(&m.base, bytes), "cudaMalloc base");
     if (m.spec.type == GX_MAP_ARRAY) CK(cudaMemcpy(m.base, m.data, bytes, cudaMemcpyDeviceToDevice), "base");
     else {
-        int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, bytes / 8, (uint64_t *)m.base, 0);
+        int e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, m.spec.max_entries, m.spec.value_size / 8,
+                             (uint64_t *)m.base, 0);
         if (e) return cuda_err(rt, (cudaError_t)e, "base fold");
     }
     CK(cudaDeviceSynchronize(), "base");
@@ -905,7 +910,7 @@ int gx_merge_export(gx_rt *rt, int fd, uint64_t *d_delta, void *stream) {
     if (m.spec.type == GX_MAP_ARRAY) {
         e = gx_k_sub((const uint64_t *)m.data, (const uint64_t *)m.base, d_delta, words, s);
     } else {
-        e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, words, d_delta, s);
+        e = gx_k_pt_fold((const uint64_t *)m.data, m.nshards, m.spec.max_entries, m.spec.value_size / 8, d_delta, s);
         if (!e) e = gx_k_sub(d_delta, (const uint64_t *)m.base, d_delta, words, s);
     }
     if (e) return cuda_err(rt, (cudaError_t)e, "merge export");
@@ -927,7 +932,8 @@ int gx_merge_apply(gx_rt *rt, int fd, const uint64_t *d_sum, void *stream) {
             cudaError_t ce = cudaMemcpyAsync(m.data, m.base, words * 8, cudaMemcpyDeviceToDevice, s);
             if (ce != cudaSuccess) return cuda_err(rt, ce, "merge apply");
         } else {
-            e = gx_k_pt_store_canonical((uint64_t *)m.data, m.nshards, words, (const uint64_t *)m.base, s);
+            e = gx_k_pt_store_canonical((uint64_t *)m.data, m.nshards, m.spec.max_entries, m.spec.value_size / 8,
+                                        (const uint64_t *)m.base, s);
         }
     }
     if (e) return cuda_err(rt, (cudaError_t)e, "merge apply");
