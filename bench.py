@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-c1", action="store_true", help="skip the C1 (1M-event counter) section")
     p.add_argument("--extra", action="store_true", help="also time C1/C3/C4 single-GPU lines (stderr)")
     p.add_argument("--engine", default="jit", choices=["jit", "interp"],
                    help="headline engine (the other one is timed too and reported under 'engines')")
@@ -306,12 +307,74 @@ def main():
         line["cpu_baseline"] = {"value": r, "unit": "events/s", "cores": 1, "kind": "oracle",
                                 "sample": f"prefix of {done} events of the {config} stream (seed {seed}) in "
                                           f"{t:.1f} s, interpretation only; host has {host_cores()} cores, {cpu_model()}"}
+    if rank == 0 and world == 1 and not args.no_c1:
+        try:
+            line["c1"] = c1_measure(local)
+        except Exception as exc:  # pragma: no cover - box-dependent
+            line["c1"] = {"error": str(exc)[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.extra:
             extra_lines(rt, args)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c1_measure(device):
+    """BASELINE.json configs[0] / the north-star target: the counter policy over 2^20-event batches.
+    8 distinct batches (256 MiB > L2) are rotated so every launch streams from HBM.  Reported both
+    per single launch (CUDA events around each launch) and steady state (100 back-to-back launches
+    captured in one CUDA graph, SURVEY.md §8d C1 timing protocol)."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+    peaks = measured_peaks()[0]
+    out = {}
+    n, nb = 1 << 20, 8
+    for config in ("C1", "C1d"):
+        rt = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
+        s = configs.setup(rt, config)
+        bufs = [gen_gpu.generate_device(config, configs.SEEDS[config], n, i0=k * n, n_total=nb * n, device=device)
+                for k in range(nb)]
+        stream = torch.cuda.Stream(device)
+        with torch.cuda.stream(stream):
+            for k in range(3 * nb):
+                rt.run(bufs[k % nb], s.prog_arg, stream=stream)
+            stream.synchronize()
+            times = []
+            for k in range(5 * nb):
+                a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                rt.run(bufs[k % nb], s.prog_arg, stream=stream)
+                b2.record(stream)
+                times.append((a, b2))
+            stream.synchronize()
+            single = float(np.median([a.elapsed_time(b2) for a, b2 in times]))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for k in range(100):
+                    rt.run(bufs[k % nb], s.prog_arg, stream=stream)
+            g.replay()
+            stream.synchronize()
+            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(5):
+                g.replay()
+            b2.record(stream)
+            stream.synchronize()
+            steady = a.elapsed_time(b2) / 500
+        counts = rt.array_u64(s.fds[(0, "counts")])
+        runs = 3 * nb + 5 * nb + 100 + 500
+        assert int(counts.sum()) == runs * n, "counter total != events (north star invariant)"
+        bw = lambda ms: EVENT_BYTES * n / (ms / 1e3) / 1e9
+        out[config] = {"events": n, "single_launch_us": single * 1e3, "single_events_per_s": n / (single / 1e3),
+                       "single_hbm_frac": bw(single) / peaks["hbm_gbs"],
+                       "steady_us": steady * 1e3, "steady_events_per_s": n / (steady / 1e3),
+                       "steady_hbm_frac": bw(steady) / peaks["hbm_gbs"], "counter_total_ok": True,
+                       "flush": "8 rotating 32-MiB batches (256 MiB > L2)"}
+        rt.close()
+        del bufs
+    return out
 
 
 def e2e_measure(rt, s, events, n, n_total, world, args):

@@ -60,10 +60,13 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
         uint64_t *side = slots + 2 * cap;
         return ld_acquire(side) == 1 ? side + 1 : nullptr;
     }
+    /* relaxed gpu-scope probes: coherent at L2 without the L1 invalidation an acquire costs; the
+     * slot was published by one 16-B atomic, and the value is only read after the key compare
+     * resolved (no load speculation on the GPU) */
     uint64_t h = mix64(key) & m.cap_mask;
     for (uint64_t i = 0; i < cap; i++) {
         uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
-        uint64_t k = ld_acquire(s);
+        uint64_t k = ld_relaxed(s);
         if (k == key) return s + 1;
         if (k == GX_HASH_EMPTY) return nullptr;
     }

@@ -336,9 +336,13 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         uint64_t *rp = d_ret;
         unsigned long long *st = rt->d_stats;
         void *args[] = {(void *)&ev, (void *)&nn, (void *)&rp, (void *)&st};
-        if (drv().launchKernel(cfg.jfunc, cfg.jgrid, 1, 1, 256, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
+        /* small batches: fewer, fuller blocks (>= 8 events per thread) so block set-up and the
+         * privatised-shard flush do not dominate; large batches: the resident grid */
+        uint64_t want = (n + 256 * 8 - 1) / (256 * 8);
+        uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
+        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, 256, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
-        rt->last_grid = cfg.jgrid;
+        rt->last_grid = grid;
         rt->last_block = 256;
         rt->last_smem = 0;
     } else {
