@@ -44,11 +44,14 @@ using gxd::E_NOENT;
 
 namespace {
 
+/* the event stream is read once: L1 no-allocate, L2 evict-first (keeps the maps resident) */
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return r;
 }
 

@@ -20,6 +20,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <sstream>
@@ -449,6 +451,8 @@ struct Gen {
     }
 
     void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+        int U = 2;
+        if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
@@ -462,12 +466,20 @@ struct Gen {
              "  const uint32_t shard = blockIdx.x * 256 + threadIdx.x;\n"
              "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
              "  const uint64_t stride = (uint64_t)gridDim.x * 256;\n"
-             "  uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;\n"
-             "  uint4 na = make_uint4(0, 0, 0, 0), nb = na;\n"
-             "  if (i < n) { na = ldg_stream(ev + 2 * i); nb = ldg_stream(ev + 2 * i + 1); }\n"
-             "  for (; i < n; i += stride) {\n"
-             "    const uint4 a = na, b = nb;\n"
-             "    if (i + stride < n) { na = ldg_stream(ev + 2 * (i + stride)); nb = ldg_stream(ev + 2 * (i + stride) + 1); }\n"
+             "  const uint64_t pol = evict_first_policy();\n"
+             "  /* U events per thread per iteration: their 2*U 16-B loads are issued back to back */\n"
+             "  for (uint64_t i0 = (uint64_t)blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += stride * " << U << ") {\n"
+             "    uint4 ea[" << U << "], eb[" << U << "];\n"
+             "    #pragma unroll\n"
+             "    for (int u = 0; u < " << U << "; u++) {\n"
+             "      const uint64_t i = i0 + u * stride;\n"
+             "      if (i < n) { ea[u] = ldg_stream_ef(ev + 2 * i, pol); eb[u] = ldg_stream_ef(ev + 2 * i + 1, pol); }\n"
+             "    }\n"
+             "    #pragma unroll\n"
+             "    for (int u = 0; u < " << U << "; u++) {\n"
+             "    const uint64_t i = i0 + u * stride;\n"
+             "    if (i >= n) break;\n"
+             "    const uint4 a = ea[u], b = eb[u];\n"
              "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n";
         if (L.single >= 0) {
             o << "    const int p = 0;\n";
@@ -482,7 +494,7 @@ struct Gen {
         for (size_t q = 0; q < images.size(); q++)
             o << "    case " << q << ": r = prog" << q << "(c, shard, spriv, c_herr, c_drop, c_rbb, c_hfull); c_run++; break;\n";
         o << "    default: c_skip++; break;\n    }\n"
-             "    if (ret) ret[i] = r;\n  }\n";
+             "    if (ret) ret[i] = r;\n    }\n  }\n";
         o << "  for (int s = 16; s; s >>= 1) {\n"
              "    c_run += __shfl_xor_sync(0xFFFFFFFFu, c_run, s); c_skip += __shfl_xor_sync(0xFFFFFFFFu, c_skip, s);\n"
              "    c_herr += __shfl_xor_sync(0xFFFFFFFFu, c_herr, s); c_drop += __shfl_xor_sync(0xFFFFFFFFu, c_drop, s);\n"
