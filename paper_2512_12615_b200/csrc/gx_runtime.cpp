@@ -266,7 +266,8 @@ int get_launch(gx_rt *rt, int prog_fd, LaunchCfg *&out) {
         h.maps[m].coherent = written ? 1 : 0;
         const Map &mm = rt->maps[m];
         uint64_t bytes = (uint64_t)mm.spec.max_entries * mm.spec.value_size;
-        if (used && written && accum && mm.spec.type == GX_MAP_ARRAY && h.n_priv < 8 && priv + bytes <= kPrivMaxBytes) {
+        if (used && written && accum && mm.spec.type == GX_MAP_ARRAY && h.n_priv < 8 && priv + bytes <= kPrivMaxBytes &&
+            !getenv("GX_NO_PRIV")) {
             h.maps[m].priv_off = priv;
             h.priv_maps[h.n_priv++] = m;
             priv += (uint32_t)((bytes + 15) & ~15ull);
@@ -338,7 +339,9 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         void *args[] = {(void *)&ev, (void *)&nn, (void *)&rp, (void *)&st};
         /* small batches: fewer, fuller blocks (>= 8 events per thread) so block set-up and the
          * privatised-shard flush do not dominate; large batches: the resident grid */
-        uint64_t want = (n + 256 * 8 - 1) / (256 * 8);
+        static const uint64_t per_thread = getenv("GX_JIT_EPT") ? strtoull(getenv("GX_JIT_EPT"), nullptr, 10) : 8;
+        static const uint64_t cap = getenv("GX_JIT_GRID") ? strtoull(getenv("GX_JIT_GRID"), nullptr, 10) : ~0ull;
+        uint64_t want = std::min<uint64_t>(cap, (n + 256 * per_thread - 1) / (256 * per_thread));
         uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
         if (drv().launchKernel(cfg.jfunc, grid, 1, 1, 256, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
