@@ -450,25 +450,25 @@ struct Gen {
         st(fetch ? R(g.src) + " = " + e + ";" : "(void)" + e + ";");
     }
 
-    void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+    void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes, int B) {
         int U = 2;
         if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
-        o << "extern \"C\" __global__ void __launch_bounds__(256) gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
+        o << "extern \"C\" __global__ void __launch_bounds__(" << B << ") gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
              "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
-             "  for (uint32_t k = threadIdx.x; k < " << priv_words << "u; k += 256) spriv[k] = 0;\n"
+             "  for (uint32_t k = threadIdx.x; k < " << priv_words << "u; k += " << B << ") spriv[k] = 0;\n"
              "  if (threadIdx.x < 8) sstats[threadIdx.x] = 0;\n"
              "  __syncthreads();\n"
-             "  const uint32_t shard = blockIdx.x * 256 + threadIdx.x;\n"
+             "  const uint32_t shard = blockIdx.x * " << B << " + threadIdx.x;\n"
              "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
-             "  const uint64_t stride = (uint64_t)gridDim.x * 256;\n"
+             "  const uint64_t stride = (uint64_t)gridDim.x * " << B << ";\n"
              "  const uint64_t pol = evict_first_policy();\n"
              "  /* U events per thread per iteration: their 2*U 16-B loads are issued back to back */\n"
-             "  for (uint64_t i0 = (uint64_t)blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += stride * " << U << ") {\n"
+             "  for (uint64_t i0 = (uint64_t)blockIdx.x * " << B << " + threadIdx.x; i0 < n; i0 += stride * " << U << ") {\n"
              "    uint4 ea[" << U << "], eb[" << U << "];\n"
              "    #pragma unroll\n"
              "    for (int u = 0; u < " << U << "; u++) {\n"
@@ -512,7 +512,7 @@ struct Gen {
         for (uint32_t k = 0; k < L.n_priv; k++) {
             const GxMapDesc &m = L.maps[L.priv_maps[k]];
             const uint32_t nw = m.max_entries * m.value_size / 8;
-            o << "  for (uint32_t w = threadIdx.x; w < " << nw << "u; w += 256) {\n"
+            o << "  for (uint32_t w = threadIdx.x; w < " << nw << "u; w += " << B << ") {\n"
               << "    const uint64_t v = (uint64_t)spriv[" << m.priv_off / 4 << " + w] | ((uint64_t)spriv["
               << m.priv_off / 4 + nw << " + w] << 32);\n"
               << "    if (v) atomicAdd((unsigned long long *)" << hex(m.data) << " + w, (unsigned long long)v);\n  }\n";
@@ -523,9 +523,19 @@ struct Gen {
 
 }  // namespace
 
-std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+int gx_jit_block() {
+    static int b = [] {
+        int v = 1024;
+        if (const char *e = getenv("GX_JIT_BLOCK")) v = atoi(e);
+        return (v == 256 || v == 512 || v == 1024) ? v : 1024;
+    }();
+    return b;
+}
+
+std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes,
+                          int block) {
     Gen g(L);
-    g.kernel(images, sizes);
+    g.kernel(images, sizes, block);
     return g.o.str();
 }
 

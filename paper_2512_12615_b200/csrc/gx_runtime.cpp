@@ -96,7 +96,7 @@ struct LaunchCfg {
     bool jit_tried = false;
     CUmodule jmod = nullptr;
     CUfunction jfunc = nullptr;
-    uint32_t jgrid = 0;
+    uint32_t jgrid = 0, jblock = 256;
     std::string jit_log;
     double jit_ms = 0;
 };
@@ -309,21 +309,35 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         images.push_back(rt->progs[q].vr.image.data());
         sizes.push_back((uint32_t)rt->progs[q].vr.image.size());
     }
-    std::string src = gx_jit_source(cfg.h, images, sizes);
-    if (const char *dump = getenv("GX_JIT_DUMP")) {
-        if (FILE *f = fopen(dump, "w")) {
-            fputs(src.c_str(), f);
-            fclose(f);
+    /* fewer, larger blocks keep the per-block privatised-shard flush small; fall back to 256-thread
+     * blocks when register pressure would cut residency below 1536 threads per SM */
+    for (int B : {gx_jit_block(), 256}) {
+        std::string src = gx_jit_source(cfg.h, images, sizes, B);
+        if (const char *dump = getenv("GX_JIT_DUMP")) {
+            if (FILE *f = fopen(dump, "w")) {
+                fputs(src.c_str(), f);
+                fclose(f);
+            }
         }
+        std::vector<char> cubin;
+        if (gx_jit_compile(src, cubin, cfg.jit_log)) return set_err(rt, -ENOSYS, "JIT compile failed: %s", cfg.jit_log.c_str());
+        CUmodule mod = nullptr;
+        CUfunction fn = nullptr;
+        if (d.moduleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
+        if (d.moduleGetFunction(&fn, mod, "gx_jit_kernel") != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
+        int bps = 0;
+        if (!d.occupancy || d.occupancy(&bps, fn, B, 0) != CUDA_SUCCESS || bps < 1) bps = 1;
+        bps = std::min(bps, 2048 / B); /* per-thread shards: at most 2048 resident threads per SM */
+        if (bps * B < 1536 && B != 256) {
+            if (d.moduleUnload) d.moduleUnload(mod);
+            continue;
+        }
+        cfg.jmod = mod;
+        cfg.jfunc = fn;
+        cfg.jblock = (uint32_t)B;
+        cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
+        break;
     }
-    std::vector<char> cubin;
-    if (gx_jit_compile(src, cubin, cfg.jit_log)) return set_err(rt, -ENOSYS, "JIT compile failed: %s", cfg.jit_log.c_str());
-    if (d.moduleLoadData(&cfg.jmod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
-    if (d.moduleGetFunction(&cfg.jfunc, cfg.jmod, "gx_jit_kernel") != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
-    int bps = 0;
-    if (!d.occupancy || d.occupancy(&bps, cfg.jfunc, 256, 0) != CUDA_SUCCESS || bps < 1) bps = 4;
-    bps = std::min(bps, 8);
-    cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
     cfg.jit_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return 0;
 }
@@ -341,12 +355,13 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
          * privatised-shard flush do not dominate; large batches: the resident grid */
         static const uint64_t per_thread = getenv("GX_JIT_EPT") ? strtoull(getenv("GX_JIT_EPT"), nullptr, 10) : 8;
         static const uint64_t cap = getenv("GX_JIT_GRID") ? strtoull(getenv("GX_JIT_GRID"), nullptr, 10) : ~0ull;
-        uint64_t want = std::min<uint64_t>(cap, (n + 256 * per_thread - 1) / (256 * per_thread));
+        const uint64_t B = cfg.jblock;
+        uint64_t want = std::min<uint64_t>(cap, (n + B * per_thread - 1) / (B * per_thread));
         uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
-        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, 256, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
+        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
         rt->last_grid = grid;
-        rt->last_block = 256;
+        rt->last_block = (uint32_t)B;
         rt->last_smem = 0;
     } else {
         int e = gx_launch_exec(cfg.d, d_events, n, d_ret, cfg.grid, cfg.smem, stream);
@@ -739,7 +754,7 @@ int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *
     h.single = 0;
     std::vector<const GxInsn *> images{vr.image.data()};
     std::vector<uint32_t> sizes{(uint32_t)vr.image.size()};
-    std::string s = gx_jit_source(h, images, sizes);
+    std::string s = gx_jit_source(h, images, sizes, gx_jit_block());
     if (src && src_len) {
         size_t k = std::min<size_t>(src_len - 1, s.size());
         memcpy(src, s.data(), k);
