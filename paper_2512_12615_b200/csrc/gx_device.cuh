@@ -131,6 +131,46 @@ __device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key,
     }
 }
 
+/* Warp-cooperative HASH helpers: the lanes of `mask` call together; `me` marks the lanes whose
+ * event is executing the helper.  When every executing lane asks for the same key (a warp-uniform
+ * key -- a page swept by a whole warp record in C3's prefill), one lane probes / inserts and the
+ * others reuse its result instead of 31 probes and 31 contending CASes on one slot.  Sequential
+ * equivalent: the leader's event goes first. */
+__device__ __forceinline__ uint64_t *hash_lookup_coop(const GxMapDesc &m, uint64_t key, bool me, unsigned mask) {
+    const unsigned part = __ballot_sync(mask, me);
+    if (!part) return nullptr;
+    const unsigned lane = threadIdx.x & 31;
+    const int leader = __ffs(part) - 1;
+    const uint64_t k0 = __shfl_sync(mask, key, leader);
+    if (__all_sync(mask, !me || key == k0)) {
+        uint64_t *v = nullptr;
+        if ((int)lane == leader) v = hash_find(m, key);
+        return reinterpret_cast<uint64_t *>(__shfl_sync(mask, reinterpret_cast<unsigned long long>(v), leader));
+    }
+    return me ? hash_find(m, key) : nullptr;
+}
+__device__ __forceinline__ int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
+                                                    bool &full, bool me, unsigned mask) {
+    full = false;
+    const unsigned part = __ballot_sync(mask, me);
+    if (!part) return 0;
+    const unsigned lane = threadIdx.x & 31;
+    const int leader = __ffs(part) - 1;
+    const uint64_t k0 = __shfl_sync(mask, key, leader);
+    const uint64_t f0 = __shfl_sync(mask, flags, leader);
+    if (__all_sync(mask, !me || (key == k0 && flags == f0))) {
+        int64_t rc = 0;
+        if ((int)lane == leader) rc = hash_update(m, key, val, flags, full);
+        const int64_t rc0 = (int64_t)__shfl_sync(mask, (unsigned long long)rc, leader);
+        __syncwarp(mask);
+        if (!me || (int)lane == leader) return rc;
+        /* NOEXIST after the leader inserted (or found) the key: it is present for everyone else */
+        if (flags == 1 && (rc0 == 0 || rc0 == -E_EXIST)) return -E_EXIST;
+        return hash_update(m, key, val, flags, full);
+    }
+    return me ? hash_update(m, key, val, flags, full) : 0;
+}
+
 /* ---- per-thread ARRAY (S4): one private copy per executor thread ("shard").  Value pointers a
  * program holds are LOGICAL addresses data + key*vs + off; the physical word is
  *     pt_word_index(K, W, k, w, shard) = ((q*K*W) + ((k - r) mod K)*W + w) * 32 + l

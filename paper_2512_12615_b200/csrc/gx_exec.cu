@@ -541,19 +541,21 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     }
                     if (in.flags & (GXF_FETCH | GXF_W32)) goto lookup_branch;
                     break;
-                case GX_CALL_LOOKUP_HASH:
+                case GX_CALL_LOOKUP_HASH: {
+                    const GxMapDesc &md = M[in.aux];
+                    uint64_t k = 0;
                     if (me) {
-                        const GxMapDesc &md = M[in.aux];
-                        uint64_t k = (in.flags & GXF_KEY_MAPV)
-                                         ? (md.key_size == 4 ? *reinterpret_cast<const uint32_t *>(R[2 * 32 + lane])
-                                                             : *reinterpret_cast<const uint64_t *>(R[2 * 32 + lane]))
-                                         : K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
+                        k = (in.flags & GXF_KEY_MAPV)
+                                ? (md.key_size == 4 ? *reinterpret_cast<const uint32_t *>(R[2 * 32 + lane])
+                                                    : *reinterpret_cast<const uint64_t *>(R[2 * 32 + lane]))
+                                : K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
                         if (md.key_size == 4) k &= 0xFFFFFFFFull;
-                        uint64_t *v = gxd::hash_find(md, k);
-                        R[lane] = (uint64_t)v;
                     }
+                    uint64_t *v = gxd::hash_lookup_coop(md, k, me, GX_FULL);
+                    if (me) R[lane] = (uint64_t)v;
                     if (in.flags & (GXF_FETCH | GXF_W32)) goto lookup_branch;
                     break;
+                }
                 case GX_CALL_UPDATE_ARRAY:
                 case GX_CALL_UPDATE_PT:
                     if (me) {
@@ -580,23 +582,28 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         R[lane] = (uint64_t)rc;
                     }
                     break;
-                case GX_CALL_UPDATE_HASH:
+                case GX_CALL_UPDATE_HASH: {
+                    const GxMapDesc &md = M[in.aux];
+                    uint64_t k = 0, v = 0, fl = 0;
                     if (me) {
-                        const GxMapDesc &md = M[in.aux];
-                        uint64_t k = (in.flags & GXF_KEY_MAPV)
-                                         ? (md.key_size == 4 ? *reinterpret_cast<const uint32_t *>(R[2 * 32 + lane])
-                                                             : *reinterpret_cast<const uint64_t *>(R[2 * 32 + lane]))
-                                         : K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
+                        k = (in.flags & GXF_KEY_MAPV)
+                                ? (md.key_size == 4 ? *reinterpret_cast<const uint32_t *>(R[2 * 32 + lane])
+                                                    : *reinterpret_cast<const uint64_t *>(R[2 * 32 + lane]))
+                                : K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
                         if (md.key_size == 4) k &= 0xFFFFFFFFull;
-                        const uint64_t v = (in.flags & GXF_VAL_MAPV) ? *reinterpret_cast<const uint64_t *>(R[3 * 32 + lane])
-                                                                      : K[((uint32_t)in.imm / 8) * 32 + lane];
-                        bool full;
-                        const int64_t rc = gxd::hash_update(md, k, v, R[4 * 32 + lane], full);
+                        v = (in.flags & GXF_VAL_MAPV) ? *reinterpret_cast<const uint64_t *>(R[3 * 32 + lane])
+                                                      : K[((uint32_t)in.imm / 8) * 32 + lane];
+                        fl = R[4 * 32 + lane];
+                    }
+                    bool full;
+                    const int64_t rc = gxd::hash_update_coop(md, k, v, fl, full, me, GX_FULL);
+                    if (me) {
                         if (rc) c_herr++;
                         if (full) c_hfull++;
                         R[lane] = (uint64_t)rc;
                     }
                     break;
+                }
                 case GX_CALL_RINGBUF_OUTPUT: {
                     const GxMapDesc &md = M[in.aux];
                     const uint32_t size = (uint32_t)in.imm, flags = (uint32_t)(in.imm >> 32);
