@@ -314,8 +314,7 @@ struct Gen {
                           ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
                           : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
-                if (getenv("GX_JIT_NOCOOP")) st("r0 = (uint64_t)gxd::hash_find(" + md(g.aux) + ", " + key + ");");
-                else st("r0 = (uint64_t)gxd::hash_lookup_coop(" + md(g.aux) + ", " + key + ", true, __activemask());");
+                st("r0 = (uint64_t)jit_hash_find(" + md(g.aux) + ", " + key + ");");
             } else {
                 key = (g.flags & GXF_KEY_MAPV) ? "*(const uint32_t *)r2"
                                                : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
@@ -354,12 +353,8 @@ struct Gen {
                                   : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
             const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
-            if (getenv("GX_JIT_NOCOOP"))
-                st("{ bool full; const int64_t rc = gxd::hash_update(" + md(g.aux) + ", " + key + ", " + v +
-                   ", r4, full); if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
-            else
-                st("{ bool full; const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", " + key + ", " + v +
-                   ", r4, full, true, __activemask()); if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
+            st("{ bool full; const int64_t rc = jit_hash_update(" + md(g.aux) + ", " + key + ", " + v +
+               ", r4, full); if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
             break;
         }
         case GX_CALL_RINGBUF_OUTPUT: {

@@ -9,7 +9,7 @@
  * header.  One thread runs one event; SIMT divergence is the hardware's (independent thread
  * scheduling reconverges at post-dominators), so the interpreter's uniform-PC / min-PC machinery
  * is not needed here.  Helpers keep the interpreter's semantics: warp-aggregated map atomics over
- * the lanes that execute the atomic together (__activemask + __match_any_sync + __reduce_*_sync),
+ * the lanes of a fully present warp (__match_any_sync + __reduce_*_sync; per-lane when diverged),
  * shared-memory privatised ADD accumulators, one ringbuf reservation per converged warp.
  * Included only by NVRTC-compiled sources.
  */
@@ -177,9 +177,20 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
  * per address; a match_any/segmented-reduce costs more than it saves on random keys), and
  * __match_any_sync groups for FETCH ops, whose lanes get old + their exclusive group prefix in
  * lane order (a valid linearisation). */
+/* Warp collectives in JIT code are used only where the whole warp is present (__activemask() is
+ * full): every lane then executes the same helper body and reaches the same *_sync operations.
+ * A mask built from a partial __activemask() is not a convergence guarantee (lanes can be
+ * re-split under independent thread scheduling) and deadlocked at scale, so diverged lanes use the
+ * per-lane forms, which are equally valid linearisations. */
+__device__ __forceinline__ bool warp_converged() { return __activemask() == 0xFFFFFFFFu; }
+
 template <uint32_t OP, bool W32, bool FETCH>
 __device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
-    const unsigned act = __activemask();
+    if (!warp_converged()) {
+        const uint64_t old = global_atomic(OP, addr, v, W32, FETCH);
+        return W32 ? (uint32_t)old : old;
+    }
+    const unsigned act = 0xFFFFFFFFu;
     const unsigned lane = threadIdx.x & 31;
     const unsigned leader = __ffs(act) - 1;
     const uint64_t a0 = __shfl_sync(act, addr, leader);
@@ -235,7 +246,11 @@ __device__ __forceinline__ void priv_one(uint32_t *lo, uint32_t *hi, uint32_t w,
     if (h) atomicAdd(&hi[w], h);
 }
 __device__ __forceinline__ void priv_add(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
-    const unsigned act = __activemask();
+    if (!warp_converged()) {
+        priv_one(lo, hi, w, v);
+        return;
+    }
+    const unsigned act = 0xFFFFFFFFu;
     const unsigned leader = __ffs(act) - 1;
     const uint32_t w0 = __shfl_sync(act, w, leader);
     if (__all_sync(act, w == w0)) {
@@ -249,7 +264,7 @@ __device__ __forceinline__ void priv_add(uint32_t *lo, uint32_t *hi, uint32_t w,
 /* one ringbuf reservation per converged group of lanes; returns 0 or -EAGAIN */
 __device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uint64_t *words, uint32_t size,
                                                   unsigned long long &drops, unsigned long long &bytes) {
-    const unsigned act = __activemask();
+    const unsigned act = warp_converged() ? 0xFFFFFFFFu : (1u << (threadIdx.x & 31)); /* else: per-lane reservation */
     const unsigned lane = threadIdx.x & 31;
     const uint64_t recb = (8 + size + 7) & ~7u;
     const uint32_t cnt = __popc(act), rank = __popc(act & ((1u << lane) - 1));
@@ -278,6 +293,18 @@ __device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uin
         bytes += nok * recb;
     }
     return ok ? 0 : -(int64_t)gxd::E_AGAIN;
+}
+
+/* HASH helpers for JIT code: warp-cooperative (one probe / insert for a warp-uniform key) when the
+ * whole warp is present, per lane otherwise */
+__device__ __forceinline__ uint64_t *jit_hash_find(const GxMapDesc &m, uint64_t key) {
+    if (warp_converged()) return gxd::hash_lookup_coop(m, key, true, 0xFFFFFFFFu);
+    return gxd::hash_find(m, key);
+}
+__device__ __forceinline__ int64_t jit_hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
+                                                   bool &full) {
+    if (warp_converged()) return gxd::hash_update_coop(m, key, val, flags, full, true, 0xFFFFFFFFu);
+    return gxd::hash_update(m, key, val, flags, full);
 }
 
 }  // namespace gxj
