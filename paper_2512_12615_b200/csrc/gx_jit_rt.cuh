@@ -298,12 +298,20 @@ __device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uin
 /* HASH helpers for JIT code: warp-cooperative (one probe / insert for a warp-uniform key) when the
  * whole warp is present, per lane otherwise */
 __device__ __forceinline__ uint64_t *jit_hash_find(const GxMapDesc &m, uint64_t key) {
-    if (warp_converged()) return gxd::hash_lookup_coop(m, key, true, 0xFFFFFFFFu);
+#ifndef GX_NOCOOP
+    if (warp_converged())
+#else
+    if (false)
+#endif return gxd::hash_lookup_coop(m, key, true, 0xFFFFFFFFu);
     return gxd::hash_find(m, key);
 }
 __device__ __forceinline__ int64_t jit_hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
                                                    bool &full) {
-    if (warp_converged()) return gxd::hash_update_coop(m, key, val, flags, full, true, 0xFFFFFFFFu);
+#ifndef GX_NOCOOP
+    if (warp_converged())
+#else
+    if (false)
+#endif return gxd::hash_update_coop(m, key, val, flags, full, true, 0xFFFFFFFFu);
     return gxd::hash_update(m, key, val, flags, full);
 }
 
