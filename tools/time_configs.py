@@ -28,8 +28,11 @@ for spec in [a for a in sys.argv[1:] if ":" in a]:
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 5
+    st = rt.stats()
     print(json.dumps({"config": config, "n": n, "unroll": os.environ.get("GX_JIT_UNROLL", "2"), "ms": round(ms, 4),
                       "ev_per_s": n / ms * 1e3, "hbm_frac": round(32 * n / (ms / 1e3) / 1e9 / peak, 4),
-                      "grid": gx.gx_exec_info(rt.rt)["grid"]}), flush=True)
+                      "grid": gx.gx_exec_info(rt.rt)["grid"], "block": gx.gx_exec_info(rt.rt)["block"],
+                      "run_ok": st["events_run"] == 8 * n, "hash_full": st["hash_full"],
+                      "rb_drops": st["ringbuf_drops"]}), flush=True)
     del ev
     rt.close()
