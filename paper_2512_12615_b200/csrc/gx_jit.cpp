@@ -454,6 +454,7 @@ struct Gen {
         int U = 2;
         if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
         if (getenv("GX_JIT_NOCOOP")) o << "#define GX_NOCOOP 1\n";
+        if (getenv("GX_JIT_NOWARPAGG")) o << "#define GX_NOWARPAGG 1\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;

@@ -182,7 +182,13 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
  * A mask built from a partial __activemask() is not a convergence guarantee (lanes can be
  * re-split under independent thread scheduling) and deadlocked at scale, so diverged lanes use the
  * per-lane forms, which are equally valid linearisations. */
-__device__ __forceinline__ bool warp_converged() { return __activemask() == 0xFFFFFFFFu; }
+__device__ __forceinline__ bool warp_converged() {
+#ifdef GX_NOWARPAGG
+    return false;
+#else
+    return __activemask() == 0xFFFFFFFFu;
+#endif
+}
 
 template <uint32_t OP, bool W32, bool FETCH>
 __device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
