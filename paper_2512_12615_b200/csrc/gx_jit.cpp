@@ -159,15 +159,40 @@ struct Gen {
         return v;
     }
 
-    void program(int q, const GxInsn *im, uint32_t n) {
-        std::set<uint32_t> targets;
+    static bool is_jcc(uint8_t op) { return op >= GX_JEQ && op <= GX_JSET32; }
+    static bool is_lookup(uint8_t op) {
+        return op == GX_CALL_LOOKUP_ARRAY || op == GX_CALL_LOOKUP_PT || op == GX_CALL_LOOKUP_HASH;
+    }
+    static bool ends_block(const GxInsn &g) {
+        return g.op == GX_JA || g.op == GX_EXIT || g.op == GX_OP_NOP || is_jcc(g.op) ||
+               (is_lookup(g.op) && (g.flags & (GXF_FETCH | GXF_W32)));
+    }
+
+    std::ostringstream *out_ = nullptr;
+    void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
+    void me(const std::string &x) { (*out_) << "  if (me) { " << x << " }\n"; }
+
+    /* SIMT-convergent code (v2): the whole warp runs every program; basic blocks execute under a
+     * per-lane `me` predicate.  Uniform-PC fast path: while all active lanes agree, blocks jump
+     * straight to their successor after one ballot per branch.  On a split, the min-PC dispatcher
+     * (__reduce_min_sync over the lanes' next-block ids) runs one block at a time for the lanes at
+     * the lowest id until they meet again -- the interpreter's a3 scheme at basic-block granularity.
+     * Every helper that uses warp collectives is therefore called by all 32 lanes. */
+    void program(int q, const GxInsn *im0, uint32_t n) {
+        std::set<uint32_t> targets, leaders{0};
+        for (uint32_t i = 0; i < n; i++) {
+            const GxInsn &g = im0[i];
+            if (g.op == GX_JA || is_jcc(g.op)) targets.insert(g.aux);
+            if (is_lookup(g.op) && (g.flags & (GXF_FETCH | GXF_W32))) targets.insert((uint32_t)g.imm);
+        }
+        std::vector<GxInsn> sched = hoist_loads(im0, n, targets);
+        const GxInsn *im = sched.data();
+        for (uint32_t t : targets) leaders.insert(t);
+        for (uint32_t i = 0; i < n; i++)
+            if (ends_block(im[i]) && i + 1 < n) leaders.insert(i + 1);
         std::set<int> slots;
         for (uint32_t i = 0; i < n; i++) {
             const GxInsn &g = im[i];
-            if (g.op == GX_JA || (g.op >= GX_JEQ && g.op <= GX_JSET32)) targets.insert(g.aux);
-            if ((g.op == GX_CALL_LOOKUP_ARRAY || g.op == GX_CALL_LOOKUP_PT || g.op == GX_CALL_LOOKUP_HASH) &&
-                (g.flags & (GXF_FETCH | GXF_W32)))
-                targets.insert((uint32_t)g.imm);
             switch (g.op) {
             case GX_LDX_STACK: case GX_ST_STACK: case GX_ATOM_STACK: slots.insert(g.off >> 3); break;
             case GX_CALL_LOOKUP_ARRAY: case GX_CALL_LOOKUP_PT: case GX_CALL_LOOKUP_HASH:
@@ -190,19 +215,45 @@ struct Gen {
             default: break;
             }
         }
-        std::vector<GxInsn> sched = hoist_loads(im, n, targets);
-        im = sched.data();
-        o << "__device__ __forceinline__ uint64_t prog" << q
-          << "(const Ctx &c, const uint32_t shard, uint32_t *spriv, unsigned long long &c_herr, "
-             "unsigned long long &c_drop, unsigned long long &c_rbb, unsigned long long &c_hfull) {\n";
-        o << "  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0, r8 = 0, r9 = 0;\n"
+        std::ostringstream body;
+        out_ = &body;
+        o << "__device__ __forceinline__ void prog" << q
+          << "(const Ctx &c, unsigned active, uint64_t &retv, const uint32_t shard, uint32_t *spriv, "
+             "unsigned long long &c_herr, unsigned long long &c_drop, unsigned long long &c_rbb, "
+             "unsigned long long &c_hfull) {\n"
+             "  const unsigned lane = threadIdx.x & 31;\n"
+             "  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0, r8 = 0, r9 = 0;\n"
              "  const uint64_t r10 = 512;\n  (void)r10; (void)spriv; (void)shard;\n";
         for (int s : slots) o << "  uint64_t s" << s << " = 0;\n";
+        o << "  unsigned exec = active;\n  bool me = (active >> lane) & 1, uni = true;\n  uint32_t pc = 0, mypc = 0;\n"
+             "  (void)pc;\n  goto B0;\n dispatch:\n  if (!active) return;\n"
+             "  { const uint32_t v_ = ((active >> lane) & 1) ? mypc : 0xFFFFFFFFu;\n"
+             "    pc = __reduce_min_sync(GX_ALL, v_);\n    exec = __ballot_sync(GX_ALL, v_ == pc);\n"
+             "    uni = exec == active;\n    me = (exec >> lane) & 1; }\n  switch (pc) {\n";
+        for (uint32_t l : leaders) o << "  case " << l << ": goto B" << l << ";\n";
+        o << "  default: active = 0; return;\n  }\n";
         for (uint32_t i = 0; i < n; i++) {
-            if (targets.count(i)) o << " L" << i << ":\n";
-            insn(im[i], i);
+            if (leaders.count(i)) body << " B" << i << ":\n";
+            const GxInsn &g = im[i];
+            insn(g, i);
+            const bool last = i + 1 >= n || leaders.count(i + 1);
+            if (last && !ends_block(g)) goto_next(i + 1); /* falls into the next block */
         }
-        o << "  return r0;\n}\n\n";
+        o << body.str();
+        o << "}\n\n";
+    }
+
+    void goto_next(uint32_t t) {
+        st("if (uni) goto B" + std::to_string(t) + "; if (me) mypc = " + std::to_string(t) + "; goto dispatch;");
+    }
+    void branch(const std::string &cond, uint32_t t, uint32_t nx) {
+        st("{ const bool t_ = me && (" + cond + "); const unsigned tb_ = __ballot_sync(GX_ALL, t_);");
+        st("  if (uni) { if (tb_ == exec) goto B" + std::to_string(t) + "; if (tb_ == 0) goto B" + std::to_string(nx) +
+           "; uni = false; }");
+        st("  if (me) mypc = t_ ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; goto dispatch; }");
+    }
+    void exit_lanes(const std::string &val) {
+        st("if (me) retv = " + val + "; active &= ~exec; if (!active) return; goto dispatch;");
     }
 
     std::string src_operand(const GxInsn &g, bool is64) {
@@ -213,116 +264,121 @@ struct Gen {
     void insn(const GxInsn &g, uint32_t i) {
         const std::string d = R(g.dst), s = R(g.src);
         const std::string S64 = src_operand(g, true), S32 = src_operand(g, false);
-        auto st = [&](const std::string &x) { o << "  " << x << "\n"; };
         const bool sxf = g.flags & GXF_SX;
         const unsigned lg = g.aux & 15;
         auto ld_fix = [&](const std::string &v) {
             return sxf ? "sx(" + v + ", " + std::to_string(8u << lg) + ")" : v;
         };
-        auto branch_cond = [&](const std::string &cond, uint32_t tgt) { st("if (" + cond + ") goto L" + std::to_string(tgt) + ";"); };
         switch (g.op) {
-        case GX_ADD64: st(d + " += " + S64 + ";"); break;
-        case GX_SUB64: st(d + " -= " + S64 + ";"); break;
-        case GX_MUL64: st(d + " *= " + S64 + ";"); break;
-        case GX_DIV64: st("{ const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " / t : 0; }"); break;
-        case GX_MOD64: st("{ const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " % t : " + d + "; }"); break;
+        case GX_ADD64: me(d + " += " + S64 + ";"); break;
+        case GX_SUB64: me(d + " -= " + S64 + ";"); break;
+        case GX_MUL64: me(d + " *= " + S64 + ";"); break;
+        case GX_DIV64: me("const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " / t : 0;"); break;
+        case GX_MOD64: me("const uint64_t t = " + S64 + "; " + d + " = t ? " + d + " % t : " + d + ";"); break;
         case GX_SDIV64:
-            st("{ const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
-               " = t == 0 ? 0 : (a == (int64_t)0x8000000000000000ll && t == -1) ? (uint64_t)a : (uint64_t)(a / t); }");
+            me("const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
+               " = t == 0 ? 0 : (a == (int64_t)0x8000000000000000ll && t == -1) ? (uint64_t)a : (uint64_t)(a / t);");
             break;
         case GX_SMOD64:
-            st("{ const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
-               " = t == 0 ? (uint64_t)a : t == -1 ? 0 : (uint64_t)(a % t); }");
+            me("const int64_t a = (int64_t)" + d + ", t = (int64_t)" + S64 + "; " + d +
+               " = t == 0 ? (uint64_t)a : t == -1 ? 0 : (uint64_t)(a % t);");
             break;
-        case GX_OR64: st(d + " |= " + S64 + ";"); break;
-        case GX_AND64: st(d + " &= " + S64 + ";"); break;
-        case GX_XOR64: st(d + " ^= " + S64 + ";"); break;
-        case GX_LSH64: st(d + " <<= (" + S64 + " & 63);"); break;
-        case GX_RSH64: st(d + " >>= (" + S64 + " & 63);"); break;
-        case GX_ARSH64: st(d + " = (uint64_t)((int64_t)" + d + " >> (" + S64 + " & 63));"); break;
-        case GX_NEG64: st(d + " = 0 - " + d + ";"); break;
-        case GX_MOV64: st(d + " = " + S64 + ";"); break;
-        case GX_MOVSX64: st(d + " = sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
-        case GX_ADD32: st(d + " = (uint32_t)((uint32_t)" + d + " + " + S32 + ");"); break;
-        case GX_SUB32: st(d + " = (uint32_t)((uint32_t)" + d + " - " + S32 + ");"); break;
-        case GX_MUL32: st(d + " = (uint32_t)((uint32_t)" + d + " * " + S32 + ");"); break;
-        case GX_DIV32: st("{ const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " / t : 0; }"); break;
-        case GX_MOD32: st("{ const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " % t : (uint32_t)" + d + "; }"); break;
+        case GX_OR64: me(d + " |= " + S64 + ";"); break;
+        case GX_AND64: me(d + " &= " + S64 + ";"); break;
+        case GX_XOR64: me(d + " ^= " + S64 + ";"); break;
+        case GX_LSH64: me(d + " <<= (" + S64 + " & 63);"); break;
+        case GX_RSH64: me(d + " >>= (" + S64 + " & 63);"); break;
+        case GX_ARSH64: me(d + " = (uint64_t)((int64_t)" + d + " >> (" + S64 + " & 63));"); break;
+        case GX_NEG64: me(d + " = 0 - " + d + ";"); break;
+        case GX_MOV64: me(d + " = " + S64 + ";"); break;
+        case GX_MOVSX64: me(d + " = sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_ADD32: me(d + " = (uint32_t)((uint32_t)" + d + " + " + S32 + ");"); break;
+        case GX_SUB32: me(d + " = (uint32_t)((uint32_t)" + d + " - " + S32 + ");"); break;
+        case GX_MUL32: me(d + " = (uint32_t)((uint32_t)" + d + " * " + S32 + ");"); break;
+        case GX_DIV32: me("const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " / t : 0;"); break;
+        case GX_MOD32: me("const uint32_t t = " + S32 + "; " + d + " = t ? (uint32_t)" + d + " % t : (uint32_t)" + d + ";"); break;
         case GX_SDIV32:
-            st("{ const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
-               " = (uint32_t)(t == 0 ? 0 : (a == (int32_t)0x80000000 && t == -1) ? a : a / t); }");
+            me("const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
+               " = (uint32_t)(t == 0 ? 0 : (a == (int32_t)0x80000000 && t == -1) ? a : a / t);");
             break;
         case GX_SMOD32:
-            st("{ const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
-               " = (uint32_t)(t == 0 ? a : t == -1 ? 0 : a % t); }");
+            me("const int32_t a = (int32_t)" + d + ", t = (int32_t)" + S32 + "; " + d +
+               " = (uint32_t)(t == 0 ? a : t == -1 ? 0 : a % t);");
             break;
-        case GX_OR32: st(d + " = (uint32_t)" + d + " | " + S32 + ";"); break;
-        case GX_AND32: st(d + " = (uint32_t)" + d + " & " + S32 + ";"); break;
-        case GX_XOR32: st(d + " = (uint32_t)" + d + " ^ " + S32 + ";"); break;
-        case GX_LSH32: st(d + " = (uint32_t)((uint32_t)" + d + " << (" + S32 + " & 31));"); break;
-        case GX_RSH32: st(d + " = (uint32_t)" + d + " >> (" + S32 + " & 31);"); break;
-        case GX_ARSH32: st(d + " = (uint32_t)((int32_t)" + d + " >> (" + S32 + " & 31));"); break;
-        case GX_NEG32: st(d + " = (uint32_t)(0u - (uint32_t)" + d + ");"); break;
-        case GX_MOV32: st(d + " = (uint32_t)(" + S32 + ");"); break;
-        case GX_MOVSX32: st(d + " = (uint32_t)sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_OR32: me(d + " = (uint32_t)" + d + " | " + S32 + ";"); break;
+        case GX_AND32: me(d + " = (uint32_t)" + d + " & " + S32 + ";"); break;
+        case GX_XOR32: me(d + " = (uint32_t)" + d + " ^ " + S32 + ";"); break;
+        case GX_LSH32: me(d + " = (uint32_t)((uint32_t)" + d + " << (" + S32 + " & 31));"); break;
+        case GX_RSH32: me(d + " = (uint32_t)" + d + " >> (" + S32 + " & 31);"); break;
+        case GX_ARSH32: me(d + " = (uint32_t)((int32_t)" + d + " >> (" + S32 + " & 31));"); break;
+        case GX_NEG32: me(d + " = (uint32_t)(0u - (uint32_t)" + d + ");"); break;
+        case GX_MOV32: me(d + " = (uint32_t)(" + S32 + ");"); break;
+        case GX_MOVSX32: me(d + " = (uint32_t)sx(" + s + ", " + std::to_string(g.aux) + ");"); break;
         case GX_LE:
-            if (g.aux < 64) st(d + " &= " + hex((1ull << g.aux) - 1) + ";");
+            if (g.aux < 64) me(d + " &= " + hex((1ull << g.aux) - 1) + ";");
             break;
-        case GX_BE: st(d + " = bswap_w(" + d + ", " + std::to_string(g.aux) + ");"); break;
+        case GX_BE: me(d + " = bswap_w(" + d + ", " + std::to_string(g.aux) + ");"); break;
         case GX_LDIMM:
-            if (g.flags & GXF_VAL_MAPV) st(d + " = " + hex(L.maps[g.aux].data + g.imm) + ";");
-            else st(d + " = " + hex(g.imm) + ";");
+            if (g.flags & GXF_VAL_MAPV) me(d + " = " + hex(L.maps[g.aux].data + g.imm) + ";");
+            else me(d + " = " + hex(g.imm) + ";");
             break;
-        case GX_JA: st("goto L" + std::to_string(g.aux) + ";"); break;
-        case GX_EXIT: st(std::string("return ") + ((g.flags & GXF_SX) ? hex(g.imm) : "r0") + ";"); break;
-        case GX_LDX_CTX: st(d + " = " + ld_fix("ctx_ld(c, " + std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";"); break;
+        case GX_JA:
+            st("if (uni) goto B" + std::to_string(g.aux) + "; if (me) mypc = " + std::to_string(g.aux) + "; goto dispatch;");
+            break;
+        case GX_EXIT: exit_lanes((g.flags & GXF_SX) ? hex(g.imm) : "r0"); break;
+        case GX_OP_NOP:
+            st("if (me) c_herr++;");
+            exit_lanes("0");
+            break;
+        case GX_LDX_CTX: me(d + " = " + ld_fix("ctx_ld(c, " + std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";"); break;
         case GX_LDX_STACK:
-            st(d + " = " + ld_fix("zx(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ", " + std::to_string(lg) + ")") + ";");
+            me(d + " = " + ld_fix("zx(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ", " + std::to_string(lg) + ")") + ";");
             break;
         case GX_LDX_MAP: {
             const bool coh = L.maps[g.imm].coherent;
-            st(d + " = " + ld_fix(std::string("gload<") + (coh ? "true" : "false") + ">(" + s + " + (int64_t)" +
+            me(d + " = " + ld_fix(std::string("gload<") + (coh ? "true" : "false") + ">(" + s + " + (int64_t)" +
                                   std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";");
             break;
         }
         case GX_LDX_PT:
-            st(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
+            me(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
                                   std::to_string(g.off) + ", shard), " + std::to_string(lg) + ")") + ";");
             break;
         case GX_ST_STACK: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            st(slot(g.off) + " = word_set(" + slot(g.off) + ", " + std::to_string(g.off & 7) + ", " + std::to_string(lg) + ", " + v + ");");
+            me(slot(g.off) + " = word_set(" + slot(g.off) + ", " + std::to_string(g.off & 7) + ", " + std::to_string(lg) + ", " + v + ");");
             break;
         }
         case GX_ST_MAP: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            st("gstore(" + d + " + (int64_t)" + std::to_string(g.off) + ", " + std::to_string(lg) + ", " + v + ");");
+            me("gstore(" + d + " + (int64_t)" + std::to_string(g.off) + ", " + std::to_string(lg) + ", " + v + ");");
             break;
         }
         case GX_ST_PT: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            st("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
+            me("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
                ", shard), " + std::to_string(lg) + ", " + v + ");");
             break;
         }
         case GX_ATOM_STACK: case GX_ATOM_PT: case GX_ATOM_MAP: atomic(g); break;
         case GX_CALL_LOOKUP_ARRAY: case GX_CALL_LOOKUP_PT: case GX_CALL_LOOKUP_HASH: {
             const GxMapDesc &m = L.maps[g.aux];
-            std::string key;
             if (g.op == GX_CALL_LOOKUP_HASH) {
-                key = (g.flags & GXF_KEY_MAPV)
-                          ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
-                          : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+                std::string key = (g.flags & GXF_KEY_MAPV)
+                                      ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
+                                      : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
-                st("r0 = (uint64_t)jit_hash_find(" + md(g.aux) + ", " + key + ");");
+                st("{ uint64_t k_ = 0; if (me) k_ = " + key + "; uint64_t *v_ = gxd::hash_lookup_coop(" + md(g.aux) +
+                   ", k_, me, GX_ALL); if (me) r0 = (uint64_t)v_; }");
             } else {
-                key = (g.flags & GXF_KEY_MAPV) ? "*(const uint32_t *)r2"
-                                               : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
-                st("{ const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
-                   " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0; }");
+                const std::string key = (g.flags & GXF_KEY_MAPV)
+                                            ? "*(const uint32_t *)r2"
+                                            : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
+                me("const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
+                   " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0;");
             }
-            if (g.flags & GXF_FETCH) branch_cond("r0 == 0", (uint32_t)g.imm);
-            if (g.flags & GXF_W32) branch_cond("r0 != 0", (uint32_t)g.imm);
+            if (g.flags & GXF_FETCH) branch("r0 == 0", (uint32_t)g.imm, i + 1);
+            if (g.flags & GXF_W32) branch("r0 != 0", (uint32_t)g.imm, i + 1);
             break;
         }
         case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: {
@@ -331,19 +387,18 @@ struct Gen {
                                         ? "*(const uint32_t *)r2"
                                         : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             std::ostringstream b;
-            b << "{ const uint32_t k = " << key << "; int64_t rc = 0;\n"
-              << "    if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17;\n"
-              << "    else {\n";
+            b << "const uint32_t k = " << key << "; int64_t rc = 0;"
+              << " if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17; else {";
             for (uint32_t w = 0; w < m.value_size / 8; w++) {
                 const std::string v = (g.flags & GXF_VAL_MAPV) ? "((const uint64_t *)r3)[" + std::to_string(w) + "]"
                                                                : "s" + std::to_string((uint32_t)g.imm / 8 + w);
                 const std::string logical = hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u + " +
                                             std::to_string(8 * w);
-                if (g.op == GX_CALL_UPDATE_ARRAY) b << "      *(uint64_t *)(" << logical << ") = " << v << ";\n";
-                else b << "      *(uint64_t *)gxd::pt_phys(" << md(g.aux) << ", " << logical << ", shard) = " << v << ";\n";
+                if (g.op == GX_CALL_UPDATE_ARRAY) b << " *(uint64_t *)(" << logical << ") = " << v << ";";
+                else b << " *(uint64_t *)gxd::pt_phys(" << md(g.aux) << ", " << logical << ", shard) = " << v << ";";
             }
-            b << "    }\n    if (rc) c_herr++; r0 = (uint64_t)rc; }";
-            st(b.str());
+            b << " } if (rc) c_herr++; r0 = (uint64_t)rc;";
+            me(b.str());
             break;
         }
         case GX_CALL_UPDATE_HASH: {
@@ -353,14 +408,15 @@ struct Gen {
                                   : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
             const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
-            st("{ bool full; const int64_t rc = jit_hash_update(" + md(g.aux) + ", " + key + ", " + v +
-               ", r4, full); if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
+            st("{ uint64_t k_ = 0, v_ = 0, f_ = 0; if (me) { k_ = " + key + "; v_ = " + v + "; f_ = r4; } bool full = false;");
+            st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, f_, full, me, GX_ALL);");
+            st("  if (me) { if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; } }");
             break;
         }
         case GX_CALL_RINGBUF_OUTPUT: {
             const uint32_t size = (uint32_t)g.imm, flags = (uint32_t)(g.imm >> 32);
             if (flags > 2) {
-                st("r0 = (uint64_t)(int64_t)-22; c_herr++;");
+                me("r0 = (uint64_t)(int64_t)-22; c_herr++;");
                 break;
             }
             std::ostringstream b;
@@ -371,14 +427,13 @@ struct Gen {
                 for (uint32_t k = 0; k < (size + 7) / 8; k++) b << (k ? ", " : "") << "s" << ((uint16_t)g.off / 8 + k);
                 b << "};";
             }
-            b << " r0 = (uint64_t)ringbuf_output(" << md(g.aux) << ", w, " << size << "u, c_drop, c_rbb);"
-              << " if (r0) c_herr++; }";
+            b << " const int64_t rc = ringbuf2(me, " << md(g.aux) << ", w, " << size << "u, c_drop, c_rbb);"
+              << " if (me) { r0 = (uint64_t)rc; if (rc) c_herr++; } }";
             st(b.str());
             break;
         }
-        case GX_OP_NOP: st("{ c_herr++; return 0; }"); break;
         default:
-            if (g.op >= GX_JEQ && g.op <= GX_JSET32) {
+            if (is_jcc(g.op)) {
                 const bool is32 = g.op >= GX_JEQ32;
                 const int cop = is32 ? g.op - (GX_JEQ32 - GX_JEQ) : g.op;
                 std::string a = is32 ? "(uint32_t)" + d : d;
@@ -399,12 +454,12 @@ struct Gen {
                 case GX_JSLE: c = sa + " <= " + sb; break;
                 default: c = "(" + a + " & " + b + ") != 0"; break;
                 }
-                branch_cond(c, g.aux);
+                branch(c, g.aux, i + 1);
             } else {
-                st("{ c_herr++; return 0; }");
+                st("if (me) c_herr++;");
+                exit_lanes("0");
             }
         }
-        (void)i;
     }
 
     void atomic(const GxInsn &g) {
@@ -412,11 +467,10 @@ struct Gen {
         const bool w32 = (g.aux & 15) == 2, fetch = op & 1, kop = g.flags & GXF_PRIV;
         const std::string v = kop ? hex((uint64_t)(int64_t)(int32_t)(g.imm >> 32)) : R(g.src);
         const std::string ret = op == 0xF1 ? "r0" : R(g.src);
-        auto st = [&](const std::string &x) { o << "  " << x << "\n"; };
         if (g.op == GX_ATOM_STACK) {
             std::string e = "rmw_word(" + slot(g.off) + ", " + std::to_string(g.off & 7) + ", " + (w32 ? "true" : "false") +
                             ", " + std::to_string(op) + "u, " + v + ", r0)";
-            st(fetch ? "{ const uint64_t old = " + e + "; " + ret + " = old; }" : "(void)" + e + ";");
+            me(fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";");
             return;
         }
         const int fd = g.aux >> 4;
@@ -424,85 +478,96 @@ struct Gen {
         if (g.op == GX_ATOM_PT) {
             std::string e = "rmw_global_private((uint64_t)gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
                             (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
-            st(fetch ? "{ const uint64_t old = " + e + "; " + ret + " = old; }" : "(void)" + e + ";");
+            me(fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";");
             return;
         }
-        /* shared map value */
         if (op == 0xE1) {
-            st(R(g.src) + " = " + (w32 ? "atomicExch((unsigned *)(" + addr + "), (uint32_t)" + v + ")"
+            me(R(g.src) + " = " + (w32 ? "atomicExch((unsigned *)(" + addr + "), (uint32_t)" + v + ")"
                                        : "atomicExch((unsigned long long *)(" + addr + "), " + v + ")") + ";");
             return;
         }
         if (op == 0xF1) {
-            st("r0 = " + (w32 ? "atomicCAS((unsigned *)(" + addr + "), (uint32_t)r0, (uint32_t)" + v + ")"
+            me("r0 = " + (w32 ? "atomicCAS((unsigned *)(" + addr + "), (uint32_t)r0, (uint32_t)" + v + ")"
                                : "atomicCAS((unsigned long long *)(" + addr + "), r0, " + v + ")") + ";");
             return;
         }
         const GxMapDesc &m = L.maps[fd];
         if (m.priv_off != 0xFFFFFFFFu && !fetch && (op & 0xF0) == 0 && !w32) {
             const uint32_t nw = m.max_entries * m.value_size / 8;
-            st("priv_add(spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
+            st("priv_add2(me, spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
                ", (uint32_t)((" + addr + " - " + hex(m.data) + ") >> 3), " + v + ");");
             return;
         }
-        std::string e = "warp_atomic<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
-                        (fetch ? "true" : "false") + ">(" + addr + ", " + v + ")";
-        st(fetch ? R(g.src) + " = " + e + ";" : "(void)" + e + ";");
+        std::string e = "atomic2<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
+                        (fetch ? "true" : "false") + ">(me, " + addr + ", " + v + ")";
+        if (fetch) st("{ const uint64_t res_ = " + e + "; if (me) " + R(g.src) + " = res_; }");
+        else st("(void)" + e + ";");
     }
 
     void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes, int B) {
         int U = 2;
         if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
-        if (getenv("GX_JIT_NOCOOP")) o << "#define GX_NOCOOP 1\n";
-        if (getenv("GX_JIT_NOWARPAGG")) o << "#define GX_NOWARPAGG 1\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
-        o << "extern \"C\" __global__ void __launch_bounds__(" << B << ") gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
-             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
+        o << "extern \"C\" __global__ void __launch_bounds__(" << B << ") gx_jit_kernel(const uint4 *__restrict__ ev, "
+             "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
              "  for (uint32_t k = threadIdx.x; k < " << priv_words << "u; k += " << B << ") spriv[k] = 0;\n"
              "  if (threadIdx.x < 8) sstats[threadIdx.x] = 0;\n"
              "  __syncthreads();\n"
+             "  const uint32_t lane = threadIdx.x & 31;\n"
              "  const uint32_t shard = blockIdx.x * " << B << " + threadIdx.x;\n"
              "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
-             "  const uint64_t stride = (uint64_t)gridDim.x * " << B << ";\n"
+             "  const uint64_t nrec = (n + 31) >> 5;\n"
+             "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
              "  const uint64_t pol = evict_first_policy();\n"
-             "  /* U events per thread per iteration: their 2*U 16-B loads are issued back to back */\n"
-             "  for (uint64_t i0 = (uint64_t)blockIdx.x * " << B << " + threadIdx.x; i0 < n; i0 += stride * " << U << ") {\n"
+             "  /* one warp = one 32-event record at a time (event lane == executor lane); U records per\n"
+             "   * iteration, their loads issued back to back */\n"
+             "  for (uint64_t rb = (uint64_t)blockIdx.x * " << B / 32 << " + (threadIdx.x >> 5); rb < nrec; rb += nwarps * " << U << ") {\n"
              "    uint4 ea[" << U << "], eb[" << U << "];\n"
              "    #pragma unroll\n"
              "    for (int u = 0; u < " << U << "; u++) {\n"
-             "      const uint64_t i = i0 + u * stride;\n"
+             "      const uint64_t i = (rb + u * nwarps) * 32 + lane;\n"
              "      if (i < n) { ea[u] = ldg_stream_ef(ev + 2 * i, pol); eb[u] = ldg_stream_ef(ev + 2 * i + 1, pol); }\n"
              "    }\n"
              "    #pragma unroll\n"
              "    for (int u = 0; u < " << U << "; u++) {\n"
-             "    const uint64_t i = i0 + u * stride;\n"
-             "    if (i >= n) break;\n"
+             "    const uint64_t rec = rb + u * nwarps;\n"
+             "    if (rec >= nrec) break;\n"
+             "    const uint64_t i = rec * 32 + lane;\n"
+             "    const bool valid = i < n;\n"
              "    const uint4 a = ea[u], b = eb[u];\n"
-             "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n";
+             "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
+             "    int p = -1;\n";
         if (L.single >= 0) {
-            o << "    const int p = 0;\n";
+            o << "    if (valid) p = 0;\n";
         } else {
-            o << "    int p = -1;\n    { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
+            o << "    if (valid) { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
             for (int k = 0; k < GX_MAX_KINDS; k++)
                 for (int t = 0; t < 256; t++)
                     if (L.attach[k][t] >= 0) o << "      case " << k * 256 + t << ": p = " << (int)L.attach[k][t] << "; break;\n";
             o << "      default: break;\n      }\n    }\n";
         }
-        o << "    uint64_t r = 0;\n    switch (p) {\n";
+        o << "    uint64_t retv = 0;\n"
+             "    if (valid) { if (p >= 0) c_run++; else c_skip++; }\n"
+             "    unsigned todo = __ballot_sync(GX_ALL, p >= 0);\n"
+             "    while (todo) {\n"
+             "      const int pq = __shfl_sync(GX_ALL, p, __ffs(todo) - 1);\n"
+             "      const unsigned m = __ballot_sync(GX_ALL, p == pq) & todo;\n"
+             "      todo &= ~m;\n"
+             "      switch (pq) {\n";
         for (size_t q = 0; q < images.size(); q++)
-            o << "    case " << q << ": r = prog" << q << "(c, shard, spriv, c_herr, c_drop, c_rbb, c_hfull); c_run++; break;\n";
-        o << "    default: c_skip++; break;\n    }\n"
-             "    if (ret) ret[i] = r;\n    }\n  }\n";
+            o << "      case " << q << ": prog" << q << "(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull); break;\n";
+        o << "      default: break;\n      }\n    }\n"
+             "    if (ret && valid) ret[i] = retv;\n    }\n  }\n";
         o << "  for (int s = 16; s; s >>= 1) {\n"
-             "    c_run += __shfl_xor_sync(0xFFFFFFFFu, c_run, s); c_skip += __shfl_xor_sync(0xFFFFFFFFu, c_skip, s);\n"
-             "    c_herr += __shfl_xor_sync(0xFFFFFFFFu, c_herr, s); c_drop += __shfl_xor_sync(0xFFFFFFFFu, c_drop, s);\n"
-             "    c_rbb += __shfl_xor_sync(0xFFFFFFFFu, c_rbb, s); c_hfull += __shfl_xor_sync(0xFFFFFFFFu, c_hfull, s);\n"
+             "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
+             "    c_herr += __shfl_xor_sync(GX_ALL, c_herr, s); c_drop += __shfl_xor_sync(GX_ALL, c_drop, s);\n"
+             "    c_rbb += __shfl_xor_sync(GX_ALL, c_rbb, s); c_hfull += __shfl_xor_sync(GX_ALL, c_hfull, s);\n"
              "  }\n"
-             "  if ((threadIdx.x & 31) == 0) {\n"
+             "  if (lane == 0) {\n"
              "    if (c_run) atomicAdd(&sstats[" << GXS_RUN << "], c_run);\n"
              "    if (c_skip) atomicAdd(&sstats[" << GXS_SKIP << "], c_skip);\n"
              "    if (c_herr) atomicAdd(&sstats[" << GXS_HERR << "], c_herr);\n"

@@ -321,4 +321,113 @@ __device__ __forceinline__ int64_t jit_hash_update(const GxMapDesc &m, uint64_t 
     return gxd::hash_update(m, key, val, flags, full);
 }
 
+/* ---------------------------------------------------------------------------------------------
+ * Convergent (v2) helpers.  JIT v2 code keeps all 32 lanes of a warp together: basic blocks run
+ * under a per-lane `me` predicate (uniform-PC fast path with direct block-to-block jumps, min-PC
+ * dispatch when lanes diverge -- the interpreter's scheme, compiled), so every helper below is
+ * called by the whole warp and may use full-mask warp collectives; `me` marks the lanes whose
+ * event executes the helper. */
+#define GX_ALL 0xFFFFFFFFu
+
+template <uint32_t OP, bool W32, bool FETCH>
+__device__ __forceinline__ uint64_t atomic2(bool me, uint64_t addr, uint64_t v) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned part = __ballot_sync(GX_ALL, me);
+    if (!part) return 0;
+    const unsigned leader = __ffs(part) - 1;
+    const uint64_t a0 = __shfl_sync(GX_ALL, addr, leader);
+    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    const uint64_t mine = me ? v : ident;
+    if (__all_sync(GX_ALL, !me || addr == a0)) {
+        if (!FETCH) {
+            const uint64_t agg = group_reduce(GX_ALL, OP, mine, W32);
+            if (lane == leader) global_atomic(OP, a0, agg, W32, false);
+            return 0;
+        }
+        uint64_t inc = W32 ? (uint32_t)mine : mine;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(GX_ALL, inc, d);
+            if ((int)lane >= d) inc = apply_op(OP, inc, o);
+        }
+        if (W32) inc = (uint32_t)inc;
+        const uint64_t tot = __shfl_sync(GX_ALL, inc, 31);
+        uint64_t old = 0;
+        if (lane == leader) old = global_atomic(OP, a0, tot, W32, true);
+        old = __shfl_sync(GX_ALL, old, leader);
+        uint64_t exc = __shfl_up_sync(GX_ALL, inc, 1);
+        if (lane == 0) exc = ident;
+        const uint64_t r = apply_op(OP, old, exc);
+        return W32 ? (uint32_t)r : r;
+    }
+    if (!FETCH) {
+        if (me) global_atomic(OP, addr, v, W32, false);
+        return 0;
+    }
+    const unsigned peers = __match_any_sync(GX_ALL, me ? addr : 0ull);
+    uint64_t res = 0;
+    if (me) {
+        const unsigned gl = __ffs(peers) - 1;
+        uint64_t pre = ident, tot = ident;
+        for (unsigned m = peers; m; m &= m - 1) {
+            const int jl = __ffs(m) - 1;
+            const uint64_t vj = __shfl_sync(peers, v, jl);
+            if (jl < (int)lane) pre = apply_op(OP, pre, vj);
+            tot = apply_op(OP, tot, vj);
+        }
+        uint64_t old = 0;
+        if (lane == gl) old = global_atomic(OP, addr, tot, W32, true);
+        old = __shfl_sync(peers, old, gl);
+        res = apply_op(OP, old, pre);
+        if (W32) res = (uint32_t)res;
+    }
+    return res;
+}
+
+__device__ __forceinline__ void priv_add2(bool me, uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
+    const unsigned part = __ballot_sync(GX_ALL, me);
+    if (!part) return;
+    const unsigned leader = __ffs(part) - 1;
+    const uint32_t w0 = __shfl_sync(GX_ALL, w, leader);
+    if (__all_sync(GX_ALL, !me || w == w0)) {
+        const uint64_t agg = group_sum64(GX_ALL, me ? v : 0);
+        if ((threadIdx.x & 31) == leader) priv_one(lo, hi, w0, agg);
+    } else if (me) {
+        priv_one(lo, hi, w, v);
+    }
+}
+
+__device__ __forceinline__ int64_t ringbuf2(bool me, const GxMapDesc &md, const uint64_t *words, uint32_t size,
+                                            unsigned long long &drops, unsigned long long &bytes) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned act = __ballot_sync(GX_ALL, me);
+    if (!act) return 0;
+    const uint64_t recb = (8 + size + 7) & ~7u;
+    const uint32_t cnt = __popc(act), rank = __popc(act & ((1u << lane) - 1));
+    const uint32_t leader = __ffs(act) - 1;
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(md.aux);
+    uint64_t base = 0;
+    if (lane == leader) base = atomicAdd(&ctr[0], (unsigned long long)(cnt * recb));
+    base = __shfl_sync(GX_ALL, base, leader);
+    const uint64_t o = base + rank * recb;
+    const bool ok = me && (o + recb <= (uint64_t)md.cap_mask + 1);
+    if (ok) {
+        uint64_t *dst = reinterpret_cast<uint64_t *>(md.data + o);
+        dst[0] = (uint64_t)size | ((o >> 12) << 32);
+        const uint32_t nw = (size + 7) / 8;
+        for (uint32_t w = 0; w < nw; w++) {
+            uint64_t v = words[w];
+            if (w == nw - 1 && (size & 7)) v &= (1ull << (8 * (size & 7))) - 1;
+            dst[1 + w] = v;
+        }
+    } else if (me) {
+        drops++;
+    }
+    const uint32_t nok = __popc(__ballot_sync(GX_ALL, ok));
+    if (nok && lane == leader) {
+        atomicAdd(&ctr[1], (unsigned long long)(nok * recb));
+        bytes += nok * recb;
+    }
+    return ok ? 0 : -(int64_t)gxd::E_AGAIN;
+}
+
 }  // namespace gxj
