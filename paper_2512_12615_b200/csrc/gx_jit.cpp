@@ -169,15 +169,20 @@ struct Gen {
     }
 
     std::ostringstream *out_ = nullptr;
+    bool dmode_ = false; /* emitting the min-PC (diverged) copy of a block */
     void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
-    void me(const std::string &x) { (*out_) << "  if (me) { " << x << " }\n"; }
+    void me(const std::string &x) { (*out_) << "  { " << x << " }\n"; }
+    std::string M() const { return dmode_ ? "exec" : "active"; }
 
-    /* SIMT-convergent code (v2): the whole warp runs every program; basic blocks execute under a
-     * per-lane `me` predicate.  Uniform-PC fast path: while all active lanes agree, blocks jump
-     * straight to their successor after one ballot per branch.  On a split, the min-PC dispatcher
-     * (__reduce_min_sync over the lanes' next-block ids) runs one block at a time for the lanes at
-     * the lowest id until they meet again -- the interpreter's a3 scheme at basic-block granularity.
-     * Every helper that uses warp collectives is therefore called by all 32 lanes. */
+    /* SIMT-convergent code.  prog<q>(ctx, active, ...) is called by all 32 lanes; `active` is the
+     * group of lanes whose event runs program q, and the other lanes return at once.  Uniform copy
+     * (labels U<pc>): the group runs every basic block together and branches with one ballot --
+     * all taken / none taken jump straight on.  When the group splits, every lane records its next
+     * block in `mypc` and enters the min-PC loop (DIV): the lanes at the lowest block id (`exec`)
+     * run that block's diverged copy, and once the live lanes all wait at one block again they
+     * re-enter the uniform copy there.  This is the interpreter's a3 scheme at basic-block
+     * granularity, and it makes the lane group known at every helper call: the helpers' warp
+     * collectives take `active` (uniform copy) or `exec` (diverged copy) as their mask. */
     void program(int q, const GxInsn *im0, uint32_t n) {
         std::set<uint32_t> targets, leaders{0};
         for (uint32_t i = 0; i < n; i++) {
@@ -215,45 +220,68 @@ struct Gen {
             default: break;
             }
         }
-        std::ostringstream body;
-        out_ = &body;
+        std::vector<std::pair<uint32_t, uint32_t>> blocks; /* [start, end) */
+        for (auto it = leaders.begin(); it != leaders.end(); ++it) {
+            auto nx = std::next(it);
+            blocks.push_back({*it, nx == leaders.end() ? n : *nx});
+        }
         o << "__device__ __forceinline__ void prog" << q
           << "(const Ctx &c, unsigned active, uint64_t &retv, const uint32_t shard, uint32_t *spriv, "
              "unsigned long long &c_herr, unsigned long long &c_drop, unsigned long long &c_rbb, "
              "unsigned long long &c_hfull) {\n"
              "  const unsigned lane = threadIdx.x & 31;\n"
+             "  if (!((active >> lane) & 1)) return;\n"
              "  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0, r8 = 0, r9 = 0;\n"
              "  const uint64_t r10 = 512;\n  (void)r10; (void)spriv; (void)shard;\n";
         for (int s : slots) o << "  uint64_t s" << s << " = 0;\n";
-        o << "  unsigned exec = active;\n  bool me = (active >> lane) & 1, uni = true;\n  uint32_t pc = 0, mypc = 0;\n"
-             "  (void)pc;\n  goto B0;\n dispatch:\n  if (!active) return;\n"
-             "  { const uint32_t v_ = ((active >> lane) & 1) ? mypc : 0xFFFFFFFFu;\n"
-             "    pc = __reduce_min_sync(GX_ALL, v_);\n    exec = __ballot_sync(GX_ALL, v_ == pc);\n"
-             "    uni = exec == active;\n    me = (exec >> lane) & 1; }\n  switch (pc) {\n";
-        for (uint32_t l : leaders) o << "  case " << l << ": goto B" << l << ";\n";
-        o << "  default: active = 0; return;\n  }\n";
-        for (uint32_t i = 0; i < n; i++) {
-            if (leaders.count(i)) body << " B" << i << ":\n";
-            const GxInsn &g = im[i];
-            insn(g, i);
-            const bool last = i + 1 >= n || leaders.count(i + 1);
-            if (last && !ends_block(g)) goto_next(i + 1); /* falls into the next block */
+        o << "  uint32_t mypc = 0;\n  (void)mypc;\n";
+        std::ostringstream body;
+        out_ = &body;
+        /* uniform copy */
+        dmode_ = false;
+        for (auto [b, e] : blocks) {
+            body << " U" << b << ":\n";
+            for (uint32_t i = b; i < e; i++) insn(im[i], i);
+            if (e > b && !ends_block(im[e - 1])) goto_next(e);
         }
+        /* min-PC copy */
+        body << " DIV:\n  for (;;) {\n"
+                "  const uint32_t pc_ = __reduce_min_sync(active, mypc);\n"
+                "  if (pc_ == 0xFFFFFFFFu) return;\n"
+                "  const unsigned exec = __ballot_sync(active, mypc == pc_);\n"
+                "  const unsigned live = __ballot_sync(active, mypc != 0xFFFFFFFFu);\n"
+                "  if (exec == live) {\n    if (mypc == 0xFFFFFFFFu) return;\n    active = live;\n    switch (pc_) {\n";
+        for (auto [b, e] : blocks) body << "    case " << b << ": goto U" << b << ";\n";
+        body << "    default: return;\n    }\n  }\n  if (mypc != pc_) continue;\n  switch (pc_) {\n";
+        dmode_ = true;
+        for (auto [b, e] : blocks) {
+            body << "  case " << b << ": {\n";
+            for (uint32_t i = b; i < e; i++) insn(im[i], i);
+            if (e > b && !ends_block(im[e - 1])) goto_next(e);
+            body << "  }\n";
+        }
+        body << "  default: mypc = 0xFFFFFFFFu; continue;\n  }\n  }\n";
+        dmode_ = false;
         o << body.str();
         o << "}\n\n";
     }
 
     void goto_next(uint32_t t) {
-        st("if (uni) goto B" + std::to_string(t) + "; if (me) mypc = " + std::to_string(t) + "; goto dispatch;");
+        if (dmode_) st("mypc = " + std::to_string(t) + "u; continue;");
+        else st("goto U" + std::to_string(t) + ";");
     }
     void branch(const std::string &cond, uint32_t t, uint32_t nx) {
-        st("{ const bool t_ = me && (" + cond + "); const unsigned tb_ = __ballot_sync(GX_ALL, t_);");
-        st("  if (uni) { if (tb_ == exec) goto B" + std::to_string(t) + "; if (tb_ == 0) goto B" + std::to_string(nx) +
-           "; uni = false; }");
-        st("  if (me) mypc = t_ ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; goto dispatch; }");
+        if (dmode_) {
+            st("mypc = (" + cond + ") ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; continue;");
+            return;
+        }
+        st("{ const bool t_ = " + cond + "; const unsigned tb_ = __ballot_sync(active, t_);");
+        st("  if (tb_ == active) goto U" + std::to_string(t) + "; if (tb_ == 0) goto U" + std::to_string(nx) + ";");
+        st("  mypc = t_ ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; goto DIV; }");
     }
     void exit_lanes(const std::string &val) {
-        st("if (me) retv = " + val + "; active &= ~exec; if (!active) return; goto dispatch;");
+        if (dmode_) st("retv = " + val + "; mypc = 0xFFFFFFFFu; continue;");
+        else st("retv = " + val + "; return;");
     }
 
     std::string src_operand(const GxInsn &g, bool is64) {
@@ -323,11 +351,11 @@ struct Gen {
             else me(d + " = " + hex(g.imm) + ";");
             break;
         case GX_JA:
-            st("if (uni) goto B" + std::to_string(g.aux) + "; if (me) mypc = " + std::to_string(g.aux) + "; goto dispatch;");
+            goto_next(g.aux);
             break;
         case GX_EXIT: exit_lanes((g.flags & GXF_SX) ? hex(g.imm) : "r0"); break;
         case GX_OP_NOP:
-            st("if (me) c_herr++;");
+            st("c_herr++;");
             exit_lanes("0");
             break;
         case GX_LDX_CTX: me(d + " = " + ld_fix("ctx_ld(c, " + std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";"); break;
@@ -368,8 +396,8 @@ struct Gen {
                                       ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
                                       : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
-                st("{ uint64_t k_ = 0; if (me) k_ = " + key + "; uint64_t *v_ = gxd::hash_lookup_coop(" + md(g.aux) +
-                   ", k_, me, GX_ALL); if (me) r0 = (uint64_t)v_; }");
+                st("{ const uint64_t k_ = " + key + "; r0 = (uint64_t)gxd::hash_lookup_coop(" + md(g.aux) + ", k_, true, " +
+                   M() + "); }");
             } else {
                 const std::string key = (g.flags & GXF_KEY_MAPV)
                                             ? "*(const uint32_t *)r2"
@@ -408,9 +436,9 @@ struct Gen {
                                   : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
             const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
-            st("{ uint64_t k_ = 0, v_ = 0, f_ = 0; if (me) { k_ = " + key + "; v_ = " + v + "; f_ = r4; } bool full = false;");
-            st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, f_, full, me, GX_ALL);");
-            st("  if (me) { if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; } }");
+            st("{ const uint64_t k_ = " + key + ", v_ = " + v + "; bool full = false;");
+            st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, r4, full, true, " + M() + ");");
+            st("  if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
             break;
         }
         case GX_CALL_RINGBUF_OUTPUT: {
@@ -427,8 +455,8 @@ struct Gen {
                 for (uint32_t k = 0; k < (size + 7) / 8; k++) b << (k ? ", " : "") << "s" << ((uint16_t)g.off / 8 + k);
                 b << "};";
             }
-            b << " const int64_t rc = ringbuf2(me, " << md(g.aux) << ", w, " << size << "u, c_drop, c_rbb);"
-              << " if (me) { r0 = (uint64_t)rc; if (rc) c_herr++; } }";
+            b << " const int64_t rc = group_ringbuf(" << M() << ", " << md(g.aux) << ", w, " << size << "u, c_drop, c_rbb);"
+              << " r0 = (uint64_t)rc; if (rc) c_herr++; }";
             st(b.str());
             break;
         }
@@ -456,7 +484,7 @@ struct Gen {
                 }
                 branch(c, g.aux, i + 1);
             } else {
-                st("if (me) c_herr++;");
+                st("c_herr++;");
                 exit_lanes("0");
             }
         }
@@ -494,23 +522,28 @@ struct Gen {
         const GxMapDesc &m = L.maps[fd];
         if (m.priv_off != 0xFFFFFFFFu && !fetch && (op & 0xF0) == 0 && !w32) {
             const uint32_t nw = m.max_entries * m.value_size / 8;
-            st("priv_add2(me, spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
+            st("group_priv_add(" + M() + ", spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
                ", (uint32_t)((" + addr + " - " + hex(m.data) + ") >> 3), " + v + ");");
             return;
         }
-        std::string e = "atomic2<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
-                        (fetch ? "true" : "false") + ">(me, " + addr + ", " + v + ")";
-        if (fetch) st("{ const uint64_t res_ = " + e + "; if (me) " + R(g.src) + " = res_; }");
+        std::string e = "group_atomic<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
+                        (fetch ? "true" : "false") + ">(" + M() + ", " + addr + ", " + v + ")";
+        if (fetch) st("{ const uint64_t res_ = " + e + "; " + R(g.src) + " = res_; }");
         else st("(void)" + e + ";");
     }
 
     void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes, int B) {
         int U = 2;
         if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
+        /* GX_JIT_MINB: min resident blocks per SM in __launch_bounds__ (default 1: up to 64 registers
+         * at 1024 threads -- without it NVRTC caps at 32 and spills; measured faster on every config);
+         * GX_JIT_PUNROLL=0: one inlined copy of the programs (records rotate through the load buffer) */
+        const int minb = getenv("GX_JIT_MINB") ? atoi(getenv("GX_JIT_MINB")) : 1;
+        const bool punroll = !getenv("GX_JIT_PUNROLL") || atoi(getenv("GX_JIT_PUNROLL")) != 0;
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
-        o << "extern \"C\" __global__ void __launch_bounds__(" << B << ") gx_jit_kernel(const uint4 *__restrict__ ev, "
+        o << "extern \"C\" __global__ void __launch_bounds__(" << B << (minb > 0 ? ", " + std::to_string(minb) : std::string()) << ") gx_jit_kernel(const uint4 *__restrict__ ev, "
              "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
@@ -532,13 +565,16 @@ struct Gen {
              "      const uint64_t i = (rb + u * nwarps) * 32 + lane;\n"
              "      if (i < n) { ea[u] = ldg_stream_ef(ev + 2 * i, pol); eb[u] = ldg_stream_ef(ev + 2 * i + 1, pol); }\n"
              "    }\n"
-             "    #pragma unroll\n"
+             "    #pragma unroll" << (punroll ? "" : " 1") << "\n"
              "    for (int u = 0; u < " << U << "; u++) {\n"
              "    const uint64_t rec = rb + u * nwarps;\n"
              "    if (rec >= nrec) break;\n"
              "    const uint64_t i = rec * 32 + lane;\n"
              "    const bool valid = i < n;\n"
-             "    const uint4 a = ea[u], b = eb[u];\n"
+             << (punroll ? "    const uint4 a = ea[u], b = eb[u];\n"
+                         : "    const uint4 a = ea[0], b = eb[0];\n"
+                           "    #pragma unroll\n    for (int k = 0; k + 1 < " + std::to_string(U) +
+                               "; k++) { ea[k] = ea[k + 1]; eb[k] = eb[k + 1]; }\n") <<
              "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
              "    int p = -1;\n";
         if (L.single >= 0) {

@@ -11,5 +11,5 @@ std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &
 /* NVRTC -> sm_100a cubin.  Returns 0, or -1 with the compiler log. */
 int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string &log);
 /* preferred threads per block of the generated kernel (1024; GX_JIT_BLOCK = 256 / 512 for experiments);
- * the runtime falls back to 256 when a program's register use would leave < 1536 threads per SM */
+ * the runtime falls back to 256 only when a 1024-thread block cannot be resident */
 int gx_jit_block();

@@ -6,11 +6,13 @@
  * (§5.3).  gx_jit.cpp translates the verifier's pre-decoded image into straight-line
  * CUDA C++ (eBPF registers become SSA values in GPU registers, the stack becomes constant-indexed
  * registers, branches become branches) and NVRTC compiles it for sm_100a together with this
- * header.  One thread runs one event; SIMT divergence is the hardware's (independent thread
- * scheduling reconverges at post-dominators), so the interpreter's uniform-PC / min-PC machinery
- * is not needed here.  Helpers keep the interpreter's semantics: warp-aggregated map atomics over
- * the lanes of a fully present warp (__match_any_sync + __reduce_*_sync; per-lane when diverged),
- * shared-memory privatised ADD accumulators, one ringbuf reservation per converged warp.
+ * header.  One lane runs one event.  Control flow is the interpreter's scheme compiled: a uniform-PC
+ * copy of every basic block (the group of lanes running the program branches together, one ballot
+ * per branch) and a min-PC copy entered when the group splits, which runs one basic block at a
+ * time for the lanes at the lowest block id until the group is whole again.  The group is
+ * therefore known at every helper call, and the helpers below use it as their collective mask:
+ * group-aggregated map atomics (__match_any_sync + __reduce_*_sync), shared-memory privatised ADD
+ * accumulators, one ringbuf reservation per group.
  * Included only by NVRTC-compiled sources.
  */
 #pragma once
@@ -18,6 +20,8 @@
 #include "gx_internal.h"
 
 namespace gxj {
+
+#define GX_ALL 0xFFFFFFFFu
 
 typedef unsigned long long u64;
 typedef unsigned int u32;
@@ -151,83 +155,94 @@ __device__ __forceinline__ uint64_t group_reduce(unsigned mask, uint32_t op, uin
     default: return __reduce_xor_sync(mask, lo) | ((uint64_t)__reduce_xor_sync(mask, hi) << 32);
     }
 }
+/* map values are device memory: .global atomics (a generic atom. would add a shared-window test) */
 __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, uint64_t v, bool w32, bool fetch) {
+    uint64_t r = 0;
     if (w32) {
-        unsigned *p = reinterpret_cast<unsigned *>(addr);
-        const uint32_t x = (uint32_t)v;
+        uint32_t x = (uint32_t)v, o = 0;
         switch (op & 0xF0) {
-        case 0x00: if (!fetch) { atomicAdd(p, x); return 0; } return atomicAdd(p, x);
-        case 0x40: return atomicOr(p, x);
-        case 0x50: return atomicAnd(p, x);
-        default: return atomicXor(p, x);
+        case 0x00:
+            if (!fetch) asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr), "r"(x) : "memory");
+            else asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(addr), "r"(x) : "memory");
+            break;
+        case 0x40: asm volatile("atom.global.or.b32 %0, [%1], %2;" : "=r"(o) : "l"(addr), "r"(x) : "memory"); break;
+        case 0x50: asm volatile("atom.global.and.b32 %0, [%1], %2;" : "=r"(o) : "l"(addr), "r"(x) : "memory"); break;
+        default: asm volatile("atom.global.xor.b32 %0, [%1], %2;" : "=r"(o) : "l"(addr), "r"(x) : "memory"); break;
         }
+        return o;
     }
-    unsigned long long *p = reinterpret_cast<unsigned long long *>(addr);
     switch (op & 0xF0) {
-    case 0x00: if (!fetch) { atomicAdd(p, v); return 0; } return atomicAdd(p, v);
-    case 0x40: return atomicOr(p, v);
-    case 0x50: return atomicAnd(p, v);
-    default: return atomicXor(p, v);
+    case 0x00:
+        if (!fetch) asm volatile("red.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+        else asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(addr), "l"(v) : "memory");
+        break;
+    case 0x40: asm volatile("atom.global.or.b64 %0, [%1], %2;" : "=l"(r) : "l"(addr), "l"(v) : "memory"); break;
+    case 0x50: asm volatile("atom.global.and.b64 %0, [%1], %2;" : "=l"(r) : "l"(addr), "l"(v) : "memory"); break;
+    default: asm volatile("atom.global.xor.b64 %0, [%1], %2;" : "=l"(r) : "l"(addr), "l"(v) : "memory"); break;
     }
+    return r;
 }
 
-/* Warp-aggregated atomic on a shared map value (ADD/OR/AND/XOR, +-FETCH) among the lanes that
- * execute it together.  All lanes on one address (record-uniform keys): one REDUX + one L2 atomic
- * for the warp.  Mixed addresses: plain per-lane atomics for non-FETCH ops (the L2 serialises
- * per address; a match_any/segmented-reduce costs more than it saves on random keys), and
- * __match_any_sync groups for FETCH ops, whose lanes get old + their exclusive group prefix in
- * lane order (a valid linearisation). */
-/* Warp collectives in JIT code are used only where the whole warp is present (__activemask() is
- * full): every lane then executes the same helper body and reaches the same *_sync operations.
- * A mask built from a partial __activemask() is not a convergence guarantee (lanes can be
- * re-split under independent thread scheduling) and deadlocked at scale, so diverged lanes use the
- * per-lane forms, which are equally valid linearisations. */
-__device__ __forceinline__ bool warp_converged() {
-#ifdef GX_NOWARPAGG
-    return false;
-#else
-    return __activemask() == 0xFFFFFFFFu;
-#endif
-}
-
+/* ---------------------------------------------------------------------------------------------
+ * Group helpers.  JIT code runs a program for a group of lanes that are at the same basic block
+ * together: `mask` is that group (the uniform-PC group, or the min-PC group of a diverged warp)
+ * and every lane of `mask` calls the helper -- the warp collectives below name exactly the lanes
+ * that reach them.  (A mask taken from __activemask() is not such a guarantee and deadlocked at
+ * scale; the group is known by construction here.)
+ *
+ * Map atomic (ADD/OR/AND/XOR, +-FETCH).  All lanes on one address (record-uniform keys): one
+ * REDUX + one L2 atomic for the group.  Mixed addresses: plain per-lane atomics for non-FETCH
+ * ops (the L2 serialises per address; a match_any costs more than it saves on random keys), and
+ * __match_any_sync groups for FETCH ops, whose lanes get old + their exclusive prefix in lane
+ * order (a valid linearisation of the group's sequential order). */
 template <uint32_t OP, bool W32, bool FETCH>
-__device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
-    if (!warp_converged()) {
-        const uint64_t old = global_atomic(OP, addr, v, W32, FETCH);
-        return W32 ? (uint32_t)old : old;
-    }
-    const unsigned act = 0xFFFFFFFFu;
+__device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, uint64_t v) {
     const unsigned lane = threadIdx.x & 31;
-    const unsigned leader = __ffs(act) - 1;
-    const uint64_t a0 = __shfl_sync(act, addr, leader);
-    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
-    if (__all_sync(act, addr == a0)) {
+    const unsigned leader = __ffs(mask) - 1;
+    const uint64_t a0 = __shfl_sync(mask, addr, leader);
+    constexpr uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    if (__all_sync(mask, addr == a0)) {
         if (!FETCH) {
-            const uint64_t agg = group_reduce(act, OP, v, W32);
-            if (lane == leader) global_atomic(OP, addr, agg, W32, false);
+            const uint64_t agg = group_reduce(mask, OP, v, W32);
+            if (lane == leader) global_atomic(OP, a0, agg, W32, false);
             return 0;
         }
-        if (act == 0xFFFFFFFFu) {
-            uint64_t inc = W32 ? (uint32_t)v : v;
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint64_t o = __shfl_up_sync(act, inc, d);
-                if ((int)lane >= d) inc = apply_op(OP, inc, o);
+        /* partial group: explicit walk over its lanes (shfl_up chains need all 32) */
+        if (mask != 0xFFFFFFFFu) {
+            uint64_t pre = ident, tot = ident;
+            for (unsigned m = mask; m; m &= m - 1) {
+                const int jl = __ffs(m) - 1;
+                const uint64_t vj = __shfl_sync(mask, v, jl);
+                if (jl < (int)lane) pre = apply_op(OP, pre, vj);
+                tot = apply_op(OP, tot, vj);
             }
-            if (W32) inc = (uint32_t)inc;
-            const uint64_t tot = __shfl_sync(act, inc, 31);
             uint64_t old = 0;
-            if (lane == leader) old = global_atomic(OP, addr, tot, W32, true);
-            old = __shfl_sync(act, old, leader);
-            uint64_t exc = __shfl_up_sync(act, inc, 1);
-            if (lane == 0) exc = ident;
-            const uint64_t r = apply_op(OP, old, exc);
+            if (lane == leader) old = global_atomic(OP, a0, tot, W32, true);
+            old = __shfl_sync(mask, old, leader);
+            const uint64_t r = apply_op(OP, old, pre);
             return W32 ? (uint32_t)r : r;
         }
-    } else if (!FETCH) {
+        /* full warp: inclusive scan in lane order */
+        uint64_t inc = W32 ? (uint32_t)v : v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(mask, inc, d);
+            if ((int)lane >= d) inc = apply_op(OP, inc, o);
+        }
+        if (W32) inc = (uint32_t)inc;
+        const uint64_t tot = __shfl_sync(mask, inc, 31);
+        uint64_t old = 0;
+        if (lane == leader) old = global_atomic(OP, a0, tot, W32, true);
+        old = __shfl_sync(mask, old, leader);
+        uint64_t exc = __shfl_up_sync(mask, inc, 1);
+        if (lane == 0) exc = ident;
+        const uint64_t r = apply_op(OP, old, exc);
+        return W32 ? (uint32_t)r : r;
+    }
+    if (!FETCH) {
         global_atomic(OP, addr, v, W32, false);
         return 0;
     }
-    const unsigned peers = __match_any_sync(act, addr);
+    const unsigned peers = __match_any_sync(mask, addr);
     const unsigned gl = __ffs(peers) - 1;
     uint64_t pre = ident, tot = ident;
     for (unsigned m = peers; m; m &= m - 1) {
@@ -243,48 +258,43 @@ __device__ __forceinline__ uint64_t warp_atomic(uint64_t addr, uint64_t v) {
     return W32 ? (uint32_t)r : r;
 }
 
-/* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory; one atomic per warp
- * when every converged lane adds to the same word, else one per lane */
+/* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory; one shared atomic
+ * per group when the group adds to one word, else one per lane */
 __device__ __forceinline__ void priv_one(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
     const uint32_t old = atomicAdd(&lo[w], (uint32_t)v);
     const uint32_t carry = ((uint32_t)(old + (uint32_t)v) < old) ? 1u : 0u;
     const uint32_t h = (uint32_t)(v >> 32) + carry;
     if (h) atomicAdd(&hi[w], h);
 }
-__device__ __forceinline__ void priv_add(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
-    if (!warp_converged()) {
-        priv_one(lo, hi, w, v);
-        return;
-    }
-    const unsigned act = 0xFFFFFFFFu;
-    const unsigned leader = __ffs(act) - 1;
-    const uint32_t w0 = __shfl_sync(act, w, leader);
-    if (__all_sync(act, w == w0)) {
-        const uint64_t agg = group_sum64(act, v);
+__device__ __forceinline__ void group_priv_add(unsigned mask, uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
+    const unsigned leader = __ffs(mask) - 1;
+    const uint32_t w0 = __shfl_sync(mask, w, leader);
+    if (__all_sync(mask, w == w0)) {
+        const uint64_t agg = group_sum64(mask, v);
         if ((threadIdx.x & 31) == leader) priv_one(lo, hi, w0, agg);
     } else {
         priv_one(lo, hi, w, v);
     }
 }
 
-/* one ringbuf reservation per converged group of lanes; returns 0 or -EAGAIN */
-__device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uint64_t *words, uint32_t size,
-                                                  unsigned long long &drops, unsigned long long &bytes) {
-    const unsigned act = warp_converged() ? 0xFFFFFFFFu : (1u << (threadIdx.x & 31)); /* else: per-lane reservation */
+/* one ringbuf reservation per group (records in lane order); returns 0 or -EAGAIN */
+__device__ __forceinline__ int64_t group_ringbuf(unsigned mask, const GxMapDesc &md, const uint64_t *words, uint32_t size,
+                                                 unsigned long long &drops, unsigned long long &bytes) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t recb = (8 + size + 7) & ~7u;
-    const uint32_t cnt = __popc(act), rank = __popc(act & ((1u << lane) - 1));
-    const uint32_t leader = __ffs(act) - 1;
+    const uint32_t cnt = __popc(mask), rank = __popc(mask & ((1u << lane) - 1));
+    const uint32_t leader = __ffs(mask) - 1;
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(md.aux);
     uint64_t base = 0;
     if (lane == leader) base = atomicAdd(&ctr[0], (unsigned long long)(cnt * recb));
-    base = __shfl_sync(act, base, leader);
+    base = __shfl_sync(mask, base, leader);
     const uint64_t o = base + rank * recb;
     const bool ok = o + recb <= (uint64_t)md.cap_mask + 1;
     if (ok) {
         uint64_t *dst = reinterpret_cast<uint64_t *>(md.data + o);
         dst[0] = (uint64_t)size | ((o >> 12) << 32);
         const uint32_t nw = (size + 7) / 8;
+#pragma unroll
         for (uint32_t w = 0; w < nw; w++) {
             uint64_t v = words[w];
             if (w == nw - 1 && (size & 7)) v &= (1ull << (8 * (size & 7))) - 1;
@@ -293,136 +303,7 @@ __device__ __forceinline__ int64_t ringbuf_output(const GxMapDesc &md, const uin
     } else {
         drops++;
     }
-    const uint32_t nok = __popc(__ballot_sync(act, ok));
-    if (nok && lane == leader) {
-        atomicAdd(&ctr[1], (unsigned long long)(nok * recb));
-        bytes += nok * recb;
-    }
-    return ok ? 0 : -(int64_t)gxd::E_AGAIN;
-}
-
-/* HASH helpers for JIT code: warp-cooperative (one probe / insert for a warp-uniform key) when the
- * whole warp is present, per lane otherwise */
-__device__ __forceinline__ uint64_t *jit_hash_find(const GxMapDesc &m, uint64_t key) {
-#ifndef GX_NOCOOP
-    if (warp_converged())
-#else
-    if (false)
-#endif return gxd::hash_lookup_coop(m, key, true, 0xFFFFFFFFu);
-    return gxd::hash_find(m, key);
-}
-__device__ __forceinline__ int64_t jit_hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
-                                                   bool &full) {
-#ifndef GX_NOCOOP
-    if (warp_converged())
-#else
-    if (false)
-#endif return gxd::hash_update_coop(m, key, val, flags, full, true, 0xFFFFFFFFu);
-    return gxd::hash_update(m, key, val, flags, full);
-}
-
-/* ---------------------------------------------------------------------------------------------
- * Convergent (v2) helpers.  JIT v2 code keeps all 32 lanes of a warp together: basic blocks run
- * under a per-lane `me` predicate (uniform-PC fast path with direct block-to-block jumps, min-PC
- * dispatch when lanes diverge -- the interpreter's scheme, compiled), so every helper below is
- * called by the whole warp and may use full-mask warp collectives; `me` marks the lanes whose
- * event executes the helper. */
-#define GX_ALL 0xFFFFFFFFu
-
-template <uint32_t OP, bool W32, bool FETCH>
-__device__ __forceinline__ uint64_t atomic2(bool me, uint64_t addr, uint64_t v) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned part = __ballot_sync(GX_ALL, me);
-    if (!part) return 0;
-    const unsigned leader = __ffs(part) - 1;
-    const uint64_t a0 = __shfl_sync(GX_ALL, addr, leader);
-    const uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
-    const uint64_t mine = me ? v : ident;
-    if (__all_sync(GX_ALL, !me || addr == a0)) {
-        if (!FETCH) {
-            const uint64_t agg = group_reduce(GX_ALL, OP, mine, W32);
-            if (lane == leader) global_atomic(OP, a0, agg, W32, false);
-            return 0;
-        }
-        uint64_t inc = W32 ? (uint32_t)mine : mine;
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint64_t o = __shfl_up_sync(GX_ALL, inc, d);
-            if ((int)lane >= d) inc = apply_op(OP, inc, o);
-        }
-        if (W32) inc = (uint32_t)inc;
-        const uint64_t tot = __shfl_sync(GX_ALL, inc, 31);
-        uint64_t old = 0;
-        if (lane == leader) old = global_atomic(OP, a0, tot, W32, true);
-        old = __shfl_sync(GX_ALL, old, leader);
-        uint64_t exc = __shfl_up_sync(GX_ALL, inc, 1);
-        if (lane == 0) exc = ident;
-        const uint64_t r = apply_op(OP, old, exc);
-        return W32 ? (uint32_t)r : r;
-    }
-    if (!FETCH) {
-        if (me) global_atomic(OP, addr, v, W32, false);
-        return 0;
-    }
-    const unsigned peers = __match_any_sync(GX_ALL, me ? addr : 0ull);
-    uint64_t res = 0;
-    if (me) {
-        const unsigned gl = __ffs(peers) - 1;
-        uint64_t pre = ident, tot = ident;
-        for (unsigned m = peers; m; m &= m - 1) {
-            const int jl = __ffs(m) - 1;
-            const uint64_t vj = __shfl_sync(peers, v, jl);
-            if (jl < (int)lane) pre = apply_op(OP, pre, vj);
-            tot = apply_op(OP, tot, vj);
-        }
-        uint64_t old = 0;
-        if (lane == gl) old = global_atomic(OP, addr, tot, W32, true);
-        old = __shfl_sync(peers, old, gl);
-        res = apply_op(OP, old, pre);
-        if (W32) res = (uint32_t)res;
-    }
-    return res;
-}
-
-__device__ __forceinline__ void priv_add2(bool me, uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {
-    const unsigned part = __ballot_sync(GX_ALL, me);
-    if (!part) return;
-    const unsigned leader = __ffs(part) - 1;
-    const uint32_t w0 = __shfl_sync(GX_ALL, w, leader);
-    if (__all_sync(GX_ALL, !me || w == w0)) {
-        const uint64_t agg = group_sum64(GX_ALL, me ? v : 0);
-        if ((threadIdx.x & 31) == leader) priv_one(lo, hi, w0, agg);
-    } else if (me) {
-        priv_one(lo, hi, w, v);
-    }
-}
-
-__device__ __forceinline__ int64_t ringbuf2(bool me, const GxMapDesc &md, const uint64_t *words, uint32_t size,
-                                            unsigned long long &drops, unsigned long long &bytes) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned act = __ballot_sync(GX_ALL, me);
-    if (!act) return 0;
-    const uint64_t recb = (8 + size + 7) & ~7u;
-    const uint32_t cnt = __popc(act), rank = __popc(act & ((1u << lane) - 1));
-    const uint32_t leader = __ffs(act) - 1;
-    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(md.aux);
-    uint64_t base = 0;
-    if (lane == leader) base = atomicAdd(&ctr[0], (unsigned long long)(cnt * recb));
-    base = __shfl_sync(GX_ALL, base, leader);
-    const uint64_t o = base + rank * recb;
-    const bool ok = me && (o + recb <= (uint64_t)md.cap_mask + 1);
-    if (ok) {
-        uint64_t *dst = reinterpret_cast<uint64_t *>(md.data + o);
-        dst[0] = (uint64_t)size | ((o >> 12) << 32);
-        const uint32_t nw = (size + 7) / 8;
-        for (uint32_t w = 0; w < nw; w++) {
-            uint64_t v = words[w];
-            if (w == nw - 1 && (size & 7)) v &= (1ull << (8 * (size & 7))) - 1;
-            dst[1 + w] = v;
-        }
-    } else if (me) {
-        drops++;
-    }
-    const uint32_t nok = __popc(__ballot_sync(GX_ALL, ok));
+    const uint32_t nok = __popc(__ballot_sync(mask, ok));
     if (nok && lane == leader) {
         atomicAdd(&ctr[1], (unsigned long long)(nok * recb));
         bytes += nok * recb;

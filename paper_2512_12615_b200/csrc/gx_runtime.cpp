@@ -309,8 +309,9 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         images.push_back(rt->progs[q].vr.image.data());
         sizes.push_back((uint32_t)rt->progs[q].vr.image.size());
     }
-    /* fewer, larger blocks keep the per-block privatised-shard flush small; fall back to 256-thread
-     * blocks when register pressure would cut residency below 1536 threads per SM */
+    /* fewer, larger blocks keep the per-block privatised-shard flush small; one 1024-thread block
+     * per SM measured fastest on every config (profiles/r1_jit_variants.md); 256-thread blocks only
+     * if the 1024-thread kernel cannot be resident at all */
     for (int B : {gx_jit_block(), 256}) {
         std::string src = gx_jit_source(cfg.h, images, sizes, B);
         if (const char *dump = getenv("GX_JIT_DUMP")) {
@@ -328,7 +329,7 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         int bps = 0;
         if (!d.occupancy || d.occupancy(&bps, fn, B, 0) != CUDA_SUCCESS || bps < 1) bps = 1;
         bps = std::min(bps, 2048 / B); /* per-thread shards: at most 2048 resident threads per SM */
-        if (bps * B < 1536 && B != 256) {
+        if (bps * B < 1024 && B != 256) {
             if (d.moduleUnload) d.moduleUnload(mod);
             continue;
         }
