@@ -170,6 +170,7 @@ struct Gen {
 
     std::ostringstream *out_ = nullptr;
     bool dmode_ = false; /* emitting the min-PC (diverged) copy of a block */
+    bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
     void me(const std::string &x) { (*out_) << "  { " << x << " }\n"; }
     std::string M() const { return dmode_ ? "exec" : "active"; }
@@ -182,7 +183,11 @@ struct Gen {
      * run that block's diverged copy, and once the live lanes all wait at one block again they
      * re-enter the uniform copy there.  This is the interpreter's a3 scheme at basic-block
      * granularity, and it makes the lane group known at every helper call: the helpers' warp
-     * collectives take `active` (uniform copy) or `exec` (diverged copy) as their mask. */
+     * collectives take `active` (uniform copy) or `exec` (diverged copy) as their mask.
+     * prog<q><FULL = true> is the instance for a whole-warp group (the common case): `active` is
+     * the constant full mask throughout its uniform copy -- it re-enters the uniform copy only when
+     * all 32 lanes are live again -- so every uniform-copy collective compiles without the
+     * runtime-mask convergence checks (REDUX.OR + BRA.DIV per collective, profiles/r1_ncu_c2_jit.md). */
     void program(int q, const GxInsn *im0, uint32_t n) {
         std::set<uint32_t> targets, leaders{0};
         for (uint32_t i = 0; i < n; i++) {
@@ -225,11 +230,12 @@ struct Gen {
             auto nx = std::next(it);
             blocks.push_back({*it, nx == leaders.end() ? n : *nx});
         }
-        o << "__device__ __forceinline__ void prog" << q
+        o << "template <bool FULL>\n__device__ __forceinline__ void prog" << q
           << "(const Ctx &c, unsigned active, uint64_t &retv, const uint32_t shard, uint32_t *spriv, "
              "unsigned long long &c_herr, unsigned long long &c_drop, unsigned long long &c_rbb, "
-             "unsigned long long &c_hfull) {\n"
+             "unsigned long long &c_hfull, PtCache &ptc) {\n"
              "  const unsigned lane = threadIdx.x & 31;\n"
+             "  if (FULL) active = GX_ALL;\n"
              "  if (!((active >> lane) & 1)) return;\n"
              "  uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0, r8 = 0, r9 = 0;\n"
              "  const uint64_t r10 = 512;\n  (void)r10; (void)spriv; (void)shard;\n";
@@ -250,7 +256,7 @@ struct Gen {
                 "  if (pc_ == 0xFFFFFFFFu) return;\n"
                 "  const unsigned exec = __ballot_sync(active, mypc == pc_);\n"
                 "  const unsigned live = __ballot_sync(active, mypc != 0xFFFFFFFFu);\n"
-                "  if (exec == live) {\n    if (mypc == 0xFFFFFFFFu) return;\n    active = live;\n    switch (pc_) {\n";
+                "  if (exec == live && (!FULL || live == GX_ALL)) {\n    if (mypc == 0xFFFFFFFFu) return;\n    active = FULL ? GX_ALL : live;\n    switch (pc_) {\n";
         for (auto [b, e] : blocks) body << "    case " << b << ": goto U" << b << ";\n";
         body << "    default: return;\n    }\n  }\n  if (mypc != pc_) continue;\n  switch (pc_) {\n";
         dmode_ = true;
@@ -369,8 +375,12 @@ struct Gen {
             break;
         }
         case GX_LDX_PT:
-            me(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
-                                  std::to_string(g.off) + ", shard), " + std::to_string(lg) + ")") + ";");
+            if (ptc_)
+                me("const uint64_t la_ = " + s + " + (int64_t)" + std::to_string(g.off) + "; " + d + " = " +
+                   ld_fix("ptc_ld(ptc, la_, gxd::pt_phys(" + md((int)g.imm) + ", la_, shard), " + std::to_string(lg) + ")") + ";");
+            else
+                me(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
+                                      std::to_string(g.off) + ", shard), " + std::to_string(lg) + ")") + ";");
             break;
         case GX_ST_STACK: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
@@ -384,8 +394,12 @@ struct Gen {
         }
         case GX_ST_PT: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            me("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
-               ", shard), " + std::to_string(lg) + ", " + v + ");");
+            if (ptc_)
+                me("const uint64_t la_ = " + d + " + (int64_t)" + std::to_string(g.off) + "; ptc_st(ptc, la_, gxd::pt_phys(" +
+                   md(g.aux >> 4) + ", la_, shard), " + std::to_string(lg) + ", " + v + ");");
+            else
+                me("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
+                   ", shard), " + std::to_string(lg) + ", " + v + ");");
             break;
         }
         case GX_ATOM_STACK: case GX_ATOM_PT: case GX_ATOM_MAP: atomic(g); break;
@@ -423,6 +437,9 @@ struct Gen {
                 const std::string logical = hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u + " +
                                             std::to_string(8 * w);
                 if (g.op == GX_CALL_UPDATE_ARRAY) b << " *(uint64_t *)(" << logical << ") = " << v << ";";
+                else if (ptc_)
+                    b << " { const uint64_t la_ = " << logical << "; ptc_st(ptc, la_, gxd::pt_phys(" << md(g.aux)
+                      << ", la_, shard), 3, " << v << "); }";
                 else b << " *(uint64_t *)gxd::pt_phys(" << md(g.aux) << ", " << logical << ", shard) = " << v << ";";
             }
             b << " } if (rc) c_herr++; r0 = (uint64_t)rc;";
@@ -504,8 +521,10 @@ struct Gen {
         const int fd = g.aux >> 4;
         const std::string addr = R(g.dst) + " + (int64_t)" + std::to_string(g.off);
         if (g.op == GX_ATOM_PT) {
-            std::string e = "rmw_global_private((uint64_t)gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
-                            (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
+            std::string e = ptc_ ? "ptc_rmw(ptc, " + addr + ", gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
+                                       (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)"
+                                 : "rmw_global_private((uint64_t)gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
+                                       (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
             me(fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";");
             return;
         }
@@ -540,9 +559,11 @@ struct Gen {
          * GX_JIT_PUNROLL=0: one inlined copy of the programs (records rotate through the load buffer) */
         const int minb = getenv("GX_JIT_MINB") ? atoi(getenv("GX_JIT_MINB")) : 1;
         const bool punroll = !getenv("GX_JIT_PUNROLL") || atoi(getenv("GX_JIT_PUNROLL")) != 0;
+        ptc_ = getenv("GX_JIT_PTCACHE") && atoi(getenv("GX_JIT_PTCACHE")) != 0;
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
+        const int S = gx_jit_stages();
         o << "extern \"C\" __global__ void __launch_bounds__(" << B << (minb > 0 ? ", " + std::to_string(minb) : std::string()) << ") gx_jit_kernel(const uint4 *__restrict__ ev, "
              "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
@@ -553,29 +574,96 @@ struct Gen {
              "  const uint32_t lane = threadIdx.x & 31;\n"
              "  const uint32_t shard = blockIdx.x * " << B << " + threadIdx.x;\n"
              "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
+             "  PtCache ptc;\n"
              "  const uint64_t nrec = (n + 31) >> 5;\n"
              "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
-             "  const uint64_t pol = evict_first_policy();\n"
-             "  /* one warp = one 32-event record at a time (event lane == executor lane); U records per\n"
-             "   * iteration, their loads issued back to back */\n"
-             "  for (uint64_t rb = (uint64_t)blockIdx.x * " << B / 32 << " + (threadIdx.x >> 5); rb < nrec; rb += nwarps * " << U << ") {\n"
-             "    uint4 ea[" << U << "], eb[" << U << "];\n"
-             "    #pragma unroll\n"
-             "    for (int u = 0; u < " << U << "; u++) {\n"
-             "      const uint64_t i = (rb + u * nwarps) * 32 + lane;\n"
-             "      if (i < n) { ea[u] = ldg_stream_ef(ev + 2 * i, pol); eb[u] = ldg_stream_ef(ev + 2 * i + 1, pol); }\n"
-             "    }\n"
-             "    #pragma unroll" << (punroll ? "" : " 1") << "\n"
-             "    for (int u = 0; u < " << U << "; u++) {\n"
-             "    const uint64_t rec = rb + u * nwarps;\n"
-             "    if (rec >= nrec) break;\n"
-             "    const uint64_t i = rec * 32 + lane;\n"
-             "    const bool valid = i < n;\n"
-             << (punroll ? "    const uint4 a = ea[u], b = eb[u];\n"
-                         : "    const uint4 a = ea[0], b = eb[0];\n"
-                           "    #pragma unroll\n    for (int k = 0; k + 1 < " + std::to_string(U) +
-                               "; k++) { ea[k] = ea[k + 1]; eb[k] = eb[k + 1]; }\n") <<
-             "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
+             "  const uint64_t pol = evict_first_policy();\n";
+        if (S >= 2) {
+            /* a1 through a per-warp ring of S one-record (1 KiB) slots in dynamic shared memory:
+             * record k+S-1 is in flight while record k runs.  Modes (GX_JIT_STAGE_MODE):
+             *   0 lane: lane l cp.asyncs its own event's two 16-B halves to slot words l, 32+l
+             *           (no cross-lane hazard; stride-32 B global reads),
+             *   1 coal: lane l cp.asyncs record bytes 16l and 512+16l (coalesced), the record keeps
+             *           its AoS layout and a __syncwarp orders the lanes,
+             *   2 bulk: one 1-D TMA bulk copy per record (cp.async.bulk + per-slot mbarrier). */
+            const int mode = gx_jit_stage_mode();
+            auto issue = [&](const std::string &ls, const std::string &rec) {
+                std::ostringstream t;
+                if (mode == 0) {
+                    t << "{ const uint64_t i_ = (" << rec << ") * 32 + lane; if (i_ < n) { cp_async16(ring_s + (" << ls
+                      << ") * 1024u + lane * 16u, ev + 2 * i_, pol); cp_async16(ring_s + (" << ls
+                      << ") * 1024u + 512u + lane * 16u, ev + 2 * i_ + 1, pol); } cp_async_commit(); }";
+                } else if (mode == 1) {
+                    t << "{ const uint64_t r_ = " << rec << "; const uint64_t i_ = r_ * 32 + (lane >> 1);"
+                      << " if (i_ < n) cp_async16(ring_s + (" << ls << ") * 1024u + lane * 16u, ev + r_ * 64 + lane, pol);"
+                      << " if (i_ + 16 < n) cp_async16(ring_s + (" << ls << ") * 1024u + 512u + lane * 16u, ev + r_ * 64 + 32 + lane, pol);"
+                      << " cp_async_commit(); }";
+                } else {
+                    t << "{ const uint64_t r_ = " << rec << "; if (lane == 0 && r_ < nrec) { const uint64_t left_ = n - r_ * 32;"
+                      << " bulk_load(ring_s + (" << ls << ") * 1024u, ev + r_ * 64, left_ >= 32 ? 1024u : (uint32_t)left_ * 32u, bar_s + ("
+                      << ls << ") * 8u, pol); } }";
+                }
+                return t.str();
+            };
+            o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
+                 "  const uint4 *ring = gx_ring + (threadIdx.x >> 5) * " << 64 * S << ";\n"
+                 "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);\n"
+                 "  const uint64_t rec0 = (uint64_t)blockIdx.x * " << B / 32 << " + (threadIdx.x >> 5);\n";
+            if (mode == 2) {
+                o << "  __shared__ __align__(8) uint64_t gx_bar[" << (B / 32) * S << "];\n"
+                     "  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(gx_bar + (threadIdx.x >> 5) * " << S << ");\n"
+                     "  if (lane == 0) {\n"
+                     "    for (int k = 0; k < " << S << "; k++) mbar_init(bar_s + k * 8u, 1);\n"
+                     "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+                     "  }\n"
+                     "  __syncwarp();\n"
+                     "  uint32_t phases = 0;\n";
+            }
+            o << "  #pragma unroll\n"
+                 "  for (int k = 0; k < " << S - 1 << "; k++) " << issue("k", "rec0 + k * nwarps") << "\n"
+                 "  uint32_t slot = 0;\n"
+                 "  #pragma unroll 1\n"
+                 "  for (uint64_t rec = rec0; rec < nrec; rec += nwarps) {\n"
+                 "    {\n"
+                 "      const uint32_t ls = slot == 0 ? " << S - 1 << "u : slot - 1;\n"
+              << (mode == 0 ? "" : "      __syncwarp();\n")
+              << "      " << issue("ls", "rec + " + std::to_string(S - 1) + " * nwarps") << "\n"
+                 "    }\n";
+            if (mode == 2)
+                o << "    mbar_wait(bar_s + slot * 8u, (phases >> slot) & 1u);\n"
+                     "    phases ^= 1u << slot;\n";
+            else
+                o << "    cp_async_wait<" << S - 1 << ">();\n";
+            if (mode == 1) o << "    __syncwarp();\n";
+            if (mode == 0)
+                o << "    const uint4 a = ring[slot * 64 + lane], b = ring[slot * 64 + 32 + lane];\n";
+            else
+                o << "    const uint4 a = ring[slot * 64 + 2 * lane], b = ring[slot * 64 + 2 * lane + 1];\n";
+            o << "    slot = slot == " << S - 1 << "u ? 0u : slot + 1;\n"
+                 "    const uint64_t i = rec * 32 + lane;\n"
+                 "    const bool valid = i < n;\n";
+        } else {
+            o << "  /* one warp = one 32-event record at a time (event lane == executor lane); U records per\n"
+                 "   * iteration, their loads issued back to back */\n"
+                 "  for (uint64_t rb = (uint64_t)blockIdx.x * " << B / 32 << " + (threadIdx.x >> 5); rb < nrec; rb += nwarps * " << U << ") {\n"
+                 "    uint4 ea[" << U << "], eb[" << U << "];\n"
+                 "    #pragma unroll\n"
+                 "    for (int u = 0; u < " << U << "; u++) {\n"
+                 "      const uint64_t i = (rb + u * nwarps) * 32 + lane;\n"
+                 "      if (i < n) { ea[u] = ldg_stream_ef(ev + 2 * i, pol); eb[u] = ldg_stream_ef(ev + 2 * i + 1, pol); }\n"
+                 "    }\n"
+                 "    #pragma unroll" << (punroll ? "" : " 1") << "\n"
+                 "    for (int u = 0; u < " << U << "; u++) {\n"
+                 "    const uint64_t rec = rb + u * nwarps;\n"
+                 "    if (rec >= nrec) break;\n"
+                 "    const uint64_t i = rec * 32 + lane;\n"
+                 "    const bool valid = i < n;\n"
+              << (punroll ? "    const uint4 a = ea[u], b = eb[u];\n"
+                          : "    const uint4 a = ea[0], b = eb[0];\n"
+                            "    #pragma unroll\n    for (int k = 0; k + 1 < " + std::to_string(U) +
+                                "; k++) { ea[k] = ea[k + 1]; eb[k] = eb[k + 1]; }\n");
+        }
+        o << "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
              "    int p = -1;\n";
         if (L.single >= 0) {
             o << "    if (valid) p = 0;\n";
@@ -595,10 +683,12 @@ struct Gen {
              "      todo &= ~m;\n"
              "      switch (pq) {\n";
         for (size_t q = 0; q < images.size(); q++)
-            o << "      case " << q << ": prog" << q << "(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull); break;\n";
+            o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+              << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n        break;\n";
         o << "      default: break;\n      }\n    }\n"
-             "    if (ret && valid) ret[i] = retv;\n    }\n  }\n";
-        o << "  for (int s = 16; s; s >>= 1) {\n"
+             "    if (ret && valid) ret[i] = retv;\n" << (S >= 2 ? "  }\n" : "    }\n  }\n");
+        o << "  ptc_flush(ptc);\n"
+             "  for (int s = 16; s; s >>= 1) {\n"
              "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
              "    c_herr += __shfl_xor_sync(GX_ALL, c_herr, s); c_drop += __shfl_xor_sync(GX_ALL, c_drop, s);\n"
              "    c_rbb += __shfl_xor_sync(GX_ALL, c_rbb, s); c_hfull += __shfl_xor_sync(GX_ALL, c_hfull, s);\n"
@@ -625,6 +715,24 @@ struct Gen {
 };
 
 }  // namespace
+
+int gx_jit_stages() {
+    static int s = [] {
+        int v = 0;
+        if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
+        return std::max(0, std::min(8, v));
+    }();
+    return s;
+}
+
+int gx_jit_stage_mode() {
+    static int m = [] {
+        int v = 2;
+        if (const char *e = getenv("GX_JIT_STAGE_MODE")) v = atoi(e);
+        return (v >= 0 && v <= 2) ? v : 2;
+    }();
+    return m;
+}
 
 int gx_jit_block() {
     static int b = [] {

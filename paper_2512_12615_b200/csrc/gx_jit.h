@@ -13,3 +13,13 @@ int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string
 /* preferred threads per block of the generated kernel (1024; GX_JIT_BLOCK = 256 / 512 for experiments);
  * the runtime falls back to 256 only when a 1024-thread block cannot be resident */
 int gx_jit_block();
+/* depth of the per-warp shared-memory event ring (cp.async / TMA staging, a1): 0 by default
+ * (GX_JIT_STAGES; < 2 = register double-load path).  Dynamic shared memory per block =
+ * gx_jit_smem(block) bytes. */
+int gx_jit_stages();
+/* staging mode: 0 per-lane cp.async, 1 coalesced cp.async, 2 TMA bulk (default) */
+int gx_jit_stage_mode();
+inline unsigned gx_jit_smem(int block) {
+    const int s = gx_jit_stages();
+    return s >= 2 ? (unsigned)(block / 32) * (unsigned)s * 1024u : 0u;
+}

@@ -48,6 +48,33 @@ __device__ __forceinline__ uint4 ldg_stream_ef(const uint4 *p, uint64_t pol) {
     return r;
 }
 
+/* asynchronous staging of the event stream into a per-warp shared-memory ring (16 B per lane per
+ * copy, L2 evict-first): each lane copies and later reads back only its own event's bytes, so the
+ * per-thread cp.async groups are the only synchronisation needed and the stream's memory-level
+ * parallelism no longer depends on the program's own latency chain */
+__device__ __forceinline__ void cp_async16(uint32_t dst, const uint4 *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+/* 1-D TMA bulk copy of a whole warp record (<= 1 KiB) into the warp's ring slot, completion
+ * signalled on the slot's mbarrier (one elected lane issues; every lane waits on the phase) */
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ uint64_t sx(uint64_t v, unsigned bits) {
     if (bits >= 64) return v;
     const uint64_t m = 1ull << (bits - 1);
@@ -119,6 +146,71 @@ __device__ __forceinline__ uint64_t rmw_global_private(uint64_t a, bool w32, uin
     const uint64_t old = rmw_word(v, (unsigned)(a & 7), w32, op, s, r0);
     *w = v;
     return old;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * Per-thread ARRAY write-back cache in registers (a5).  A per-thread shard is owned by exactly one
+ * executor thread for the whole launch (shard = global thread index; helpers cannot take pointers
+ * into per-thread maps -- the verifier rejects them), and the host and the fold / merge kernels
+ * read it only after the launch.  So the JIT keeps the thread's most recent per-thread words in
+ * registers: two direct-mapped 8-B entries selected by bit 3 of the logical address, tagged with
+ * the physical word address (bit 0 = dirty), written back on eviction and at the end of the
+ * launch.  Every per-thread load, store, atomic and update_elem goes through it, so it is
+ * unobservable (I-18) -- and C2's per-event read-modify-write of {cnt, bytes} never leaves the SM. */
+struct PtCache {
+    uint64_t t0 = 0, v0 = 0, t1 = 0, v1 = 0;
+};
+/* one direct-mapped entry (tag t, value v): make it hold the word at wphys (write back a dirty
+ * victim; fill from memory unless the caller overwrites the whole word) */
+__device__ __forceinline__ void ptc_fill(uint64_t &t, uint64_t &v, uint64_t wphys, bool fill) {
+    if ((t & ~1ull) != wphys) {
+        if (t & 1) *reinterpret_cast<uint64_t *>(t & ~1ull) = v;
+        if (fill) v = *reinterpret_cast<const uint64_t *>(wphys);
+        t = wphys;
+    }
+}
+__device__ __forceinline__ uint64_t ptc_ld(PtCache &c, uint64_t logical, const uint8_t *phys, unsigned lg) {
+    const uint64_t p = reinterpret_cast<uint64_t>(phys);
+    uint64_t w;
+    if ((logical >> 3) & 1) {
+        ptc_fill(c.t1, c.v1, p & ~7ull, true);
+        w = c.v1;
+    } else {
+        ptc_fill(c.t0, c.v0, p & ~7ull, true);
+        w = c.v0;
+    }
+    return zx(w >> (8 * (p & 7)), lg);
+}
+__device__ __forceinline__ void ptc_st(PtCache &c, uint64_t logical, const uint8_t *phys, unsigned lg, uint64_t val) {
+    const uint64_t p = reinterpret_cast<uint64_t>(phys);
+    if ((logical >> 3) & 1) {
+        ptc_fill(c.t1, c.v1, p & ~7ull, lg < 3);
+        c.v1 = word_set(c.v1, (unsigned)(p & 7), lg, val);
+        c.t1 |= 1;
+    } else {
+        ptc_fill(c.t0, c.v0, p & ~7ull, lg < 3);
+        c.v0 = word_set(c.v0, (unsigned)(p & 7), lg, val);
+        c.t0 |= 1;
+    }
+}
+__device__ __forceinline__ uint64_t ptc_rmw(PtCache &c, uint64_t logical, const uint8_t *phys, bool w32, uint32_t op, uint64_t s,
+                                            uint64_t r0) {
+    const uint64_t p = reinterpret_cast<uint64_t>(phys);
+    uint64_t old;
+    if ((logical >> 3) & 1) {
+        ptc_fill(c.t1, c.v1, p & ~7ull, true);
+        old = rmw_word(c.v1, (unsigned)(p & 7), w32, op, s, r0);
+        c.t1 |= 1;
+    } else {
+        ptc_fill(c.t0, c.v0, p & ~7ull, true);
+        old = rmw_word(c.v0, (unsigned)(p & 7), w32, op, s, r0);
+        c.t0 |= 1;
+    }
+    return old;
+}
+__device__ __forceinline__ void ptc_flush(PtCache &c) {
+    if (c.t0 & 1) *reinterpret_cast<uint64_t *>(c.t0 & ~1ull) = c.v0;
+    if (c.t1 & 1) *reinterpret_cast<uint64_t *>(c.t1 & ~1ull) = c.v1;
 }
 
 __device__ __forceinline__ uint64_t apply_op(uint32_t op, uint64_t a, uint64_t b) {

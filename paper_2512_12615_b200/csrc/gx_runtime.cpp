@@ -110,6 +110,7 @@ struct Drv {
                              CUstream, void **, void **) = nullptr;
     CUresult (*occupancy)(int *, CUfunction, int, size_t) = nullptr;
     CUresult (*moduleUnload)(CUmodule) = nullptr;
+    CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
 };
 Drv &drv() {
     static Drv d;
@@ -124,6 +125,7 @@ Drv &drv() {
         ok &= cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void **)&d.occupancy,
                                       cudaEnableDefault, &q) == cudaSuccess;
         ok &= cudaGetDriverEntryPoint("cuModuleUnload", (void **)&d.moduleUnload, cudaEnableDefault, &q) == cudaSuccess;
+        ok &= cudaGetDriverEntryPoint("cuFuncSetAttribute", (void **)&d.funcSetAttribute, cudaEnableDefault, &q) == cudaSuccess;
         d.ok = ok && d.moduleLoadData && d.moduleGetFunction && d.launchKernel;
     }
     return d;
@@ -326,8 +328,11 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         CUfunction fn = nullptr;
         if (d.moduleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
         if (d.moduleGetFunction(&fn, mod, "gx_jit_kernel") != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
+        const unsigned smem = gx_jit_smem(B);
+        if (smem && d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+            return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
         int bps = 0;
-        if (!d.occupancy || d.occupancy(&bps, fn, B, 0) != CUDA_SUCCESS || bps < 1) bps = 1;
+        if (!d.occupancy || d.occupancy(&bps, fn, B, smem) != CUDA_SUCCESS || bps < 1) bps = 1;
         bps = std::min(bps, 2048 / B); /* per-thread shards: at most 2048 resident threads per SM */
         if (bps * B < 1024 && B != 256) {
             if (d.moduleUnload) d.moduleUnload(mod);
@@ -357,13 +362,16 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         static const uint64_t per_thread = getenv("GX_JIT_EPT") ? strtoull(getenv("GX_JIT_EPT"), nullptr, 10) : 8;
         static const uint64_t cap = getenv("GX_JIT_GRID") ? strtoull(getenv("GX_JIT_GRID"), nullptr, 10) : ~0ull;
         const uint64_t B = cfg.jblock;
-        uint64_t want = std::min<uint64_t>(cap, (n + B * per_thread - 1) / (B * per_thread));
+        uint64_t want = (n + B * per_thread - 1) / (B * per_thread);
+        if (want * 2 >= cfg.jgrid) want = cfg.jgrid; /* past half the resident grid: every SM streams */
+        want = std::min<uint64_t>(cap, want);
         uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
-        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, 0, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
+        const unsigned smem = gx_jit_smem((int)B);
+        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
         rt->last_grid = grid;
         rt->last_block = (uint32_t)B;
-        rt->last_smem = 0;
+        rt->last_smem = smem;
     } else {
         int e = gx_launch_exec(cfg.d, d_events, n, d_ret, cfg.grid, cfg.smem, stream);
         if (e) return cuda_err(rt, (cudaError_t)e, "executor launch");

@@ -163,3 +163,102 @@ def test_run_batch_host_parity(gpu, engine):
     gx.gx_run_batch_host(rt.rt, ev, prog_fd=s.prog_arg, ret=r0)
     assert outputs(rt, s) == outputs(env, so)
     assert (r0 == r0o).all()
+
+
+# Per-thread ARRAY stress (a5): many lane-varying keys per thread (register write-back cache
+# evictions in the JIT), three maps with value sizes 8 / 16 / 32, sub-word loads and stores,
+# 32- and 64-bit atomics and update_elem -- all ADD-type, so the SUM fold over shards is
+# shard-invariant and must equal the oracle's sequential result exactly.
+PT_STRESS = """
+    mov64 r6, r1
+    ldxdw r7, [r6+0]          ; addr (lane-varying)
+    mov64 r2, r7
+    rsh64 r2, 3
+    and64 r2, 7
+    stxw [r10-4], r2          ; key A = (addr >> 3) & 7
+    lddw r1, map:pa
+    mov64 r2, r10
+    add64 r2, -4
+    call 1
+    jeq r0, 0, b
+    ldxdw r1, [r0+0]
+    add64 r1, 1
+    stxdw [r0+0], r1
+    ldxw r1, [r6+28]
+    atomic_add64 [r0+8], r1
+    ldxb r1, [r0+8]            ; sub-word read of the word just updated (not stored back)
+b:
+    mov64 r2, r7
+    rsh64 r2, 7
+    and64 r2, 3
+    stxw [r10-8], r2          ; key B = (addr >> 7) & 3
+    lddw r1, map:pb
+    mov64 r2, r10
+    add64 r2, -8
+    call 1
+    jeq r0, 0, c
+    mov64 r8, r0
+    mov64 r1, 2
+    atomic_fetch_add32 [r8+4], r1
+    mov64 r3, r7
+    and64 r3, 1016
+    jne r3, 0, c              ; sub-word counters on 1/128 of the events (no byte wrap on one shard)
+    ldxb r3, [r8+0]
+    add64 r3, 1
+    stxb [r8+0], r3           ; byte counter (small counts: no carry)
+    ldxh r3, [r8+2]
+    add64 r3, 3
+    stxh [r8+2], r3
+c:
+    mov64 r2, r7
+    rsh64 r2, 5
+    and64 r2, 15
+    stxw [r10-12], r2         ; key C = (addr >> 5) & 15
+    lddw r1, map:pc
+    mov64 r2, r10
+    add64 r2, -12
+    call 1
+    jeq r0, 0, out
+    ldxdw r3, [r0+24]
+    add64 r3, r7
+    stxdw [r10-24], r3        ; value for update_elem: old + addr in word 3
+    ldxdw r3, [r0+0]
+    add64 r3, 1
+    stxdw [r10-48], r3
+    ldxdw r3, [r0+8]
+    stxdw [r10-40], r3
+    ldxdw r3, [r0+16]
+    add64 r3, 5
+    stxdw [r10-32], r3
+    lddw r1, map:pc
+    mov64 r2, r10
+    add64 r2, -12
+    mov64 r3, r10
+    add64 r3, -48
+    mov64 r4, 0
+    call 2
+out:
+    mov64 r0, 0
+    exit
+"""
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("n", [1000, (1 << 16) + 7])
+def test_perthread_stress_parity(gpu, engine, n):
+    import torch
+    from oracle.oracle import Oracle
+    rng = np.random.default_rng(11 + n)
+    ev = gen.records(n, addr=rng.integers(0, 1 << 20, n, dtype=np.uint64) * 8,
+                     ts=np.zeros(n, dtype=np.uint64))
+    ev["size"] = rng.integers(1, 17, n).astype(np.uint32)
+    specs = {"pa": (6, 4, 16, 8), "pb": (6, 4, 8, 4), "pc": (6, 4, 32, 16)}
+    env, rt = Oracle(), make_runtime(engine)
+    fo = {k: env.create_map(*v) for k, v in specs.items()}
+    fg = {k: rt.create_map(*v) for k, v in specs.items()}
+    want = env.run(ev, env.load_prog(asm.assemble(PT_STRESS, fo)))
+    ret = torch.zeros(n, dtype=torch.int64, device="cuda")
+    rt.run(torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda(), rt.load_prog(asm.assemble(PT_STRESS, fg)), ret=ret)
+    assert (ret.cpu().numpy().view(np.uint64) == want).all()
+    for k in specs:
+        assert rt.dump(fg[k]) == env.dump(fo[k]), k
