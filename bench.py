@@ -324,7 +324,9 @@ def c1_measure(device):
     """BASELINE.json configs[0] / the north-star target: the counter policy over 2^20-event batches.
     8 distinct batches (256 MiB > L2) are rotated so every launch streams from HBM.  Reported both
     per single launch (CUDA events around each launch) and steady state (100 back-to-back launches
-    captured in one CUDA graph, SURVEY.md §8d C1 timing protocol)."""
+    captured in one CUDA graph, SURVEY.md §8d C1 timing protocol), the latter also with the
+    launches chained by programmatic dependent launch (gx_run_batch_ex GX_RUN_OVERLAP: the batches
+    are resident before the graph runs, which is that flag's contract)."""
     import torch
     import paper_2512_12615_b200 as gx
     from gxin import configs, gen_gpu
@@ -350,27 +352,32 @@ def c1_measure(device):
                 times.append((a, b2))
             stream.synchronize()
             single = float(np.median([a.elapsed_time(b2) for a, b2 in times]))
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for k in range(100):
-                    rt.run(bufs[k % nb], s.prog_arg, stream=stream)
-            g.replay()
-            stream.synchronize()
-            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(5):
+            steady = {}
+            for overlap in (False, True):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for k in range(100):
+                        rt.run(bufs[k % nb], s.prog_arg, stream=stream, overlap=overlap)
                 g.replay()
-            b2.record(stream)
-            stream.synchronize()
-            steady = a.elapsed_time(b2) / 500
+                stream.synchronize()
+                a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(5):
+                    g.replay()
+                b2.record(stream)
+                stream.synchronize()
+                steady[overlap] = a.elapsed_time(b2) / 500
+                del g
         counts = rt.array_u64(s.fds[(0, "counts")])
-        runs = 3 * nb + 5 * nb + 100 + 500
+        runs = 3 * nb + 5 * nb + 2 * (100 + 500)
         assert int(counts.sum()) == runs * n, "counter total != events (north star invariant)"
         bw = lambda ms: EVENT_BYTES * n / (ms / 1e3) / 1e9
         out[config] = {"events": n, "single_launch_us": single * 1e3, "single_events_per_s": n / (single / 1e3),
                        "single_hbm_frac": bw(single) / peaks["hbm_gbs"],
-                       "steady_us": steady * 1e3, "steady_events_per_s": n / (steady / 1e3),
-                       "steady_hbm_frac": bw(steady) / peaks["hbm_gbs"], "counter_total_ok": True,
+                       "steady_us": steady[False] * 1e3, "steady_events_per_s": n / (steady[False] / 1e3),
+                       "steady_hbm_frac": bw(steady[False]) / peaks["hbm_gbs"],
+                       "steady_pdl_us": steady[True] * 1e3, "steady_pdl_events_per_s": n / (steady[True] / 1e3),
+                       "steady_pdl_hbm_frac": bw(steady[True]) / peaks["hbm_gbs"], "counter_total_ok": True,
                        "flush": "8 rotating 32-MiB batches (256 MiB > L2)"}
         rt.close()
         del bufs

@@ -160,6 +160,19 @@ int  gx_attach(gx_rt *rt, int prog_fd, uint32_t hook_kind, uint32_t tenant);
  * legacy default stream).  Asynchronous (stream-ordered).  -EPERM if the program is unverified. */
 int  gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n_events, int prog_fd, uint64_t *d_ret,
                   void *cuda_stream);
+/* gx_run_batch with launch flags (0 = gx_run_batch):
+ *   GX_RUN_OVERLAP  programmatic dependent launch (JIT engine; ignored by the interpreter): the
+ *                   batch's grid may be scheduled while the preceding kernel on the stream is still
+ *                   draining and may start READING d_events before that kernel completes; every
+ *                   map access, stat update and d_ret write still waits for its completion and
+ *                   memory flush (griddepcontrol.wait), so back-to-back batches keep the sequential
+ *                   semantics (S1).  The caller promises that d_events is not written by the work
+ *                   immediately preceding on the stream (e.g. events generated or copied earlier
+ *                   and already complete, as in a steady-state stream of resident batches).
+ * Errors as gx_run_batch; -EINVAL for unknown flags. */
+enum { GX_RUN_OVERLAP = 1 };
+int  gx_run_batch_ex(gx_rt *rt, const void *d_events, uint64_t n_events, int prog_fd, uint64_t *d_ret,
+                     void *cuda_stream, uint32_t flags);
 /* Same, from HOST memory (pinned or pageable): the events are copied to the device in chunks
  * on the runtime's own streams, overlapping copies with execution; h_ret (nullable) receives R0.
  * Synchronous.  This is the end-to-end path bench.py times as "e2e". */

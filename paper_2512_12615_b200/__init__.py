@@ -27,7 +27,7 @@ RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", 
          "COMPLEXITY", "BUDGET", "UNIFORM_BRANCH", "UNIFORM_LOOP_BOUND", "UNIFORM_MAP_KEY", "NON_UNIFORM_ATOMIC",
          "MIXED_PTR")
 EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_map", "gx_read_map",
-           "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_jit_offline", "gx_attach", "gx_run_batch", "gx_run_batch_host",
+           "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_jit_offline", "gx_attach", "gx_run_batch", "gx_run_batch_ex", "gx_run_batch_host",
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply")
 
@@ -93,6 +93,7 @@ def lib():
         "gx_get_engine": (i32, [vp]),
         "gx_attach": (i32, [vp, i32, u32, u32]),
         "gx_run_batch": (i32, [vp, vp, u64, i32, vp, vp]),
+        "gx_run_batch_ex": (i32, [vp, vp, u64, i32, vp, vp, u32]),
         "gx_run_batch_host": (i32, [vp, vp, u64, i32, vp]),
         "gx_get_stats": (i32, [vp, C.POINTER(gx_batch_stats)]),
         "gx_exec_info": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), p64]),
@@ -210,15 +211,27 @@ def _stream_handle(stream):
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
-def gx_run_batch(rt, events, n=None, prog_fd=-1, ret=None, stream=None):
-    """events: torch.uint8 CUDA tensor (N, 32) (or a raw device pointer with n); ret: u64 tensor or None."""
+GX_RUN_OVERLAP = 1
+
+
+def gx_run_batch(rt, events, n=None, prog_fd=-1, ret=None, stream=None, flags=0):
+    """events: torch.uint8 CUDA tensor (N, 32) (or a raw device pointer with n); ret: u64 tensor or None.
+    flags: 0, or GX_RUN_OVERLAP (gx_run_batch_ex: programmatic dependent launch; include/gx.h)."""
     if hasattr(events, "data_ptr"):
         n = events.shape[0] if n is None else n
         ptr = events.data_ptr()
     else:
         ptr = events
     rptr = ret.data_ptr() if ret is not None else None
-    _check(lib().gx_run_batch(rt, ptr, n, prog_fd, rptr, _stream_handle(stream)), "gx_run_batch", rt)
+    if flags:
+        _check(lib().gx_run_batch_ex(rt, ptr, n, prog_fd, rptr, _stream_handle(stream), flags), "gx_run_batch_ex", rt)
+    else:
+        _check(lib().gx_run_batch(rt, ptr, n, prog_fd, rptr, _stream_handle(stream)), "gx_run_batch", rt)
+
+
+def gx_run_batch_ex(rt, events, n=None, prog_fd=-1, ret=None, stream=None, flags=0):
+    """gx_run_batch with launch flags (GX_RUN_OVERLAP)."""
+    gx_run_batch(rt, events, n=n, prog_fd=prog_fd, ret=ret, stream=stream, flags=flags)
 
 
 def gx_run_batch_host(rt, events: np.ndarray | int, n=None, prog_fd=-1, ret=None):
@@ -364,8 +377,8 @@ class Runtime:
         gx_attach(self.rt, prog, kind, tenant)
 
     # execution
-    def run(self, events, prog=-1, ret=None, stream=None):
-        gx_run_batch(self.rt, events, prog_fd=prog, ret=ret, stream=stream)
+    def run(self, events, prog=-1, ret=None, stream=None, overlap=False):
+        gx_run_batch(self.rt, events, prog_fd=prog, ret=ret, stream=stream, flags=GX_RUN_OVERLAP if overlap else 0)
 
     def stats(self) -> dict:
         return gx_get_stats(self.rt)

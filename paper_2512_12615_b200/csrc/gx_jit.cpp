@@ -99,6 +99,15 @@ struct Gen {
     }
 
     static std::string R(int r) { return "r" + std::to_string(r); }
+    /* physical address of a per-thread word: the constant-geometry form when the map's logical
+     * span fits 32-bit index arithmetic */
+    std::string ptp(int fd, const std::string &logical) {
+        const GxMapDesc &d = L.maps[fd];
+        if ((uint64_t)d.max_entries * d.value_size < (1ull << 31))
+            return "pt_phys_c<" + std::to_string(d.max_entries) + "u, " + std::to_string(d.value_size / 8) + "u>(" +
+                   hex(d.data) + ", " + logical + ", shard)";
+        return "gxd::pt_phys(" + md(fd) + ", " + logical + ", shard)";
+    }
     static std::string slot(int addr) { return "s" + std::to_string(addr >> 3); }
 
     /* Load hoisting inside basic blocks: a map / per-thread load moves above earlier instructions
@@ -377,10 +386,10 @@ struct Gen {
         case GX_LDX_PT:
             if (ptc_)
                 me("const uint64_t la_ = " + s + " + (int64_t)" + std::to_string(g.off) + "; " + d + " = " +
-                   ld_fix("ptc_ld(ptc, la_, gxd::pt_phys(" + md((int)g.imm) + ", la_, shard), " + std::to_string(lg) + ")") + ";");
+                   ld_fix("ptc_ld(ptc, la_, " + ptp((int)g.imm, "la_") + ", " + std::to_string(lg) + ")") + ";");
             else
-                me(d + " = " + ld_fix("gload<false>((uint64_t)gxd::pt_phys(" + md((int)g.imm) + ", " + s + " + (int64_t)" +
-                                      std::to_string(g.off) + ", shard), " + std::to_string(lg) + ")") + ";");
+                me(d + " = " + ld_fix("gload<false>((uint64_t)" + ptp((int)g.imm, s + " + (int64_t)" + std::to_string(g.off)) + ", " +
+                                      std::to_string(lg) + ")") + ";");
             break;
         case GX_ST_STACK: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
@@ -395,11 +404,10 @@ struct Gen {
         case GX_ST_PT: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
             if (ptc_)
-                me("const uint64_t la_ = " + d + " + (int64_t)" + std::to_string(g.off) + "; ptc_st(ptc, la_, gxd::pt_phys(" +
-                   md(g.aux >> 4) + ", la_, shard), " + std::to_string(lg) + ", " + v + ");");
+                me("const uint64_t la_ = " + d + " + (int64_t)" + std::to_string(g.off) + "; ptc_st(ptc, la_, " + ptp(g.aux >> 4, "la_") + ", " + std::to_string(lg) + ", " + v + ");");
             else
-                me("gstore((uint64_t)gxd::pt_phys(" + md(g.aux >> 4) + ", " + d + " + (int64_t)" + std::to_string(g.off) +
-                   ", shard), " + std::to_string(lg) + ", " + v + ");");
+                me("gstore((uint64_t)" + ptp(g.aux >> 4, d + " + (int64_t)" + std::to_string(g.off)) + ", " + std::to_string(lg) +
+                   ", " + v + ");");
             break;
         }
         case GX_ATOM_STACK: case GX_ATOM_PT: case GX_ATOM_MAP: atomic(g); break;
@@ -438,9 +446,8 @@ struct Gen {
                                             std::to_string(8 * w);
                 if (g.op == GX_CALL_UPDATE_ARRAY) b << " *(uint64_t *)(" << logical << ") = " << v << ";";
                 else if (ptc_)
-                    b << " { const uint64_t la_ = " << logical << "; ptc_st(ptc, la_, gxd::pt_phys(" << md(g.aux)
-                      << ", la_, shard), 3, " << v << "); }";
-                else b << " *(uint64_t *)gxd::pt_phys(" << md(g.aux) << ", " << logical << ", shard) = " << v << ";";
+                    b << " { const uint64_t la_ = " << logical << "; ptc_st(ptc, la_, " << ptp(g.aux, "la_") << ", 3, " << v << "); }";
+                else b << " *(uint64_t *)" << ptp(g.aux, logical) << " = " << v << ";";
             }
             b << " } if (rc) c_herr++; r0 = (uint64_t)rc;";
             me(b.str());
@@ -521,9 +528,9 @@ struct Gen {
         const int fd = g.aux >> 4;
         const std::string addr = R(g.dst) + " + (int64_t)" + std::to_string(g.off);
         if (g.op == GX_ATOM_PT) {
-            std::string e = ptc_ ? "ptc_rmw(ptc, " + addr + ", gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
+            std::string e = ptc_ ? "ptc_rmw(ptc, " + addr + ", " + ptp(fd, addr) + ", " +
                                        (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)"
-                                 : "rmw_global_private((uint64_t)gxd::pt_phys(" + md(fd) + ", " + addr + ", shard), " +
+                                 : "rmw_global_private((uint64_t)" + ptp(fd, addr) + ", " +
                                        (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
             me(fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";");
             return;
@@ -543,6 +550,13 @@ struct Gen {
             const uint32_t nw = m.max_entries * m.value_size / 8;
             st("group_priv_add(" + M() + ", spriv + " + std::to_string(m.priv_off / 4) + ", spriv + " + std::to_string(m.priv_off / 4 + nw) +
                ", (uint32_t)((" + addr + " - " + hex(m.data) + ") >> 3), " + v + ");");
+            return;
+        }
+        if (kop && (op & 0xF0) == 0) {
+            const std::string e = std::string("group_add_const<") + (w32 ? "true" : "false") + ", " + (fetch ? "true" : "false") +
+                                  ">(" + M() + ", " + addr + ", " + (w32 ? hex((uint32_t)(g.imm >> 32)) : v) + ")";
+            if (fetch) st("{ const uint64_t res_ = " + e + "; " + R(g.src) + " = res_; }");
+            else st("(void)" + e + ";");
             return;
         }
         std::string e = "group_atomic<" + std::to_string(op & 0xF0) + "u, " + (w32 ? "true" : "false") + ", " +
@@ -577,8 +591,57 @@ struct Gen {
              "  PtCache ptc;\n"
              "  const uint64_t nrec = (n + 31) >> 5;\n"
              "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
-             "  const uint64_t pol = evict_first_policy();\n";
-        if (S >= 2) {
+             "  const uint64_t pol = evict_first_policy();\n"
+             "  /* PDL (gx_run_batch_ex GX_RUN_OVERLAP): let the next batch's grid be scheduled; no-ops\n"
+             "   * for a plain launch */\n"
+             "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
+        const char *pdl_wait = "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\"); /* maps after the previous grid */\n";
+        if (S >= 2 && gx_jit_stage_mode() == 3) {
+            /* a1 through a block-wide ring of S stages, each one contiguous chunk of W = B/32 warp
+             * records (W KiB) brought in by ONE 1-D TMA bulk copy and signalled on the stage's
+             * mbarrier.  Block iteration t covers records (t * gridDim + blockIdx) * W + w; warp w
+             * runs record w of the stage.  The warp that releases a stage last (shared counter)
+             * refills it with chunk t + S -- no producer warp, no empty-barrier waits. */
+            const int W = B / 32;
+            o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
+                 "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
+                 "  __shared__ uint32_t gx_used[" << S << "];\n"
+                 "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(gx_ring);\n"
+                 "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
+                 "  const uint32_t wid = threadIdx.x >> 5;\n"
+                 "  const uint64_t gstride = (uint64_t)gridDim.x * " << W << ";\n"
+                 "  auto stage_issue = [&](uint32_t st, uint64_t t) {\n"
+                 "    const uint64_t r0_ = t * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
+                 "    if (r0_ >= nrec) return;\n"
+                 "    const uint64_t left_ = n - r0_ * 32;\n"
+                 "    const uint32_t bytes_ = left_ >= " << 32 * W << "ull ? " << 1024 * W << "u : (uint32_t)left_ * 32u;\n"
+                 "    bulk_load(ring_s + st * " << 1024 * W << "u, ev + r0_ * 64, bytes_, full_s + st * 8u, pol);\n"
+                 "  };\n"
+                 "  if (threadIdx.x == 0) {\n"
+                 "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); gx_used[k] = 0; }\n"
+                 "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+                 "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k);\n"
+                 "  }\n"
+                 "  __syncthreads();\n"
+              << pdl_wait <<
+                 "  uint32_t st = 0, ph = 0;\n"
+                 "  #pragma unroll 1\n"
+                 "  for (uint64_t t = 0;; t++) {\n"
+                 "    const uint64_t rec = t * gstride + (uint64_t)blockIdx.x * " << W << " + wid;\n"
+                 "    if (rec - wid >= nrec) break;\n"
+                 "    mbar_wait(full_s + st * 8u, ph);\n"
+                 "    const uint4 *slot_ = gx_ring + st * " << 64 * W << " + wid * 64;\n"
+                 "    const uint4 a = slot_[2 * lane], b = slot_[2 * lane + 1];\n"
+                 "    __syncwarp();\n"
+                 "    if (lane == 0 && atomicAdd(&gx_used[st], 1u) == " << W - 1 << "u) {\n"
+                 "      gx_used[st] = 0;\n"
+                 "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+                 "      stage_issue(st, t + " << S << ");\n"
+                 "    }\n"
+                 "    if (++st == " << S << "u) { st = 0; ph ^= 1u; }\n"
+                 "    const uint64_t i = rec * 32 + lane;\n"
+                 "    const bool valid = i < n;\n";
+        } else if (S >= 2) {
             /* a1 through a per-warp ring of S one-record (1 KiB) slots in dynamic shared memory:
              * record k+S-1 is in flight while record k runs.  Modes (GX_JIT_STAGE_MODE):
              *   0 lane: lane l cp.asyncs its own event's two 16-B halves to slot words l, 32+l
@@ -621,6 +684,7 @@ struct Gen {
             }
             o << "  #pragma unroll\n"
                  "  for (int k = 0; k < " << S - 1 << "; k++) " << issue("k", "rec0 + k * nwarps") << "\n"
+              << pdl_wait <<
                  "  uint32_t slot = 0;\n"
                  "  #pragma unroll 1\n"
                  "  for (uint64_t rec = rec0; rec < nrec; rec += nwarps) {\n"
@@ -643,6 +707,7 @@ struct Gen {
                  "    const uint64_t i = rec * 32 + lane;\n"
                  "    const bool valid = i < n;\n";
         } else {
+            o << pdl_wait;
             o << "  /* one warp = one 32-event record at a time (event lane == executor lane); U records per\n"
                  "   * iteration, their loads issued back to back */\n"
                  "  for (uint64_t rb = (uint64_t)blockIdx.x * " << B / 32 << " + (threadIdx.x >> 5); rb < nrec; rb += nwarps * " << U << ") {\n"
@@ -666,27 +731,32 @@ struct Gen {
         o << "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
              "    int p = -1;\n";
         if (L.single >= 0) {
-            o << "    if (valid) p = 0;\n";
+            /* one program for every event: the group is the record's valid lanes; the run count
+             * (= n) is added once at the end instead of per event */
+            o << "    (void)p;\n    uint64_t retv = 0;\n"
+                 "    const unsigned m = __ballot_sync(GX_ALL, valid);\n"
+                 "    if (m == GX_ALL) prog0<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                 "    else prog0<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n";
         } else {
             o << "    if (valid) { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
             for (int k = 0; k < GX_MAX_KINDS; k++)
                 for (int t = 0; t < 256; t++)
                     if (L.attach[k][t] >= 0) o << "      case " << k * 256 + t << ": p = " << (int)L.attach[k][t] << "; break;\n";
             o << "      default: break;\n      }\n    }\n";
+            o << "    uint64_t retv = 0;\n"
+                 "    if (valid) { if (p >= 0) c_run++; else c_skip++; }\n"
+                 "    unsigned todo = __ballot_sync(GX_ALL, p >= 0);\n"
+                 "    while (todo) {\n"
+                 "      const int pq = __shfl_sync(GX_ALL, p, __ffs(todo) - 1);\n"
+                 "      const unsigned m = __ballot_sync(GX_ALL, p == pq) & todo;\n"
+                 "      todo &= ~m;\n"
+                 "      switch (pq) {\n";
+            for (size_t q = 0; q < images.size(); q++)
+                o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                  << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n        break;\n";
+            o << "      default: break;\n      }\n    }\n";
         }
-        o << "    uint64_t retv = 0;\n"
-             "    if (valid) { if (p >= 0) c_run++; else c_skip++; }\n"
-             "    unsigned todo = __ballot_sync(GX_ALL, p >= 0);\n"
-             "    while (todo) {\n"
-             "      const int pq = __shfl_sync(GX_ALL, p, __ffs(todo) - 1);\n"
-             "      const unsigned m = __ballot_sync(GX_ALL, p == pq) & todo;\n"
-             "      todo &= ~m;\n"
-             "      switch (pq) {\n";
-        for (size_t q = 0; q < images.size(); q++)
-            o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
-              << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n        break;\n";
-        o << "      default: break;\n      }\n    }\n"
-             "    if (ret && valid) ret[i] = retv;\n" << (S >= 2 ? "  }\n" : "    }\n  }\n");
+        o <<              "    if (ret && valid) ret[i] = retv;\n" << (S >= 2 ? "  }\n" : "    }\n  }\n");
         o << "  ptc_flush(ptc);\n"
              "  for (int s = 16; s; s >>= 1) {\n"
              "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
@@ -710,6 +780,7 @@ struct Gen {
               << m.priv_off / 4 + nw << " + w] << 32);\n"
               << "    if (v) atomicAdd((unsigned long long *)" << hex(m.data) << " + w, (unsigned long long)v);\n  }\n";
         }
+        if (L.single >= 0) o << "  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&gstats[" << GXS_RUN << "], (unsigned long long)n);\n";
         o << "  if (threadIdx.x < 8 && sstats[threadIdx.x]) atomicAdd(&gstats[threadIdx.x], sstats[threadIdx.x]);\n}\n";
     }
 };
@@ -718,7 +789,7 @@ struct Gen {
 
 int gx_jit_stages() {
     static int s = [] {
-        int v = 0;
+        int v = 3; /* profiles/r1_jit_variants.md: 3 stages of 32 KiB beat 4 and 6 (L1 carve-out) */
         if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
         return std::max(0, std::min(8, v));
     }();
@@ -727,9 +798,9 @@ int gx_jit_stages() {
 
 int gx_jit_stage_mode() {
     static int m = [] {
-        int v = 2;
+        int v = 3;
         if (const char *e = getenv("GX_JIT_STAGE_MODE")) v = atoi(e);
-        return (v >= 0 && v <= 2) ? v : 2;
+        return (v >= 0 && v <= 3) ? v : 3;
     }();
     return m;
 }
@@ -738,7 +809,7 @@ int gx_jit_block() {
     static int b = [] {
         int v = 1024;
         if (const char *e = getenv("GX_JIT_BLOCK")) v = atoi(e);
-        return (v == 256 || v == 512 || v == 1024) ? v : 1024;
+        return (v >= 64 && v <= 1024 && v % 32 == 0) ? v : 1024;
     }();
     return b;
 }

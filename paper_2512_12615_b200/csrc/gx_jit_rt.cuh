@@ -350,6 +350,57 @@ __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, u
     return W32 ? (uint32_t)r : r;
 }
 
+/* ADD of a compile-time constant K (the verifier folded the source register: `mov r1, 1;
+ * atomic_add [r0], r1`).  Uniform address (one MATCH.ALL): the group's sum is K * popc(mask), no
+ * reduction; FETCH lanes get old + K * (their rank in the group).  Mixed addresses: per-lane RED
+ * (non-FETCH) or __match_any_sync groups with the same rank arithmetic (FETCH). */
+template <bool W32, bool FETCH>
+__device__ __forceinline__ uint64_t group_add_const(unsigned mask, uint64_t addr, uint64_t k) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    int same = 0;
+    const unsigned peers = __match_all_sync(mask, (unsigned long long)addr, &same);
+    if (same) {
+        const unsigned leader = __ffs(mask) - 1;
+        const uint64_t tot = k * (uint64_t)__popc(mask);
+        if (!FETCH) {
+            if (lane == leader) global_atomic(0x00, addr, tot, W32, false);
+            return 0;
+        }
+        uint64_t old = 0;
+        if (lane == leader) old = global_atomic(0x00, addr, tot, W32, true);
+        old = __shfl_sync(mask, old, leader);
+        const uint64_t r = old + k * (uint64_t)__popc(peers & lt);
+        return W32 ? (uint32_t)r : r;
+    }
+    if (!FETCH) {
+        global_atomic(0x00, addr, k, W32, false);
+        return 0;
+    }
+    const unsigned grp = __match_any_sync(mask, (unsigned long long)addr);
+    const unsigned gl = __ffs(grp) - 1;
+    uint64_t old = 0;
+    if (lane == gl) old = global_atomic(0x00, addr, k * (uint64_t)__popc(grp), W32, true);
+    old = __shfl_sync(grp, old, gl);
+    const uint64_t r = old + k * (uint64_t)__popc(grp & lt);
+    return W32 ? (uint32_t)r : r;
+}
+
+/* per-thread ARRAY physical address for the JIT: gxd::pt_word_index with the map geometry (K
+ * entries, W words per value, data) as compile-time constants, 32-bit index arithmetic and the
+ * per-thread part (q, l) loop-invariant -- the same layout the fold / merge kernels read */
+template <uint32_t K, uint32_t W>
+__device__ __forceinline__ uint8_t *pt_phys_c(uint64_t data, uint64_t logical, uint32_t shard) {
+    const uint32_t lo = (uint32_t)(logical - data);
+    const uint32_t wi = lo >> 3;
+    const uint32_t k = wi / W, w = wi % W;
+    const uint32_t l = shard & 31, q = shard >> 5;
+    const uint32_t r = l % K;
+    const uint32_t kk = (K & (K - 1)) == 0 ? ((k - r) & (K - 1)) : (k >= r ? k - r : k + K - r);
+    const uint64_t base = data + ((uint64_t)q * (K * W * 32) + l) * 8;
+    return reinterpret_cast<uint8_t *>(base + (uint64_t)(((kk * W + w) << 8) | (lo & 7)));
+}
+
 /* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory; one shared atomic
  * per group when the group adds to one word, else one per lane */
 __device__ __forceinline__ void priv_one(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {

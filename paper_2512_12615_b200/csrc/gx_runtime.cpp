@@ -111,6 +111,7 @@ struct Drv {
     CUresult (*occupancy)(int *, CUfunction, int, size_t) = nullptr;
     CUresult (*moduleUnload)(CUmodule) = nullptr;
     CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*launchKernelEx)(const CUlaunchConfig *, CUfunction, void **, void **) = nullptr;
 };
 Drv &drv() {
     static Drv d;
@@ -126,6 +127,8 @@ Drv &drv() {
                                       cudaEnableDefault, &q) == cudaSuccess;
         ok &= cudaGetDriverEntryPoint("cuModuleUnload", (void **)&d.moduleUnload, cudaEnableDefault, &q) == cudaSuccess;
         ok &= cudaGetDriverEntryPoint("cuFuncSetAttribute", (void **)&d.funcSetAttribute, cudaEnableDefault, &q) == cudaSuccess;
+        if (cudaGetDriverEntryPoint("cuLaunchKernelEx", (void **)&d.launchKernelEx, cudaEnableDefault, &q) != cudaSuccess)
+            d.launchKernelEx = nullptr;
         d.ok = ok && d.moduleLoadData && d.moduleGetFunction && d.launchKernel;
     }
     return d;
@@ -348,7 +351,8 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
     return 0;
 }
 
-int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream) {
+int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream,
+               uint32_t flags = 0) {
     if (rt->engine == GX_ENGINE_JIT) {
         int rc = jit_prepare(rt, cfg);
         if (rc) return rc;
@@ -367,8 +371,28 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         want = std::min<uint64_t>(cap, want);
         uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
         const unsigned smem = gx_jit_smem((int)B);
-        if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) != CUDA_SUCCESS)
+        if ((flags & GX_RUN_OVERLAP) && drv().launchKernelEx) {
+            /* programmatic dependent launch: the grid may start while the previous kernel on the
+             * stream drains; it stages its first records, then griddepcontrol.wait holds every map
+             * access until that kernel has completed and flushed (gx_jit.cpp) */
+            CUlaunchAttribute at[1];
+            at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+            at[0].value.programmaticStreamSerializationAllowed = 1;
+            CUlaunchConfig lc = {};
+            lc.gridDimX = grid;
+            lc.gridDimY = lc.gridDimZ = 1;
+            lc.blockDimX = (unsigned)B;
+            lc.blockDimY = lc.blockDimZ = 1;
+            lc.sharedMemBytes = smem;
+            lc.hStream = (CUstream)stream;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            if (drv().launchKernelEx(&lc, cfg.jfunc, args, nullptr) != CUDA_SUCCESS)
+                return set_err(rt, -EFAULT, "JIT kernel launch (PDL) failed");
+        } else if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) !=
+                   CUDA_SUCCESS) {
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
+        }
         rt->last_grid = grid;
         rt->last_block = (uint32_t)B;
         rt->last_smem = smem;
@@ -789,14 +813,19 @@ int gx_attach(gx_rt *rt, int prog_fd, uint32_t kind, uint32_t tenant) {
 }
 
 int gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, uint64_t *d_ret, void *stream) {
+    return gx_run_batch_ex(rt, d_events, n, prog_fd, d_ret, stream, 0);
+}
+
+int gx_run_batch_ex(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, uint64_t *d_ret, void *stream, uint32_t flags) {
     if (!rt) return -EINVAL;
+    if (flags & ~(uint32_t)GX_RUN_OVERLAP) return set_err(rt, -EINVAL, "unknown run flags 0x%x", flags);
     if (n == 0) return 0;
     if (!d_events || ((uintptr_t)d_events & 31)) return set_err(rt, -EINVAL, "events must be 32-byte aligned device memory");
     if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
     LaunchCfg *cfg;
     int rc = get_launch(rt, prog_fd, cfg);
     if (rc) return rc;
-    return launch_cfg(rt, *cfg, d_events, n, d_ret, (cudaStream_t)stream);
+    return launch_cfg(rt, *cfg, d_events, n, d_ret, (cudaStream_t)stream, flags);
 }
 
 int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, uint64_t *h_ret) {

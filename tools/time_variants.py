@@ -19,14 +19,21 @@ VARIANTS = {
     "hist_only": HIST_ONLY,
     "pt_only": PT_ONLY,
     "p2": P2,
+    "p1": programs.P1,
+    "p1d": programs.P1D,
 }
 peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
 n = 1 << int(sys.argv[1] if len(sys.argv) > 1 else 30)
+ONLY = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 for cfg in ("C2", "C1"):
     ev = gen_gpu.generate_device(cfg, configs.SEEDS[cfg], n)
     for name, text in VARIANTS.items():
+        if ONLY and name not in ONLY:
+            continue
         rt = gx.Runtime(0, engine=gx.GX_ENGINE_JIT)
-        fds = {k: rt.create_map(s.type, s.key_size, s.value_size, s.max_entries) for k, s in programs.P2_MAPS.items()}
+        specs = dict(programs.P2_MAPS)
+        specs.update(programs.P1_MAPS if name == "p1" else programs.P1D_MAPS if name == "p1d" else {})
+        fds = {k: rt.create_map(s.type, s.key_size, s.value_size, s.max_entries) for k, s in specs.items()}
         fd = rt.load_prog(asm.assemble(text, fds))
         for _ in range(3):
             rt.run(ev, fd)
