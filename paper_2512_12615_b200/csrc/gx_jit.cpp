@@ -578,7 +578,8 @@ struct Gen {
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
         const int S = gx_jit_stages();
-        o << "extern \"C\" __global__ void __launch_bounds__(" << B << (minb > 0 ? ", " + std::to_string(minb) : std::string()) << ") gx_jit_kernel(const uint4 *__restrict__ ev, "
+        /* the launch body, instantiated twice: gx_jit_kernel (no per-event R0) and gx_jit_kernel_r */
+        o << "template <bool WANT_RET>\n__device__ __forceinline__ void gx_body(const uint4 *__restrict__ ev, "
              "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
@@ -610,8 +611,7 @@ struct Gen {
                  "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
                  "  const uint32_t wid = threadIdx.x >> 5;\n"
                  "  const uint64_t gstride = (uint64_t)gridDim.x * " << W << ";\n"
-                 "  auto stage_issue = [&](uint32_t st, uint64_t t) {\n"
-                 "    const uint64_t r0_ = t * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
+                 "  auto stage_issue = [&](uint32_t st, uint64_t r0_) {\n"
                  "    if (r0_ >= nrec) return;\n"
                  "    const uint64_t left_ = n - r0_ * 32;\n"
                  "    const uint32_t bytes_ = left_ >= " << 32 * W << "ull ? " << 1024 * W << "u : (uint32_t)left_ * 32u;\n"
@@ -620,27 +620,25 @@ struct Gen {
                  "  if (threadIdx.x == 0) {\n"
                  "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); gx_used[k] = 0; }\n"
                  "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
-                 "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k);\n"
+                 "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k * gstride + (uint64_t)blockIdx.x * " << W << ");\n"
                  "  }\n"
                  "  __syncthreads();\n"
               << pdl_wait <<
                  "  uint32_t st = 0, ph = 0;\n"
+                 "  const uint32_t my_ring = ring_s + wid * 1024u + lane * 32u;\n"
+                 "  const uint32_t used_s = (uint32_t)__cvta_generic_to_shared(gx_used);\n"
                  "  #pragma unroll 1\n"
-                 "  for (uint64_t t = 0;; t++) {\n"
-                 "    const uint64_t rec = t * gstride + (uint64_t)blockIdx.x * " << W << " + wid;\n"
-                 "    if (rec - wid >= nrec) break;\n"
+                 "  for (uint64_t rbase = (uint64_t)blockIdx.x * " << W << "; rbase < nrec; rbase += gstride) {\n"
+                 "    const uint64_t rec = rbase + wid;\n"
                  "    mbar_wait(full_s + st * 8u, ph);\n"
-                 "    const uint4 *slot_ = gx_ring + st * " << 64 * W << " + wid * 64;\n"
-                 "    const uint4 a = slot_[2 * lane], b = slot_[2 * lane + 1];\n"
+                 "    const uint4 a = lds128(my_ring + st * " << 1024 * W << "u), b = lds128(my_ring + st * " << 1024 * W << "u + 16u);\n"
                  "    __syncwarp();\n"
-                 "    if (lane == 0 && atomicAdd(&gx_used[st], 1u) == " << W - 1 << "u) {\n"
+                 "    if (lane == 0 && atoms_add(used_s + st * 4u, 1u) == " << W - 1 << "u) {\n"
                  "      gx_used[st] = 0;\n"
                  "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-                 "      stage_issue(st, t + " << S << ");\n"
+                 "      stage_issue(st, rbase + " << S << " * gstride);\n"
                  "    }\n"
-                 "    if (++st == " << S << "u) { st = 0; ph ^= 1u; }\n"
-                 "    const uint64_t i = rec * 32 + lane;\n"
-                 "    const bool valid = i < n;\n";
+                 "    if (++st == " << S << "u) { st = 0; ph ^= 1u; }\n";
         } else if (S >= 2) {
             /* a1 through a per-warp ring of S one-record (1 KiB) slots in dynamic shared memory:
              * record k+S-1 is in flight while record k runs.  Modes (GX_JIT_STAGE_MODE):
@@ -703,9 +701,7 @@ struct Gen {
                 o << "    const uint4 a = ring[slot * 64 + lane], b = ring[slot * 64 + 32 + lane];\n";
             else
                 o << "    const uint4 a = ring[slot * 64 + 2 * lane], b = ring[slot * 64 + 2 * lane + 1];\n";
-            o << "    slot = slot == " << S - 1 << "u ? 0u : slot + 1;\n"
-                 "    const uint64_t i = rec * 32 + lane;\n"
-                 "    const bool valid = i < n;\n";
+            o << "    slot = slot == " << S - 1 << "u ? 0u : slot + 1;\n";
         } else {
             o << pdl_wait;
             o << "  /* one warp = one 32-event record at a time (event lane == executor lane); U records per\n"
@@ -721,30 +717,35 @@ struct Gen {
                  "    for (int u = 0; u < " << U << "; u++) {\n"
                  "    const uint64_t rec = rb + u * nwarps;\n"
                  "    if (rec >= nrec) break;\n"
-                 "    const uint64_t i = rec * 32 + lane;\n"
-                 "    const bool valid = i < n;\n"
               << (punroll ? "    const uint4 a = ea[u], b = eb[u];\n"
                           : "    const uint4 a = ea[0], b = eb[0];\n"
                             "    #pragma unroll\n    for (int k = 0; k + 1 < " + std::to_string(U) +
                                 "; k++) { ea[k] = ea[k + 1]; eb[k] = eb[k + 1]; }\n");
         }
         o << "    Ctx c; c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w; c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;\n"
-             "    int p = -1;\n";
+             "    const uint64_t i = rec * 32 + lane;\n"
+             "    uint64_t retv = 0;\n";
         if (L.single >= 0) {
-            /* one program for every event: the group is the record's valid lanes; the run count
-             * (= n) is added once at the end instead of per event */
-            o << "    (void)p;\n    uint64_t retv = 0;\n"
-                 "    const unsigned m = __ballot_sync(GX_ALL, valid);\n"
-                 "    if (m == GX_ALL) prog0<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
-                 "    else prog0<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n";
+            /* one program for every event.  A whole record (the warp-uniform test rec*32+32 <= n) runs
+             * the whole-warp instance; a ragged tail record runs the masked one.  The run count (= n)
+             * is added once at the end instead of per event. */
+            o << "    if (rec * 32 + 32 <= n) {\n"
+                 "      prog0<true>(c, GX_ALL, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                 "      if (WANT_RET) ret[i] = retv;\n"
+                 "    } else {\n"
+                 "      const bool valid = i < n;\n"
+                 "      const unsigned m = __ballot_sync(GX_ALL, valid);\n"
+                 "      prog0<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                 "      if (WANT_RET && valid) ret[i] = retv;\n"
+                 "    }\n";
         } else {
-            o << "    if (valid) { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
+            o << "    const bool valid = i < n;\n    int p = -1;\n"
+                 "    if (valid) { const uint32_t kind = b.x & 0xFF, tenant = (b.x >> 8) & 0xFF;\n      switch (kind * 256 + tenant) {\n";
             for (int k = 0; k < GX_MAX_KINDS; k++)
                 for (int t = 0; t < 256; t++)
                     if (L.attach[k][t] >= 0) o << "      case " << k * 256 + t << ": p = " << (int)L.attach[k][t] << "; break;\n";
             o << "      default: break;\n      }\n    }\n";
-            o << "    uint64_t retv = 0;\n"
-                 "    if (valid) { if (p >= 0) c_run++; else c_skip++; }\n"
+            o << "    if (valid) { if (p >= 0) c_run++; else c_skip++; }\n"
                  "    unsigned todo = __ballot_sync(GX_ALL, p >= 0);\n"
                  "    while (todo) {\n"
                  "      const int pq = __shfl_sync(GX_ALL, p, __ffs(todo) - 1);\n"
@@ -754,9 +755,10 @@ struct Gen {
             for (size_t q = 0; q < images.size(); q++)
                 o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
                   << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n        break;\n";
-            o << "      default: break;\n      }\n    }\n";
+            o << "      default: break;\n      }\n    }\n"
+                 "    if (WANT_RET && valid) ret[i] = retv;\n";
         }
-        o <<              "    if (ret && valid) ret[i] = retv;\n" << (S >= 2 ? "  }\n" : "    }\n  }\n");
+        o << (S >= 2 ? "  }\n" : "    }\n  }\n");
         o << "  ptc_flush(ptc);\n"
              "  for (int s = 16; s; s >>= 1) {\n"
              "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
@@ -781,7 +783,12 @@ struct Gen {
               << "    if (v) atomicAdd((unsigned long long *)" << hex(m.data) << " + w, (unsigned long long)v);\n  }\n";
         }
         if (L.single >= 0) o << "  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&gstats[" << GXS_RUN << "], (unsigned long long)n);\n";
-        o << "  if (threadIdx.x < 8 && sstats[threadIdx.x]) atomicAdd(&gstats[threadIdx.x], sstats[threadIdx.x]);\n}\n";
+        o << "  if (threadIdx.x < 8 && sstats[threadIdx.x]) atomicAdd(&gstats[threadIdx.x], sstats[threadIdx.x]);\n}\n\n";
+        const std::string lb = "__launch_bounds__(" + std::to_string(B) + (minb > 0 ? ", " + std::to_string(minb) : std::string()) + ")";
+        o << "extern \"C\" __global__ void " << lb << " gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
+             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n  gx_body<false>(ev, n, ret, gstats);\n}\n"
+             "extern \"C\" __global__ void " << lb << " gx_jit_kernel_r(const uint4 *__restrict__ ev, uint64_t n, "
+             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n  gx_body<true>(ev, n, ret, gstats);\n}\n";
     }
 };
 

@@ -70,9 +70,23 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    /* suspend-time hint: sleep until the phase completes instead of re-polling */
     asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
                  "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+}
+
+/* 16-B shared load / 32-bit shared atomic on 32-bit shared-window addresses (no generic->shared
+ * conversion per access); ordered after the stage's mbarrier wait by the memory clobbers */
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 r;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
+    uint32_t o;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
 }
 
 __device__ __forceinline__ uint64_t sx(uint64_t v, unsigned bits) {

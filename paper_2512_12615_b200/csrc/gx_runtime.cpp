@@ -95,7 +95,8 @@ struct LaunchCfg {
     /* JIT engine */
     bool jit_tried = false;
     CUmodule jmod = nullptr;
-    CUfunction jfunc = nullptr;
+    CUfunction jfunc = nullptr;   /* gx_jit_kernel: no per-event R0 */
+    CUfunction jfunc_r = nullptr; /* gx_jit_kernel_r: writes d_ret */
     uint32_t jgrid = 0, jblock = 256;
     std::string jit_log;
     double jit_ms = 0;
@@ -330,12 +331,18 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         CUmodule mod = nullptr;
         CUfunction fn = nullptr;
         if (d.moduleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
-        if (d.moduleGetFunction(&fn, mod, "gx_jit_kernel") != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
+        CUfunction fn_r = nullptr;
+        if (d.moduleGetFunction(&fn, mod, "gx_jit_kernel") != CUDA_SUCCESS ||
+            d.moduleGetFunction(&fn_r, mod, "gx_jit_kernel_r") != CUDA_SUCCESS)
+            return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
         const unsigned smem = gx_jit_smem(B);
-        if (smem && d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+        if (smem && (d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS ||
+                     d.funcSetAttribute(fn_r, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS))
             return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
         int bps = 0;
+        int bps_r = 0;
         if (!d.occupancy || d.occupancy(&bps, fn, B, smem) != CUDA_SUCCESS || bps < 1) bps = 1;
+        if (d.occupancy && d.occupancy(&bps_r, fn_r, B, smem) == CUDA_SUCCESS && bps_r >= 1) bps = std::min(bps, bps_r);
         bps = std::min(bps, 2048 / B); /* per-thread shards: at most 2048 resident threads per SM */
         if (bps * B < 1024 && B != 256) {
             if (d.moduleUnload) d.moduleUnload(mod);
@@ -343,6 +350,7 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         }
         cfg.jmod = mod;
         cfg.jfunc = fn;
+        cfg.jfunc_r = fn_r;
         cfg.jblock = (uint32_t)B;
         cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
         break;
@@ -387,9 +395,9 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
             lc.hStream = (CUstream)stream;
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (drv().launchKernelEx(&lc, cfg.jfunc, args, nullptr) != CUDA_SUCCESS)
+            if (drv().launchKernelEx(&lc, d_ret ? cfg.jfunc_r : cfg.jfunc, args, nullptr) != CUDA_SUCCESS)
                 return set_err(rt, -EFAULT, "JIT kernel launch (PDL) failed");
-        } else if (drv().launchKernel(cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) !=
+        } else if (drv().launchKernel(d_ret ? cfg.jfunc_r : cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) !=
                    CUDA_SUCCESS) {
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
         }
