@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdlib>
 #include <mutex>
 #include <set>
@@ -177,8 +178,48 @@ struct Gen {
                (is_lookup(g.op) && (g.flags & (GXF_FETCH | GXF_W32)));
     }
 
+    /* If-conversion: a conditional jump whose one or two arms are short runs of collective-free
+     * instructions that meet again (`jcc L; B...; ja J; L: ...; J:` or `jcc J; B...; J:`) is
+     * compiled as per-lane predicated code -- no ballot, no divergence, no min-PC round trip.
+     * Each lane still executes exactly its own path, so the result is the scalar one.  (C4's
+     * binary search: `jgt r2, r7, left; mov r8, r1; ja next; left: mov r9, r1; next:`.) */
+    struct IfConv {
+        uint32_t b0, b1, l0, l1, join;
+    };
+    std::map<uint32_t, IfConv> ifconv_;
+    const GxInsn *im_ = nullptr;
+    static bool simple(const GxInsn &g) {
+        if (g.op == GX_JA || g.op == GX_EXIT || g.op == GX_OP_NOP || is_jcc(g.op)) return false;
+        if (g.op >= GX_CALL_LOOKUP_ARRAY) return false;
+        if (g.op == GX_ATOM_STACK || g.op == GX_ATOM_MAP || g.op == GX_ATOM_PT) return false;
+        return true;
+    }
+    void find_ifconv(const GxInsn *im, uint32_t n, const std::map<uint32_t, int> &tcount) {
+        ifconv_.clear();
+        auto is_target = [&](uint32_t k) { return tcount.count(k) != 0; };
+        for (uint32_t i = 0; i < n; i++) {
+            if (!is_jcc(im[i].op)) continue;
+            const uint32_t t = im[i].aux;
+            if (t <= i + 1 || t > n || is_target(i + 1)) continue;
+            uint32_t e = i + 1;
+            while (e < n && e < t && simple(im[e]) && (e == i + 1 || !is_target(e)) && e - i <= 16) e++;
+            if (e == t) { /* triangle: B = [i+1, t), join t */
+                ifconv_[i] = {i + 1, t, t, t, t};
+                continue;
+            }
+            if (e < n && im[e].op == GX_JA && e + 1 == t && tcount.at(t) == 1) {
+                const uint32_t J = im[e].aux;
+                if (J <= t || J > n) continue;
+                uint32_t f = t;
+                while (f < J && simple(im[f]) && (f == t || !is_target(f)) && f - t <= 16) f++;
+                if (f == J) ifconv_[i] = {i + 1, e, t, J, J};
+            }
+        }
+    }
+
     std::ostringstream *out_ = nullptr;
     bool dmode_ = false; /* emitting the min-PC (diverged) copy of a block */
+    bool ifconv_on_ = true; /* GX_JIT_IFCONV=0: off */
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
     void me(const std::string &x) { (*out_) << "  { " << x << " }\n"; }
@@ -199,13 +240,17 @@ struct Gen {
      * runtime-mask convergence checks (REDUX.OR + BRA.DIV per collective, profiles/r1_ncu_c2_jit.md). */
     void program(int q, const GxInsn *im0, uint32_t n) {
         std::set<uint32_t> targets, leaders{0};
+        std::map<uint32_t, int> tcount;
         for (uint32_t i = 0; i < n; i++) {
             const GxInsn &g = im0[i];
-            if (g.op == GX_JA || is_jcc(g.op)) targets.insert(g.aux);
-            if (is_lookup(g.op) && (g.flags & (GXF_FETCH | GXF_W32))) targets.insert((uint32_t)g.imm);
+            if (g.op == GX_JA || is_jcc(g.op)) targets.insert(g.aux), tcount[g.aux]++;
+            if (is_lookup(g.op) && (g.flags & (GXF_FETCH | GXF_W32))) targets.insert((uint32_t)g.imm), tcount[(uint32_t)g.imm]++;
         }
         std::vector<GxInsn> sched = hoist_loads(im0, n, targets);
         const GxInsn *im = sched.data();
+        im_ = im;
+        if (ifconv_on_) find_ifconv(im, n, tcount);
+        else ifconv_.clear();
         for (uint32_t t : targets) leaders.insert(t);
         for (uint32_t i = 0; i < n; i++)
             if (ends_block(im[i]) && i + 1 < n) leaders.insert(i + 1);
@@ -506,7 +551,25 @@ struct Gen {
                 case GX_JSLE: c = sa + " <= " + sb; break;
                 default: c = "(" + a + " & " + b + ") != 0"; break;
                 }
-                branch(c, g.aux, i + 1);
+                auto ic = ifconv_.find(i);
+                if (ic != ifconv_.end()) {
+                    const IfConv &v = ic->second;
+                    st("{ const bool t_ = " + c + ";");
+                    if (v.b1 > v.b0) {
+                        st("if (!t_) {");
+                        for (uint32_t k = v.b0; k < v.b1; k++) insn(im_[k], k);
+                        st("}");
+                    }
+                    if (v.l1 > v.l0) {
+                        st("if (t_) {");
+                        for (uint32_t k = v.l0; k < v.l1; k++) insn(im_[k], k);
+                        st("}");
+                    }
+                    goto_next(v.join);
+                    st("}");
+                } else {
+                    branch(c, g.aux, i + 1);
+                }
             } else {
                 st("c_herr++;");
                 exit_lanes("0");
@@ -574,12 +637,29 @@ struct Gen {
         const int minb = getenv("GX_JIT_MINB") ? atoi(getenv("GX_JIT_MINB")) : 1;
         const bool punroll = !getenv("GX_JIT_PUNROLL") || atoi(getenv("GX_JIT_PUNROLL")) != 0;
         ptc_ = getenv("GX_JIT_PTCACHE") && atoi(getenv("GX_JIT_PTCACHE")) != 0;
+        ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
+        if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
-        const uint32_t priv_words = (L.priv_bytes + 3) / 4;
+        /* two launch bodies: event ingest through the block-wide TMA ring (large batches of light
+         * programs) and through per-lane register loads (small batches, ALU-heavy programs) --
+         * the runtime picks per launch (gx_runtime.cpp launch_cfg) */
         const int S = gx_jit_stages();
-        /* the launch body, instantiated twice: gx_jit_kernel (no per-event R0) and gx_jit_kernel_r */
-        o << "template <bool WANT_RET>\n__device__ __forceinline__ void gx_body(const uint4 *__restrict__ ev, "
+        body("gx_body_ring", S >= 2 ? S : 3, B, U, punroll, images);
+        body("gx_body_reg", 0, B, U, punroll, images);
+        const std::string lb = "__launch_bounds__(" + std::to_string(B) + (minb > 0 ? ", " + std::to_string(minb) : std::string()) + ")";
+        const char *args = "(const uint4 *__restrict__ ev, uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats)";
+        o << "extern \"C\" __global__ void " << lb << " gx_jit_kernel" << args << " {\n  gx_body_ring<false>(ev, n, ret, gstats);\n}\n"
+          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_r" << args << " {\n  gx_body_ring<true>(ev, n, ret, gstats);\n}\n"
+          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_g" << args << " {\n  gx_body_reg<false>(ev, n, ret, gstats);\n}\n"
+          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_gr" << args << " {\n  gx_body_reg<true>(ev, n, ret, gstats);\n}\n";
+    }
+
+    /* one launch body (template on WANT_RET: write per-event R0) with S-stage ring ingest (S >= 2)
+     * or register ingest (S == 0) */
+    void body(const std::string &fname, int S, int B, int U, bool punroll, const std::vector<const GxInsn *> &images) {
+        const uint32_t priv_words = (L.priv_bytes + 3) / 4;
+        o << "template <bool WANT_RET>\n__device__ __forceinline__ void " << fname << "(const uint4 *__restrict__ ev, "
              "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
@@ -600,13 +680,15 @@ struct Gen {
         if (S >= 2 && gx_jit_stage_mode() == 3) {
             /* a1 through a block-wide ring of S stages, each one contiguous chunk of W = B/32 warp
              * records (W KiB) brought in by ONE 1-D TMA bulk copy and signalled on the stage's
-             * mbarrier.  Block iteration t covers records (t * gridDim + blockIdx) * W + w; warp w
-             * runs record w of the stage.  The warp that releases a stage last (shared counter)
-             * refills it with chunk t + S -- no producer warp, no empty-barrier waits. */
+             * mbarrier.  The block's chunk c covers records (c * gridDim + blockIdx) * W + w.  Warps
+             * claim records in order from a shared counter (dynamic, so uneven per-record cost does
+             * not stall the ring); the warp that reads a stage's last record (shared counter)
+             * refills it with chunk c + S -- no producer warp, no empty-barrier waits. */
             const int W = B / 32;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
+                 "  __shared__ uint32_t gx_next;\n"
                  "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(gx_ring);\n"
                  "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
                  "  const uint32_t wid = threadIdx.x >> 5;\n"
@@ -619,26 +701,36 @@ struct Gen {
                  "  };\n"
                  "  if (threadIdx.x == 0) {\n"
                  "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); gx_used[k] = 0; }\n"
+                 "    gx_next = 0;\n"
                  "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
                  "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k * gstride + (uint64_t)blockIdx.x * " << W << ");\n"
                  "  }\n"
                  "  __syncthreads();\n"
               << pdl_wait <<
-                 "  uint32_t st = 0, ph = 0;\n"
-                 "  const uint32_t my_ring = ring_s + wid * 1024u + lane * 32u;\n"
+                 "  const uint32_t my_ring = ring_s + lane * 32u;\n"
                  "  const uint32_t used_s = (uint32_t)__cvta_generic_to_shared(gx_used);\n"
+                 "  const uint32_t next_s = (uint32_t)__cvta_generic_to_shared(&gx_next);\n"
                  "  #pragma unroll 1\n"
-                 "  for (uint64_t rbase = (uint64_t)blockIdx.x * " << W << "; rbase < nrec; rbase += gstride) {\n"
-                 "    const uint64_t rec = rbase + wid;\n"
-                 "    mbar_wait(full_s + st * 8u, ph);\n"
-                 "    const uint4 a = lds128(my_ring + st * " << 1024 * W << "u), b = lds128(my_ring + st * " << 1024 * W << "u + 16u);\n"
+                 "  for (;;) {\n"
+                 "    /* claim the block's next record: warps are not tied to a slot, so a slow record\n"
+                 "     * (a long program, a diverged warp) does not hold back the stage refills */\n"
+                 "    uint32_t r_ = 0;\n"
+                 "    if (lane == 0) r_ = atoms_add(next_s, 1u);\n"
+                 "    r_ = __shfl_sync(GX_ALL, r_, 0);\n"
+                 "    const uint32_t c_ = r_ / " << W << "u, w_ = r_ % " << W << "u;\n"
+                 "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
+                 "    if (rbase >= nrec) break;\n"
+                 "    const uint64_t rec = rbase + w_;\n"
+                 "    const uint32_t st = c_ % " << S << "u;\n"
+                 "    mbar_wait(full_s + st * 8u, (c_ / " << S << "u) & 1u);\n"
+                 "    const uint32_t ra_ = my_ring + st * " << 1024 * W << "u + w_ * 1024u;\n"
+                 "    const uint4 a = lds128(ra_), b = lds128(ra_ + 16u);\n"
                  "    __syncwarp();\n"
                  "    if (lane == 0 && atoms_add(used_s + st * 4u, 1u) == " << W - 1 << "u) {\n"
                  "      gx_used[st] = 0;\n"
                  "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
                  "      stage_issue(st, rbase + " << S << " * gstride);\n"
-                 "    }\n"
-                 "    if (++st == " << S << "u) { st = 0; ph ^= 1u; }\n";
+                 "    }\n";
         } else if (S >= 2) {
             /* a1 through a per-warp ring of S one-record (1 KiB) slots in dynamic shared memory:
              * record k+S-1 is in flight while record k runs.  Modes (GX_JIT_STAGE_MODE):
@@ -784,11 +876,6 @@ struct Gen {
         }
         if (L.single >= 0) o << "  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&gstats[" << GXS_RUN << "], (unsigned long long)n);\n";
         o << "  if (threadIdx.x < 8 && sstats[threadIdx.x]) atomicAdd(&gstats[threadIdx.x], sstats[threadIdx.x]);\n}\n\n";
-        const std::string lb = "__launch_bounds__(" + std::to_string(B) + (minb > 0 ? ", " + std::to_string(minb) : std::string()) + ")";
-        o << "extern \"C\" __global__ void " << lb << " gx_jit_kernel(const uint4 *__restrict__ ev, uint64_t n, "
-             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n  gx_body<false>(ev, n, ret, gstats);\n}\n"
-             "extern \"C\" __global__ void " << lb << " gx_jit_kernel_r(const uint4 *__restrict__ ev, uint64_t n, "
-             "uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n  gx_body<true>(ev, n, ret, gstats);\n}\n";
     }
 };
 

@@ -22,5 +22,5 @@ int gx_jit_stages();
 int gx_jit_stage_mode();
 inline unsigned gx_jit_smem(int block) {
     const int s = gx_jit_stages();
-    return s >= 2 ? (unsigned)(block / 32) * (unsigned)s * 1024u : 0u;
+    return (unsigned)(block / 32) * (unsigned)(s >= 2 ? s : 3) * 1024u; /* the ring instances' stages */
 }

@@ -69,11 +69,20 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
+#ifndef GX_WAIT_HINT
+#define GX_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    /* suspend-time hint: sleep until the phase completes instead of re-polling */
+#if GX_WAIT_HINT > 0
+    /* suspend-time hint (ns): sleep until the phase completes instead of re-polling */
     asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(phase), "n"(GX_WAIT_HINT) : "memory");
+#else
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
                  "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+#endif
 }
 
 /* 16-B shared load / 32-bit shared atomic on 32-bit shared-window addresses (no generic->shared

@@ -97,6 +97,8 @@ struct LaunchCfg {
     CUmodule jmod = nullptr;
     CUfunction jfunc = nullptr;   /* gx_jit_kernel: no per-event R0 */
     CUfunction jfunc_r = nullptr; /* gx_jit_kernel_r: writes d_ret */
+    CUfunction jfunc_g = nullptr, jfunc_gr = nullptr; /* register-ingest instances */
+    bool ring_ok = true;
     uint32_t jgrid = 0, jblock = 256;
     std::string jit_log;
     double jit_ms = 0;
@@ -329,28 +331,37 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         std::vector<char> cubin;
         if (gx_jit_compile(src, cubin, cfg.jit_log)) return set_err(rt, -ENOSYS, "JIT compile failed: %s", cfg.jit_log.c_str());
         CUmodule mod = nullptr;
-        CUfunction fn = nullptr;
         if (d.moduleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
-        CUfunction fn_r = nullptr;
-        if (d.moduleGetFunction(&fn, mod, "gx_jit_kernel") != CUDA_SUCCESS ||
-            d.moduleGetFunction(&fn_r, mod, "gx_jit_kernel_r") != CUDA_SUCCESS)
-            return set_err(rt, -EFAULT, "cuModuleGetFunction failed");
+        /* ring ingest (no R0 / R0), register ingest (no R0 / R0) */
+        static const char *names[4] = {"gx_jit_kernel", "gx_jit_kernel_r", "gx_jit_kernel_g", "gx_jit_kernel_gr"};
+        CUfunction fn[4] = {};
+        for (int k = 0; k < 4; k++)
+            if (d.moduleGetFunction(&fn[k], mod, names[k]) != CUDA_SUCCESS)
+                return set_err(rt, -EFAULT, "cuModuleGetFunction(%s) failed", names[k]);
         const unsigned smem = gx_jit_smem(B);
-        if (smem && (d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS ||
-                     d.funcSetAttribute(fn_r, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS))
-            return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
-        int bps = 0;
-        int bps_r = 0;
-        if (!d.occupancy || d.occupancy(&bps, fn, B, smem) != CUDA_SUCCESS || bps < 1) bps = 1;
-        if (d.occupancy && d.occupancy(&bps_r, fn_r, B, smem) == CUDA_SUCCESS && bps_r >= 1) bps = std::min(bps, bps_r);
-        bps = std::min(bps, 2048 / B); /* per-thread shards: at most 2048 resident threads per SM */
+        for (int k = 0; k < 2; k++)
+            if (d.funcSetAttribute(fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+                return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
+        int bps = 2048 / B; /* per-thread shards: at most 2048 resident threads per SM */
+        for (int k = 0; k < 4; k++) {
+            int b = 0;
+            if (!d.occupancy || d.occupancy(&b, fn[k], B, k < 2 ? smem : 0) != CUDA_SUCCESS || b < 1) b = 1;
+            bps = std::min(bps, b);
+        }
         if (bps * B < 1024 && B != 256) {
             if (d.moduleUnload) d.moduleUnload(mod);
             continue;
         }
         cfg.jmod = mod;
-        cfg.jfunc = fn;
-        cfg.jfunc_r = fn_r;
+        cfg.jfunc = fn[0];
+        cfg.jfunc_r = fn[1];
+        cfg.jfunc_g = fn[2];
+        cfg.jfunc_gr = fn[3];
+        /* ALU-heavy single programs (a bounded loop: > 64 instructions on the worst path) keep
+         * per-lane register ingest -- the ring's per-record bookkeeping costs more than it hides */
+        uint64_t worst = 0;
+        for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
+        cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
         cfg.jblock = (uint32_t)B;
         cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
         break;
@@ -378,7 +389,13 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         if (want * 2 >= cfg.jgrid) want = cfg.jgrid; /* past half the resident grid: every SM streams */
         want = std::min<uint64_t>(cap, want);
         uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
-        const unsigned smem = gx_jit_smem((int)B);
+        /* ingest: the TMA ring for large batches (>= 2^22 events) of light programs, per-lane register
+         * loads otherwise (GX_JIT_INGEST=ring|reg forces one; profiles/r1_jit_variants.md) */
+        const char *fe = getenv("GX_JIT_INGEST");
+        const int force = !fe ? 0 : strcmp(fe, "ring") == 0 ? 1 : strcmp(fe, "reg") == 0 ? 2 : 0;
+        const bool ring = force == 1 || (force == 0 && cfg.ring_ok && n >= (1ull << 22));
+        CUfunction fnl = ring ? (d_ret ? cfg.jfunc_r : cfg.jfunc) : (d_ret ? cfg.jfunc_gr : cfg.jfunc_g);
+        const unsigned smem = ring ? gx_jit_smem((int)B) : 0u;
         if ((flags & GX_RUN_OVERLAP) && drv().launchKernelEx) {
             /* programmatic dependent launch: the grid may start while the previous kernel on the
              * stream drains; it stages its first records, then griddepcontrol.wait holds every map
@@ -395,9 +412,9 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
             lc.hStream = (CUstream)stream;
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (drv().launchKernelEx(&lc, d_ret ? cfg.jfunc_r : cfg.jfunc, args, nullptr) != CUDA_SUCCESS)
+            if (drv().launchKernelEx(&lc, fnl, args, nullptr) != CUDA_SUCCESS)
                 return set_err(rt, -EFAULT, "JIT kernel launch (PDL) failed");
-        } else if (drv().launchKernel(d_ret ? cfg.jfunc_r : cfg.jfunc, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) !=
+        } else if (drv().launchKernel(fnl, grid, 1, 1, (unsigned)B, 1, 1, smem, (CUstream)stream, args, nullptr) !=
                    CUDA_SUCCESS) {
             return set_err(rt, -EFAULT, "JIT kernel launch failed");
         }

@@ -28,12 +28,19 @@ def oracle_run(config, ev, threshold=None):
     return env, s, r0
 
 
-ENGINES = ("interp", "jit")
+# "jit" lets the runtime pick the event ingest per launch (register loads below 2^22 events, so
+# every small parity case); "jit_ring" forces the block-wide TMA ring the large bench batches use.
+ENGINES = ("interp", "jit", "jit_ring")
 
 
 def make_runtime(engine="jit"):
+    import os
     import paper_2512_12615_b200 as gx
-    return gx.Runtime(0, engine=gx.GX_ENGINE_JIT if engine == "jit" else gx.GX_ENGINE_INTERP)
+    if engine == "jit_ring":
+        os.environ["GX_JIT_INGEST"] = "ring"
+    else:
+        os.environ.pop("GX_JIT_INGEST", None)
+    return gx.Runtime(0, engine=gx.GX_ENGINE_INTERP if engine == "interp" else gx.GX_ENGINE_JIT)
 
 
 def gpu_run(config, ev, threshold=None, want_r0=True, runtime=None, engine="jit"):

@@ -266,8 +266,9 @@ def test_perthread_stress_parity(gpu, engine, n):
         assert rt.dump(fg[k]) == env.dump(fo[k]), k
 
 
+@pytest.mark.parametrize("engine", ["jit", "jit_ring"])
 @pytest.mark.parametrize("config", ["C2", "C3", "C5"])
-def test_overlapped_batches_parity(gpu, config):
+def test_overlapped_batches_parity(gpu, config, engine):
     """gx_run_batch_ex(GX_RUN_OVERLAP): back-to-back batches launched with programmatic dependent
     launch keep the sequential semantics of one stream (S1): after 4 overlapped batches the maps and
     ringbuf equal the oracle's over the concatenated events."""
@@ -275,7 +276,7 @@ def test_overlapped_batches_parity(gpu, config):
     n = (1 << 16) + 96
     ev = configs.events(config, configs.SEEDS[config], 4 * n)
     env, so, _ = oracle_run(config, ev, threshold=2 if config == "C3" else None)
-    rt = make_runtime("jit")
+    rt = make_runtime(engine)
     s = configs.setup(rt, config, threshold=2 if config == "C3" else None)
     d_ev = torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda()
     for k in range(4):
