@@ -25,8 +25,10 @@ TENANTS = {
     "C3": [(0, "P3", (0,))],
     "C4": [(0, "P4", (0,))],
     "C5": [(0, "P1", (0,)), (1, "P2", (0,)), (2, "P3f", (0, 2)), (3, "P4", (0,))],
+    "C6": [(0, "P6", (0,))],
 }
-GEN_CONFIG = {"C1": "C1", "C1d": "C1", "C2": "C2", "C3": "C3", "C4": "C4", "C5": "C5"}
+# C6 (f2, prefetch policy) reads the C3 LLM page trace
+GEN_CONFIG = {"C1": "C1", "C1d": "C1", "C2": "C2", "C3": "C3", "C4": "C4", "C5": "C5", "C6": "C3"}
 
 
 @dataclass
@@ -65,4 +67,4 @@ def events(config: str, seed: int, n: int, i0: int = 0, n_total: int | None = No
 
 
 SEEDS = {"C1": 0x5EED0001, "C1d": 0x5EED0001, "C2": 0x5EED0002, "C3": 0x5EED0003,
-         "C4": 0x5EED0004, "C5": 0x5EED0005}
+         "C4": 0x5EED0004, "C5": 0x5EED0005, "C6": 0x5EED0003}

@@ -55,7 +55,8 @@ def generate_device(config: str, seed: int, n: int, i0: int = 0, n_total: int | 
         out = torch.empty((n, 32), dtype=torch.uint8, device=torch.device("cuda", device))
     tabs = _tables(device)
     s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
-    config = {"C1d": "C1"}.get(config, config)
+    from .configs import GEN_CONFIG
+    config = GEN_CONFIG.get(config, config)
     rc = _lib().gxgen_generate(gen.CONFIG_ID[config], seed, i0, n, n_total, *[x.data_ptr() for x in tabs],
                                out.data_ptr(), s)
     if rc:

@@ -15,7 +15,8 @@ from dataclasses import dataclass
 
 from .asm import assemble
 
-HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF = 1, 2, 6, 27
+HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF, PREFETCH_QUEUE = 1, 2, 6, 27, 64
+FN_MEM_PREFETCH = 1000   # gdev_mem_prefetch (F-1)
 HOOK_ACCESS, HOOK_BLOCK_ENTER, HOOK_FAULT = 0, 1, 2
 
 
@@ -288,8 +289,32 @@ P4_MAPS = {"cfg": MapSpec(ARRAY, 4, 8, 1), "cstat": MapSpec(ARRAY, 4, 8, 4),
            "bounds": MapSpec(ARRAY, 4, 8, 4097), "list_hits": MapSpec(HASH, 4, 8, 4096),
            "list_bytes": MapSpec(ARRAY, 4, 8, 4096), "scan_pt": MapSpec(PERTHREAD_ARRAY, 4, 8, 1)}
 
+# --- C6: the "GPU L2 Stride Prefetch" device policy ---
+# P6: when a lane touches the last 128 B of a 4-KiB page, request the next 64 KiB (16 pages)
+# through gdev_mem_prefetch; the host daemon's prefetch handler receives the requests.
+P6 = """
+    ldxdw r6, [r1+0]          ; addr
+    mov64 r2, r6
+    and64 r2, 4095
+    jlt r2, 3968, out         ; not in the page's last 128 B
+    lddw r1, map:pfq
+    mov64 r2, r6
+    rsh64 r2, 12
+    add64 r2, 1
+    lsh64 r2, 12              ; next page
+    mov64 r3, 65536           ; 16 pages ahead
+    call 1000                 ; gdev_mem_prefetch(queue, addr, len)
+    lddw r1, mapval:pstat+0
+    mov64 r2, 1
+    atomic_add64 [r1+0], r2   ; prefetch calls (a counter the host reads back)
+out:
+    mov64 r0, 0
+    exit
+"""
+P6_MAPS = {"pfq": MapSpec(PREFETCH_QUEUE, 0, 0, 1 << 24), "pstat": MapSpec(ARRAY, 4, 8, 1)}
+
 PROGRAMS = {"P1": (P1, P1_MAPS), "P1d": (P1D, P1D_MAPS), "P2": (P2, P2_MAPS),
-            "P3": (P3, P3_MAPS), "P3f": (P3F, P3F_MAPS), "P4": (P4, P4_MAPS)}
+            "P3": (P3, P3_MAPS), "P3f": (P3F, P3F_MAPS), "P4": (P4, P4_MAPS), "P6": (P6, P6_MAPS)}
 
 
 def build(name: str, fds: dict, **kw) -> bytes:

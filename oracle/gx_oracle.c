@@ -37,7 +37,10 @@
 
 /* ---- constants from bpf.h / bpf_common.h (restated, not included) ---- */
 enum { CL_LD = 0, CL_LDX = 1, CL_ST = 2, CL_STX = 3, CL_ALU = 4, CL_JMP = 5, CL_JMP32 = 6, CL_ALU64 = 7 };
-enum { MAP_HASH = 1, MAP_ARRAY = 2, MAP_PT = 6, MAP_RINGBUF = 27 };
+enum { MAP_HASH = 1, MAP_ARRAY = 2, MAP_PT = 6, MAP_RINGBUF = 27, MAP_PFQ = 64 };
+/* gdev_mem_prefetch (§4.3.1 listing "Request prefetch, triggers handler in host
+ * driver"), this build's helper id (reading F-1) */
+enum { FN_MEM_PREFETCH = 1000 };
 enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_NOMEM = 12, E_EXIST = 17, E_INVAL = 22 };
 #define STACK_SIZE 512
 #define POISON 0xDEADBEEFDEADBEEFull
@@ -75,6 +78,9 @@ typedef struct {
     /* RINGBUF: Linux-style records, header {u32 len, u32 pg_off} + payload padded to 8 */
     uint8_t *rb;
     uint64_t rb_used;
+    /* PREFETCH QUEUE (F-2): requests {u64 first_page, u32 npages, u32 0} in call order */
+    uint64_t *pfq;          /* 2 words per request */
+    uint64_t pfq_n;
 } map_t;
 
 typedef struct {
@@ -126,6 +132,7 @@ ORA_EXPORT ora_env *ora_new(void) {
 
 static void map_free(map_t *m) {
     free(m->data);
+    free(m->pfq);
     if (m->shards) {
         for (uint32_t s = 0; s < m->nshards; s++) free(m->shards[s]);
         free(m->shards);
@@ -204,6 +211,12 @@ ORA_EXPORT int ora_map_create(ora_env *e, uint32_t type, uint32_t key_size, uint
         if (key_size || value_size || max_entries < 4096 || (max_entries & (max_entries - 1))) return -E_INVAL;
         m->rb = calloc(max_entries, 1);
         if (!m->rb) return -E_NOMEM;
+        break;
+    case MAP_PFQ:   /* capacity in requests: a power of two in [64, 2^24] (F-2) */
+        if (key_size || value_size || max_entries < 64 || max_entries > (1u << 24) || (max_entries & (max_entries - 1)))
+            return -E_INVAL;
+        m->pfq = calloc(2 * (size_t)max_entries, sizeof(uint64_t));
+        if (!m->pfq) return -E_NOMEM;
         break;
     default:
         return -E_INVAL;
@@ -293,7 +306,7 @@ static int map_update(ora_env *e, map_t *m, const uint8_t *key, const uint8_t *v
 ORA_EXPORT int ora_map_update(ora_env *e, int fd, const void *key, const void *val, uint64_t flags) {
     if (fd < 0 || fd >= MAX_MAPS || !e->maps[fd].used) return -E_INVAL;
     map_t *m = &e->maps[fd];
-    if (m->type == MAP_RINGBUF) return -E_INVAL;
+    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return -E_INVAL;
     int r = map_update(e, m, key, val, flags, 0);
     if (r == 0 && m->type == MAP_PT) {
         uint32_t k;
@@ -315,6 +328,21 @@ static int ringbuf_output(ora_env *e, map_t *m, const uint8_t *data, uint64_t si
     memset(m->rb + m->rb_used + 8, 0, rec - 8);
     memcpy(m->rb + m->rb_used + 8, data, size);
     m->rb_used += rec;
+    return 0;
+}
+
+/* gdev_mem_prefetch(queue, addr, len) (F-1..F-3): the region is the
+ * run of 4-KiB pages [addr >> 12, (addr + len - 1) >> 12] ("finer-grained 4KB pages",
+ * 303 "prefetch hooks operate at page granularity"), at most 2 MiB (one UVM chunk).  len == 0,
+ * len > 2 MiB or addr + len past 2^64 -> -EINVAL, nothing queued; a full queue -> -EAGAIN (the
+ * request is dropped and counted); else the request {first_page, npages} is appended -> 0. */
+static int mem_prefetch(ora_env *e, map_t *m, uint64_t addr, uint64_t len) {
+    if (len == 0 || len > (2ull << 20) || addr + len < addr) return -E_INVAL;
+    const uint64_t first = addr >> 12, last = (addr + len - 1) >> 12;
+    if (m->pfq_n >= m->max_entries) { e->stats[ST_DROPS]++; return -E_AGAIN; }
+    m->pfq[2 * m->pfq_n] = first;
+    m->pfq[2 * m->pfq_n + 1] = last - first + 1;
+    m->pfq_n++;
     return 0;
 }
 
@@ -619,12 +647,12 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                 if (!is64 || src != 0) return fault(env, ev, pc, "bpf-to-bpf / kfunc calls unsupported");
                 reg_t *R1 = &vm->r[1], *R2 = &vm->r[2], *R3 = &vm->r[3], *R4 = &vm->r[4];
                 int64_t ret;
-                if (imm == 1 || imm == 2 || imm == 130) {
+                if (imm == 1 || imm == 2 || imm == 130 || imm == FN_MEM_PREFETCH) {
                     if (R1->tag != T_MAPH) return fault(env, ev, pc, "helper r1 is not a map handle");
                 }
                 if (imm == 1) {
                     map_t *m = &env->maps[R1->map];
-                    if (m->type == MAP_RINGBUF) return fault(env, ev, pc, "lookup on ringbuf");
+                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return fault(env, ev, pc, "lookup on ringbuf / prefetch queue");
                     const uint8_t *key = arg_bytes(vm, R2, m->key_size, pc);
                     if (!key) return -1;
                     uint8_t *v = map_lookup(m, key, vm->shard);
@@ -635,7 +663,7 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                     continue;
                 } else if (imm == 2) {
                     map_t *m = &env->maps[R1->map];
-                    if (m->type == MAP_RINGBUF) return fault(env, ev, pc, "update on ringbuf");
+                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return fault(env, ev, pc, "update on ringbuf / prefetch queue");
                     const uint8_t *key = arg_bytes(vm, R2, m->key_size, pc);
                     if (!key) return -1;
                     const uint8_t *val = arg_bytes(vm, R3, m->value_size, pc);
@@ -653,6 +681,11 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                     const uint8_t *data = arg_bytes(vm, R2, (uint32_t)R3->v, pc);
                     if (!data) return -1;
                     ret = ringbuf_output(env, m, data, R3->v, R4->v);
+                } else if (imm == FN_MEM_PREFETCH) {
+                    map_t *m = &env->maps[R1->map];
+                    if (m->type != MAP_PFQ) return fault(env, ev, pc, "mem_prefetch on a non-prefetch-queue map");
+                    if (!scalar(R2) || !scalar(R3)) return fault(env, ev, pc, "prefetch addr/len not scalar");
+                    ret = mem_prefetch(env, m, R2->v, R3->v);
                 } else {
                     return fault(env, ev, pc, "unknown or forbidden helper");
                 }
@@ -901,6 +934,41 @@ ORA_EXPORT int ora_ringbuf_dump(ora_env *e, int fd, void *buf, uint64_t cap, uin
 
 ORA_EXPORT uint64_t ora_ringbuf_used(ora_env *e, int fd) { return e->maps[fd].rb_used; }
 
+/* PREFETCH QUEUE canonical content (F-2): the SET of requests -- prefetching a region
+ * twice is the same as once, so implementations may merge identical requests -- sorted by
+ * (first_page, npages), 2 u64 words each; *n = distinct requests, *n_calls = appended requests. */
+static int pcmp(const void *a, const void *b) {
+    const uint64_t *x = a, *y = b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : x[1] > y[1];
+}
+ORA_EXPORT int ora_pfq_dump(ora_env *e, int fd, uint64_t *buf, uint64_t cap, uint64_t *n, uint64_t *n_calls) {
+    if (fd < 0 || fd >= MAX_MAPS || !e->maps[fd].used || e->maps[fd].type != MAP_PFQ) return -E_INVAL;
+    map_t *m = &e->maps[fd];
+    uint64_t *t = malloc((2 * m->pfq_n + 2) * sizeof *t);
+    memcpy(t, m->pfq, 2 * m->pfq_n * sizeof *t);
+    qsort(t, m->pfq_n, 2 * sizeof *t, pcmp);
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < m->pfq_n; i++) {
+        if (k && t[2 * (k - 1)] == t[2 * i] && t[2 * (k - 1) + 1] == t[2 * i + 1]) continue;
+        t[2 * k] = t[2 * i];
+        t[2 * k + 1] = t[2 * i + 1];
+        k++;
+    }
+    if (k > cap) { free(t); return -E_2BIG; }
+    memcpy(buf, t, 2 * k * sizeof *t);
+    free(t);
+    *n = k;
+    *n_calls = m->pfq_n;
+    return 0;
+}
+/* drain: the host handler consumed the queue (gx_prefetch_drain / the runtime daemon) */
+ORA_EXPORT int ora_pfq_reset(ora_env *e, int fd) {
+    if (fd < 0 || fd >= MAX_MAPS || !e->maps[fd].used || e->maps[fd].type != MAP_PFQ) return -E_INVAL;
+    e->maps[fd].pfq_n = 0;
+    return 0;
+}
+
 /* ------------------------------------------------------------------ shards (O10 --shards G, S3) */
 
 /* Deep copy of an environment (maps, programs, attach table, settings); stats reset. */
@@ -931,6 +999,9 @@ ORA_EXPORT ora_env *ora_clone(ora_env *src) {
         } else if (s->type == MAP_RINGBUF) {
             d->rb = calloc(s->max_entries, 1);
             memcpy(d->rb, s->rb, s->rb_used);
+        } else if (s->type == MAP_PFQ) {
+            d->pfq = calloc(2 * (size_t)s->max_entries, sizeof(uint64_t));
+            memcpy(d->pfq, s->pfq, 2 * s->pfq_n * sizeof(uint64_t));
         }
     }
     for (int i = 0; i < MAX_PROGS; i++) {
@@ -1010,6 +1081,17 @@ ORA_EXPORT int ora_merge(ora_env *init, ora_env **locals, int G) {
                 for (uint64_t o = start; o < l->rb_used; o += (8 + load_le(l->rb + o, 4) + 7) & ~7ull) {
                     uint32_t len = (uint32_t)load_le(l->rb + o, 4);
                     ringbuf_output(init, m, l->rb + o + 8, len, 0);
+                }
+            }
+        } else if (m->type == MAP_PFQ) {   /* union of the shards' requests (F-2: a set) */
+            uint64_t start = m->pfq_n;
+            for (int g = 0; g < G; g++) {
+                map_t *l = &locals[g]->maps[i];
+                for (uint64_t r = start; r < l->pfq_n; r++) {
+                    if (m->pfq_n >= m->max_entries) { init->stats[ST_DROPS]++; rc = -E_AGAIN; continue; }
+                    m->pfq[2 * m->pfq_n] = l->pfq[2 * r];
+                    m->pfq[2 * m->pfq_n + 1] = l->pfq[2 * r + 1];
+                    m->pfq_n++;
                 }
             }
         }

@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 SRC_PATH = os.path.join(_HERE, "gx_oracle.c")
 
-HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF = 1, 2, 6, 27
+HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF, PREFETCH_QUEUE = 1, 2, 6, 27, 64
+FN_MEM_PREFETCH = 1000   # gdev_mem_prefetch (F-1)
 STATS = ("events_run", "events_skipped", "ringbuf_drops", "hash_full", "helper_errors", "insns")
 
 
@@ -51,6 +52,8 @@ def lib():
         L.ora_ringbuf_dump.argtypes = [vp, i32, vp, u64, p64, p64]
         L.ora_ringbuf_used.argtypes = [vp, i32]
         L.ora_ringbuf_used.restype = u64
+        L.ora_pfq_dump.argtypes = [vp, i32, p64, u64, p64, p64]
+        L.ora_pfq_reset.argtypes = [vp, i32]
         L.ora_clone.argtypes = [vp]
         L.ora_clone.restype = vp
         L.ora_merge.argtypes = [vp, C.POINTER(vp), i32]
@@ -160,6 +163,21 @@ class Oracle:
             out.append(raw[o + 4:o + 4 + ln])
             o += 4 + ln
         return out
+
+    def prefetch_requests(self, fd) -> list[tuple[int, int]]:
+        """The prefetch queue's canonical content (F-2): the sorted SET of
+        (first_page, npages) requests; `self.last_pfq_calls` = requests appended."""
+        cap = int(self.specs[fd][3])
+        buf = (C.c_uint64 * (2 * cap + 2))()
+        n, nc = C.c_uint64(), C.c_uint64()
+        rc = self.L.ora_pfq_dump(self.h, fd, buf, cap, C.byref(n), C.byref(nc))
+        if rc:
+            raise OSError(-rc, "ora_pfq_dump")
+        self.last_pfq_calls = nc.value
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
+
+    def prefetch_reset(self, fd):
+        self.L.ora_pfq_reset(self.h, fd)
 
     def clone(self) -> "Oracle":
         c = Oracle(self.L.ora_clone(self.h))
