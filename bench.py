@@ -316,6 +316,7 @@ def main():
         print(json.dumps(line), flush=True)
         if args.extra:
             extra_lines(rt, args)
+            f2_lines()
     if world > 1:
         dist.destroy_process_group()
 
@@ -442,6 +443,46 @@ def extra_lines(rt0, args):
                           "divergent_frac": st["divergent_steps"] / max(1, st["warp_steps"])}), file=sys.stderr, flush=True)
         del ev
         rt.close()
+
+
+def f2_lines():
+    """C6 (stride-prefetch policy, 2^28 C3-trace events) and C2 (2^30)
+    with and without the runtime daemon; the daemon publishes prefetch requests / watched-map
+    snapshots at every kernel-completion boundary on the batch's stream."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+    for config, n, watch in (("C6", 1 << 28, ["pstat"]), ("C2", 1 << 30, ["hist", "lane_pt"])):
+        ev = gen_gpu.generate_device(config, configs.SEEDS[config], n)
+        for daemon in (False, True):
+            rt = gx.Runtime(0, engine=gx.GX_ENGINE_JIT)
+            s = configs.setup(rt, config)
+            if daemon:
+                for name in watch:
+                    gx.gx_daemon_watch(rt.rt, s.fds[(0, name)])
+                rt.daemon_start(None)
+            times, nreq = [], 0
+            for k in range(8):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                rt.run(ev, s.prog_arg)
+                b.record()
+                torch.cuda.synchronize()
+                if k >= 3:
+                    times.append(a.elapsed_time(b))
+                if not daemon and config == "C6":   # without a daemon the host drains (outside timing)
+                    nreq = len(gx.gx_prefetch_drain(rt.rt, s.fds[(0, "pfq")], 1 << 24))
+            ms = float(np.mean(times))
+            line = {"f2": config, "events": n, "daemon": daemon, "ms": ms, "events_per_s": n / ms * 1e3,
+                    "drops": rt.stats()["ringbuf_drops"]}
+            if daemon:
+                rt.daemon_stop()
+                line["daemon_stats"] = gx.gx_daemon_get_stats(rt.rt)
+            elif config == "C6":
+                line["requests_per_batch"] = nreq
+            print(json.dumps(line), file=sys.stderr, flush=True)
+            rt.close()
+        del ev
 
 
 if __name__ == "__main__":

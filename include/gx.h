@@ -45,7 +45,19 @@ extern "C" {
 typedef struct gx_rt gx_rt;
 
 /* map types: bpf.h:925-965 numbering; PERTHREAD_ARRAY takes PERCPU_ARRAY's slot */
-enum { GX_MAP_HASH = 1, GX_MAP_ARRAY = 2, GX_MAP_PERTHREAD_ARRAY = 6, GX_MAP_RINGBUF = 27 };
+enum { GX_MAP_HASH = 1, GX_MAP_ARRAY = 2, GX_MAP_PERTHREAD_ARRAY = 6, GX_MAP_RINGBUF = 27,
+       /* device->host prefetch request queue (F-2): key_size = value_size
+        * = 0, max_entries = capacity in requests (a power of two in [64, 2^24]) */
+       GX_MAP_PREFETCH_QUEUE = 64 };
+/* Device helper ids beyond Linux's: gdev_mem_prefetch (§4.3.1 listing
+ * "Request prefetch, triggers handler in host driver"), called as
+ *     r0 = gdev_mem_prefetch(r1 = prefetch-queue map, r2 = addr, r3 = len)
+ * The region is the run of 4-KiB pages [addr >> 12, (addr + len - 1) >> 12]; it queues the
+ * request {first_page, npages} and returns 0, -EAGAIN (-11) if the queue is full (dropped,
+ * counted in ringbuf_drops) or -EINVAL (-22) if len == 0, len > 2 MiB or addr + len wraps.
+ * Prefetching is idempotent: the queue's content is a SET, and the device merges identical
+ * requests of one warp group (PAPER.md:286 warp-level aggregation). */
+enum { GX_FN_MEM_PREFETCH = 1000 };
 /* hook kinds (event hook word bits 0-7): PAPER.md:225-230 (gdev_mem_ops.access), 260-262
  * (gdev_sched_ops.enter), 303 (fault-style records) */
 enum { GX_HOOK_MEM_ACCESS = 0, GX_HOOK_BLOCK_ENTER = 1, GX_HOOK_FAULT = 2 };
@@ -128,6 +140,49 @@ int  gx_read_map(gx_rt *rt, int map_fd, void *keys, void *vals, uint64_t cap, ui
  * bpf.h:6064-6066 layout) into buf and resets the buffer.  *n_bytes = bytes copied.  -E2BIG
  * (nothing copied) if cap < committed bytes.  Synchronous. */
 int  gx_ringbuf_drain(gx_rt *rt, int map_fd, void *buf, uint64_t cap, uint64_t *n_bytes);
+/* Copies the queued prefetch requests as u64 pairs {first_page, npages} (queue order, identical
+ * requests of one warp group merged) into reqs and empties the queue.  cap = capacity in
+ * requests; *n_req = requests copied; -E2BIG (nothing copied) if cap is too small.  Synchronous.
+ * (With a daemon running, the daemon drains the queues instead.) */
+int  gx_prefetch_drain(gx_rt *rt, int map_fd, uint64_t *reqs, uint64_t cap, uint64_t *n_req);
+
+/* ---------------------------------------------------------------- runtime daemon (§8f f2)
+ * "A runtime daemon asynchronously flushes GPU-local shards to host-visible canonical map
+ * instances, providing coherent snapshots to host-side policies without synchronization
+ * overhead" (§5.3); "snapshot-based aggregation at GPU kernel completion
+ * boundaries"; device prefetch requests "trigger host-side prefetch
+ * handlers".
+ * While a daemon runs, every gx_run_batch / gx_run_batch_ex appends to ITS OWN stream, right
+ * after the batch's kernel (= at that kernel-completion boundary): a publish kernel that writes
+ * each prefetch queue's requests and each watched map's canonical snapshot into pinned host
+ * memory and empties the queues, then an event.  The daemon thread waits for the event and
+ * hands the requests to the handler and the snapshots to gx_snapshot_read -- the caller's
+ * stream never synchronises with the host.  Four publish slots: a batch that finds none free
+ * waits for the daemon (backpressure, counted).  Handlers run on the daemon thread. */
+typedef void (*gx_prefetch_handler)(void *user, int map_fd, const uint64_t *reqs, uint64_t n_req);
+typedef struct {
+    uint64_t batches;          /* publish points processed */
+    uint64_t requests;         /* prefetch requests handed to the handler */
+    uint64_t snapshots;        /* map snapshots published */
+    uint64_t backpressure;     /* batches that waited for a free publish slot */
+    uint64_t managed_prefetches; /* default handler: cudaMemPrefetchAsync calls issued */
+} gx_daemon_stats;
+/* Starts the daemon.  handler == NULL installs the default handler: requests whose pages lie in
+ * CUDA managed memory are prefetched to the device with cudaMemPrefetchAsync, others are only
+ * counted.  -EBUSY if one runs. */
+int  gx_daemon_start(gx_rt *rt, gx_prefetch_handler handler, void *user);
+/* Drains what is published, then stops.  Safe when none runs. */
+int  gx_daemon_stop(gx_rt *rt);
+/* Adds an ARRAY or PERTHREAD_ARRAY map to the snapshot set (-EINVAL for other types). */
+int  gx_daemon_watch(gx_rt *rt, int map_fd);
+/* Latest published canonical snapshot of a watched map (max_entries * value_size bytes;
+ * per-thread maps folded) and its version (= publish points so far; 0: none yet).  Never
+ * touches the device.  -ENOENT if not watched, -E2BIG if cap is too small. */
+int  gx_snapshot_read(gx_rt *rt, int map_fd, void *buf, uint64_t cap, uint64_t *version);
+int  gx_daemon_get_stats(gx_rt *rt, gx_daemon_stats *out);
+/* Registers the CUDA managed range the default handler prefetches into (requests outside it are
+ * only counted); ptr == NULL clears it. */
+int  gx_daemon_prefetch_range(gx_rt *rt, void *managed_ptr, uint64_t bytes);
 
 /* ---------------------------------------------------------------- programs */
 /* Copies n_slots 8-byte struct bpf_insn slots (bpf.h:72-77); structural decode and map-fd

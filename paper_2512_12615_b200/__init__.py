@@ -21,7 +21,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgx.so")
 
-GX_MAP_HASH, GX_MAP_ARRAY, GX_MAP_PERTHREAD_ARRAY, GX_MAP_RINGBUF = 1, 2, 6, 27
+GX_MAP_HASH, GX_MAP_ARRAY, GX_MAP_PERTHREAD_ARRAY, GX_MAP_RINGBUF, GX_MAP_PREFETCH_QUEUE = 1, 2, 6, 27, 64
+GX_FN_MEM_PREFETCH = 1000
 RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", "UNINIT_READ", "OOB_ACCESS",
          "NULL_DEREF", "MISALIGNED", "PTR_LEAK", "SHIFT_RANGE", "BAD_HELPER", "FORBIDDEN_SYNC", "UNBOUNDED_LOOP",
          "COMPLEXITY", "BUDGET", "UNIFORM_BRANCH", "UNIFORM_LOOP_BOUND", "UNIFORM_MAP_KEY", "NON_UNIFORM_ATOMIC",
@@ -29,7 +30,8 @@ RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", 
 EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_map", "gx_read_map",
            "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_jit_offline", "gx_attach", "gx_run_batch", "gx_run_batch_ex", "gx_run_batch_host",
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
-           "gx_hash_export", "gx_hash_apply")
+           "gx_hash_export", "gx_hash_apply", "gx_prefetch_drain", "gx_daemon_start", "gx_daemon_stop", "gx_daemon_watch",
+           "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range")
 
 
 class gx_map_spec(C.Structure):
@@ -63,6 +65,16 @@ class gx_batch_stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class gx_daemon_stats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("batches", "requests", "snapshots", "backpressure", "managed_prefetches")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# void handler(void *user, int map_fd, const uint64_t *reqs, uint64_t n_req)
+PREFETCH_HANDLER = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.c_uint64)
+
 _lib = None
 
 
@@ -84,6 +96,13 @@ def lib():
         "gx_update_map": (i32, [vp, i32, vp, vp, u64, u64]),
         "gx_read_map": (i32, [vp, i32, vp, vp, u64, p64]),
         "gx_ringbuf_drain": (i32, [vp, i32, vp, u64, p64]),
+        "gx_prefetch_drain": (i32, [vp, i32, p64, u64, p64]),
+        "gx_daemon_start": (i32, [vp, PREFETCH_HANDLER, vp]),
+        "gx_daemon_stop": (i32, [vp]),
+        "gx_daemon_watch": (i32, [vp, i32]),
+        "gx_snapshot_read": (i32, [vp, i32, vp, u64, p64]),
+        "gx_daemon_get_stats": (i32, [vp, C.POINTER(gx_daemon_stats)]),
+        "gx_daemon_prefetch_range": (i32, [vp, vp, u64]),
         "gx_load_prog": (i32, [vp, u32, vp, u32, C.POINTER(i32)]),
         "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
         "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
@@ -277,6 +296,53 @@ def gx_read_map(rt, fd, spec):
     return vals.raw
 
 
+def gx_prefetch_drain(rt, fd, cap) -> list[tuple[int, int]]:
+    """Drains a prefetch queue: [(first_page, npages)] in queue order."""
+    buf = (C.c_uint64 * (2 * cap + 2))()
+    n = C.c_uint64()
+    _check(lib().gx_prefetch_drain(rt, fd, buf, cap, C.byref(n)), "gx_prefetch_drain", rt)
+    return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
+
+
+def gx_daemon_start(rt, handler=None):
+    """handler(map_fd, [(first_page, npages)]) in Python, or None for the default handler.
+    Returns the ctypes callback object (keep it alive while the daemon runs)."""
+    if handler is None:
+        cb = C.cast(None, PREFETCH_HANDLER)
+    else:
+        def _tramp(user, fd, reqs, n):
+            handler(int(fd), [(int(reqs[2 * i]), int(reqs[2 * i + 1]) & 0xFFFFFFFF) for i in range(n)])
+        cb = PREFETCH_HANDLER(_tramp)
+    _check(lib().gx_daemon_start(rt, cb, None), "gx_daemon_start", rt)
+    return cb
+
+
+def gx_daemon_stop(rt):
+    _check(lib().gx_daemon_stop(rt), "gx_daemon_stop", rt)
+
+
+def gx_daemon_watch(rt, fd):
+    _check(lib().gx_daemon_watch(rt, fd), "gx_daemon_watch", rt)
+
+
+def gx_snapshot_read(rt, fd, nbytes):
+    """(bytes or None, version) of the latest published snapshot of a watched map."""
+    buf = C.create_string_buffer(max(nbytes, 1))
+    ver = C.c_uint64()
+    _check(lib().gx_snapshot_read(rt, fd, buf, nbytes, C.byref(ver)), "gx_snapshot_read", rt)
+    return (buf.raw[:nbytes] if ver.value else None), ver.value
+
+
+def gx_daemon_get_stats(rt) -> dict:
+    st = gx_daemon_stats()
+    _check(lib().gx_daemon_get_stats(rt, C.byref(st)), "gx_daemon_get_stats", rt)
+    return st.as_dict()
+
+
+def gx_daemon_prefetch_range(rt, ptr, nbytes):
+    _check(lib().gx_daemon_prefetch_range(rt, ptr, nbytes), "gx_daemon_prefetch_range", rt)
+
+
 def gx_ringbuf_drain(rt, fd) -> list[bytes]:
     """Drains a ring buffer; returns the record payloads in buffer order."""
     n = C.c_uint64()
@@ -395,6 +461,18 @@ class Runtime:
 
     def hash_items(self, fd) -> dict:
         return {k: np.frombuffer(v, dtype=np.uint64).copy() for k, v in gx_read_map(self.rt, fd, self.specs[fd])}
+
+    def prefetch_requests(self, fd) -> list[tuple[int, int]]:
+        """Drains a prefetch queue; returns its canonical content, the sorted SET of requests
+        (F-2)."""
+        return sorted(set(gx_prefetch_drain(self.rt, fd, self.specs[fd][3])))
+
+    def daemon_start(self, handler=None):
+        self._daemon_cb = gx_daemon_start(self.rt, handler)
+
+    def daemon_stop(self):
+        gx_daemon_stop(self.rt)
+        self._daemon_cb = None
 
     def ringbuf_records(self, fd) -> list[bytes]:
         """Drains; returns the multiset as a sorted list of payloads."""

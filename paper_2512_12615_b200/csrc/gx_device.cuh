@@ -171,6 +171,48 @@ __device__ __forceinline__ int64_t hash_update_coop(const GxMapDesc &m, uint64_t
     return me ? hash_update(m, key, val, flags, full) : 0;
 }
 
+/* ---- PREFETCH QUEUE: gdev_mem_prefetch(queue, addr, len) (F-1..F-3).
+ * Called by every lane of `mask`; `me` marks lanes whose event executes the helper.  A request is
+ * the page run {addr >> 12, npages}; identical requests of the group are merged (prefetching is
+ * idempotent, F-2) -- one queue slot per distinct request, one atomicAdd per group.  Slots at or
+ * beyond the capacity are dropped (-EAGAIN, counted per requesting lane). */
+template <typename Counter>
+__device__ __forceinline__ int64_t pfq_request_coop(const GxMapDesc &md, uint64_t addr, uint64_t len, bool me,
+                                                    unsigned mask, Counter &drops) {
+    const bool valid = me && len != 0 && len <= (2ull << 20) && addr + len >= addr;
+    uint64_t first = 0, np = 0;
+    if (valid) {
+        first = addr >> 12;
+        np = ((addr + len - 1) >> 12) - first + 1;
+    }
+    const unsigned vm = __ballot_sync(mask, valid);
+    if (!vm) return me ? -(int64_t)E_INVAL : 0;
+    const uint64_t key = valid ? (first << 10) | (np - 1) : ~0ull; /* first < 2^52, np <= 513 */
+    const unsigned peers = __match_any_sync(mask, key);
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned myhead = __ffs(peers) - 1;
+    const bool head = valid && myhead == lane;
+    const unsigned heads = __ballot_sync(mask, head);
+    const unsigned leader = __ffs(heads) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long *>(md.aux), (unsigned long long)__popc(heads));
+    base = __shfl_sync(mask, base, leader);
+    const uint64_t slot = base + __popc(heads & ((1u << myhead) - 1));
+    const bool ok = slot <= (uint64_t)md.cap_mask;
+    if (head && ok) {
+        uint64_t *d = reinterpret_cast<uint64_t *>(md.data + 16 * slot);
+        d[0] = first;
+        d[1] = np;
+    }
+    if (!me) return 0;
+    if (!valid) return -(int64_t)E_INVAL;
+    if (!ok) {
+        drops++;
+        return -(int64_t)E_AGAIN;
+    }
+    return 0;
+}
+
 /* ---- per-thread ARRAY (S4): one private copy per executor thread ("shard").  Value pointers a
  * program holds are LOGICAL addresses data + key*vs + off; the physical word is
  *     pt_word_index(K, W, k, w, shard) = ((q*K*W) + ((k - r) mod K)*W + w) * 32 + l

@@ -648,6 +648,15 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     break;
                 }
 
+                case GX_CALL_MEM_PREFETCH: {
+                    const int64_t rc = gxd::pfq_request_coop(M[in.aux], R[2 * 32 + lane], R[3 * 32 + lane], me, GX_FULL, c_drop);
+                    if (me) {
+                        if (rc) c_herr++;
+                        R[lane] = (uint64_t)rc;
+                    }
+                    break;
+                }
+
                 /* ---------------- jumps */
                 case GX_JA:
                     npc = in.aux;

@@ -15,6 +15,8 @@
 #define GX_MAX_STAGED_INSNS 2048  /* total pre-decoded slots staged in shared memory per launch */
 #define GX_HASH_EMPTY 0xFFFFFFFFFFFFFFFFull
 #define GX_NREGS 11
+#define GX_FN_MEM_PREFETCH 1000   /* gdev_mem_prefetch helper id (F-1) */
+#define GX_MAP_TYPE_PFQ 64        /* prefetch queue map type (F-2) */
 
 /* ---- pre-decoded instruction (16 B), produced by the verifier for the executor ----
  * Every field is warp-uniform on the fast path, so decode costs one broadcast LDS.128. */
@@ -73,17 +75,19 @@ enum GxOp : uint8_t {
     GX_CALL_LOOKUP_ARRAY, GX_CALL_LOOKUP_PT, GX_CALL_LOOKUP_HASH,
     GX_CALL_UPDATE_ARRAY, GX_CALL_UPDATE_PT, GX_CALL_UPDATE_HASH,
     GX_CALL_RINGBUF_OUTPUT,
+    GX_CALL_MEM_PREFETCH,         /* gdev_mem_prefetch(queue = aux, addr = r2, len = r3) (f2) */
     GX_OP_COUNT
 };
 
 /* ---- device-side map descriptor ---- */
 struct GxMapDesc {
     uint64_t data;         /* ARRAY: values; PT: shards [word][shard]; HASH: slots (cap+1) x 16 B;
-                              RINGBUF: bytes */
-    uint64_t aux;          /* HASH: u64 counters {count}; RINGBUF: u64 {prod, used} */
+                              RINGBUF: bytes; PREFETCH QUEUE: 16-B requests */
+    uint64_t aux;          /* HASH: u64 counters {count}; RINGBUF: u64 {prod, used};
+                              PREFETCH QUEUE: u64 {reserved} */
     uint32_t type, key_size, value_size, max_entries;
     uint32_t nshards;      /* PT */
-    uint32_t cap_mask;     /* HASH: capacity-1; RINGBUF: capacity-1 */
+    uint32_t cap_mask;     /* HASH: capacity-1; RINGBUF: capacity-1; PREFETCH QUEUE: capacity-1 */
     uint32_t priv_off;     /* byte offset of the privatized copy in shared memory, or ~0u */
     uint32_t coherent;     /* 1: written during this launch -> loads bypass L1 */
 };
@@ -107,6 +111,16 @@ struct GxLaunch {
     uint32_t priv_maps[8];
     uint32_t pad;
     uint64_t stats;                    /* device u64[8] counters (gx_batch_stats order) */
+};
+
+/* one item of a runtime-daemon publish point (gx_maps.cu publish_kernel) */
+struct GxPublishItem {
+    uint64_t data, aux;    /* device storage / counters of the map */
+    uint64_t host_off;     /* byte offset in the host slot */
+    uint64_t cap;          /* prefetch queue capacity (requests) */
+    uint32_t kind;         /* 0 prefetch queue, 1 ARRAY, 2 PERTHREAD */
+    uint32_t K, W;         /* entries, u64 words per value */
+    uint32_t nshards;
 };
 
 enum { GXS_RUN = 0, GXS_SKIP, GXS_DIVERGENT, GXS_HERR, GXS_RB_BYTES, GXS_RB_DROPS, GXS_HFULL, GXS_STEPS };

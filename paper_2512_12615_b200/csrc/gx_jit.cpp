@@ -190,7 +190,7 @@ struct Gen {
     const GxInsn *im_ = nullptr;
     static bool simple(const GxInsn &g) {
         if (g.op == GX_JA || g.op == GX_EXIT || g.op == GX_OP_NOP || is_jcc(g.op)) return false;
-        if (g.op >= GX_CALL_LOOKUP_ARRAY) return false;
+        if (g.op >= GX_CALL_LOOKUP_ARRAY) return false; /* helpers (incl. GX_CALL_MEM_PREFETCH) */
         if (g.op == GX_ATOM_STACK || g.op == GX_ATOM_MAP || g.op == GX_ATOM_PT) return false;
         return true;
     }
@@ -510,6 +510,10 @@ struct Gen {
             st("  if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
             break;
         }
+        case GX_CALL_MEM_PREFETCH:
+            st("{ const int64_t rc_ = gxd::pfq_request_coop(" + md(g.aux) + ", r2, r3, true, " + M() +
+               ", c_drop); r0 = (uint64_t)rc_; if (rc_) c_herr++; }");
+            break;
         case GX_CALL_RINGBUF_OUTPUT: {
             const uint32_t size = (uint32_t)g.imm, flags = (uint32_t)(g.imm >> 32);
             if (flags > 2) {

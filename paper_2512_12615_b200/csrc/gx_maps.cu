@@ -46,6 +46,39 @@ __global__ void pt_store_canonical_kernel(uint64_t *data, uint32_t nshards, uint
     }
 }
 
+/* Runtime-daemon publish point (include/gx.h): runs on the batch's stream
+ * right after its kernel and writes into a pinned, device-mapped host slot -- block b handles
+ * item b: a prefetch queue (u64 count, then count x 16-B requests; the queue is emptied) or a
+ * watched map's canonical snapshot (ARRAY copy, PERTHREAD SUM fold). */
+__global__ void publish_kernel(const GxPublishItem *__restrict__ items, uint8_t *__restrict__ host) {
+    const GxPublishItem it = items[blockIdx.x];
+    uint64_t *out = reinterpret_cast<uint64_t *>(host + it.host_off);
+    if (it.kind == 0) { /* prefetch queue */
+        unsigned long long *ctr = reinterpret_cast<unsigned long long *>(it.aux);
+        const uint64_t n = min((uint64_t)*ctr, it.cap);
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
+        for (uint64_t i = threadIdx.x; i < 2 * n; i += blockDim.x) out[1 + i] = src[i];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            out[0] = n;
+            *ctr = 0;
+        }
+    } else if (it.kind == 1) { /* ARRAY */
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
+        for (uint64_t i = threadIdx.x; i < (uint64_t)it.K * it.W; i += blockDim.x) out[i] = src[i];
+    } else { /* PERTHREAD: canonical value = SUM over shards (S4) */
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
+        const uint32_t lane = threadIdx.x & 31;
+        for (uint64_t j = threadIdx.x >> 5; j < (uint64_t)it.K * it.W; j += blockDim.x >> 5) {
+            const uint32_t k = (uint32_t)(j / it.W), w = (uint32_t)(j % it.W);
+            uint64_t acc = 0;
+            for (uint32_t sh = lane; sh < it.nshards; sh += 32) acc += src[gxd::pt_word_index(it.K, it.W, k, w, sh)];
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(GX_FULL, acc, o);
+            if (lane == 0) out[j] = acc;
+        }
+    }
+}
+
 __global__ void hash_init_kernel(uint64_t *slots, uint64_t cap) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
          i += gridDim.x * (uint64_t)blockDim.x) {
@@ -156,6 +189,12 @@ int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32
     pt_store_canonical_kernel<<<grid_for((uint64_t)K * W * nshards, 256), 256, 0, s>>>(data, nshards, K, W, vals);
     return (int)cudaGetLastError();
 }
+int gx_k_publish(const GxPublishItem *items, uint32_t n_items, uint8_t *host_slot, cudaStream_t s) {
+    if (!n_items) return 0;
+    publish_kernel<<<n_items, 256, 0, s>>>(items, host_slot);
+    return (int)cudaGetLastError();
+}
+
 int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s) {
     hash_init_kernel<<<grid_for(cap + 1, 256), 256, 0, s>>>(slots, cap);
     return (int)cudaGetLastError();

@@ -13,7 +13,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <deque>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <memory>
 #include <string>
 #include <vector>
@@ -37,6 +41,7 @@ int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32
 int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, const uint64_t *vals,
                             cudaStream_t s);
 int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s);
+int gx_k_publish(const GxPublishItem *items, uint32_t n_items, uint8_t *host_slot, cudaStream_t s);
 int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t flags,
                           int64_t *rc, unsigned long long *full, cudaStream_t s);
 int gx_k_sub(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cudaStream_t s);
@@ -139,6 +144,34 @@ Drv &drv() {
 
 }  // namespace
 
+/* runtime daemon (include/gx.h) */
+struct DaemonSlot {
+    uint8_t *host = nullptr;   /* pinned, device-mapped */
+    cudaEvent_t ev = nullptr;
+    bool busy = false;
+};
+struct Daemon {
+    static constexpr int kSlots = 4;
+    bool running = false, stopping = false;
+    gx_prefetch_handler fn = nullptr;
+    void *user = nullptr;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv_work, cv_free;
+    std::deque<int> pending;
+    DaemonSlot slots[kSlots];
+    uint64_t slot_bytes = 0;
+    std::vector<int> watched;              /* map fds, in watch order */
+    std::vector<GxPublishItem> items;      /* frozen layout at start */
+    std::vector<int> item_fd;
+    GxPublishItem *d_items = nullptr;
+    std::map<int, std::vector<uint8_t>> snap; /* latest published canonical snapshots */
+    uint64_t version = 0;
+    gx_daemon_stats st{};
+    uint64_t managed_ptr = 0, managed_bytes = 0; /* default handler's prefetchable range */
+    cudaStream_t s_prefetch = nullptr;
+};
+
 struct gx_rt {
     int dev = 0;
     int nsm = 0;
@@ -159,6 +192,7 @@ struct gx_rt {
     uint64_t *d_rchunk[2] = {nullptr, nullptr};
     cudaEvent_t ev_copied[2], ev_done[2];
     bool pipe_init = false;
+    Daemon dmn;
 };
 
 namespace {
@@ -370,6 +404,105 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
     return 0;
 }
 
+/* a publish point on `stream` after the batch's kernel: take a free slot (wait for the daemon if
+ * none: backpressure), write the prefetch queues and watched snapshots into it, record its event */
+int daemon_publish(gx_rt *rt, cudaStream_t stream) {
+    Daemon &D = rt->dmn;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        return set_err(rt, -EBUSY, "the runtime daemon cannot follow batches captured into a CUDA graph");
+    int slot = -1;
+    {
+        std::unique_lock<std::mutex> lk(D.mu);
+        for (;;) {
+            for (int k = 0; k < Daemon::kSlots; k++)
+                if (!D.slots[k].busy) {
+                    slot = k;
+                    break;
+                }
+            if (slot >= 0) break;
+            D.st.backpressure++;
+            D.cv_free.wait(lk);
+        }
+        D.slots[slot].busy = true;
+    }
+    int e = gx_k_publish(D.d_items, (uint32_t)D.items.size(), D.slots[slot].host, stream);
+    if (e) return cuda_err(rt, (cudaError_t)e, "daemon publish");
+    CK(cudaEventRecord(D.slots[slot].ev, stream), "daemon event");
+    {
+        std::lock_guard<std::mutex> lk(D.mu);
+        D.pending.push_back(slot);
+    }
+    D.cv_work.notify_one();
+    return 0;
+}
+
+/* default prefetch handler: requests inside the registered managed range are prefetched to the
+ * device (cudaMemPrefetchAsync, "host-side callbacks extend prefetching"); all are
+ * counted */
+void default_prefetch(gx_rt *rt, const uint64_t *reqs, uint64_t n) {
+    Daemon &D = rt->dmn;
+    if (!D.managed_bytes) return;
+    const uint64_t lo = D.managed_ptr, hi = D.managed_ptr + D.managed_bytes;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t a = reqs[2 * i] << 12, b = a + ((reqs[2 * i + 1] & 0xFFFFFFFFull) << 12);
+        a = std::max(a, lo);
+        b = std::min(b, hi);
+        if (a >= b) continue;
+#if CUDART_VERSION >= 13000
+        cudaMemLocation loc{cudaMemLocationTypeDevice, rt->dev};
+        if (cudaMemPrefetchAsync((void *)a, b - a, loc, 0, D.s_prefetch) == cudaSuccess) D.st.managed_prefetches++;
+#else
+        if (cudaMemPrefetchAsync((void *)a, b - a, rt->dev, D.s_prefetch) == cudaSuccess) D.st.managed_prefetches++;
+#endif
+    }
+}
+
+void daemon_main(gx_rt *rt) {
+    Daemon &D = rt->dmn;
+    cudaSetDevice(rt->dev);
+    for (;;) {
+        int slot;
+        {
+            std::unique_lock<std::mutex> lk(D.mu);
+            D.cv_work.wait(lk, [&] { return !D.pending.empty() || D.stopping; });
+            if (D.pending.empty()) return; /* stopping and drained */
+            slot = D.pending.front();
+            D.pending.pop_front();
+        }
+        cudaEventSynchronize(D.slots[slot].ev);
+        const uint8_t *h = D.slots[slot].host;
+        uint64_t nreq = 0;
+        for (size_t i = 0; i < D.items.size(); i++) {
+            const GxPublishItem &it = D.items[i];
+            const uint64_t *w = reinterpret_cast<const uint64_t *>(h + it.host_off);
+            if (it.kind == 0) {
+                const uint64_t n = w[0];
+                nreq += n;
+                if (n) {
+                    if (D.fn) D.fn(D.user, D.item_fd[i], w + 1, n);
+                    else default_prefetch(rt, w + 1, n);
+                }
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(D.mu);
+            D.version++;
+            for (size_t i = 0; i < D.items.size(); i++) {
+                const GxPublishItem &it = D.items[i];
+                if (it.kind == 0) continue;
+                const uint8_t *src = h + it.host_off;
+                D.snap[D.item_fd[i]].assign(src, src + 8ull * it.K * it.W);
+                D.st.snapshots++;
+            }
+            D.st.batches++;
+            D.st.requests += nreq;
+            D.slots[slot].busy = false;
+        }
+        D.cv_free.notify_all();
+    }
+}
+
 int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream,
                uint32_t flags = 0) {
     if (rt->engine == GX_ENGINE_JIT) {
@@ -429,6 +562,7 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         rt->last_smem = cfg.smem;
     }
     rt->n_launches++;
+    if (rt->dmn.running) return daemon_publish(rt, stream);
     return 0;
 }
 
@@ -469,6 +603,7 @@ int gx_open(int cuda_device, gx_rt **out) {
 void gx_close(gx_rt *rt) {
     if (!rt) return;
     cudaSetDevice(rt->dev);
+    gx_daemon_stop(rt);
     cudaDeviceSynchronize();
     for (auto &m : rt->maps) {
         cudaFree(m.data);
@@ -539,6 +674,13 @@ int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
         m.cap = s.max_entries;
         m.data_bytes = s.max_entries;
         break;
+    case GX_MAP_PREFETCH_QUEUE:
+        if (s.key_size || s.value_size || s.max_entries < 64 || s.max_entries > (1u << 24) ||
+            (s.max_entries & (s.max_entries - 1)))
+            return set_err(rt, -EINVAL, "bad PREFETCH_QUEUE spec (capacity in requests: power of two in [64, 2^24])");
+        m.cap = s.max_entries;
+        m.data_bytes = 16ull * s.max_entries;
+        break;
     default:
         return set_err(rt, -EINVAL, "unknown map type %u", s.type);
     }
@@ -568,7 +710,8 @@ int gx_update_map(gx_rt *rt, int fd, const void *keys, const void *vals, uint64_
     int rc0 = sync(rt);
     if (rc0) return rc0;
     const uint8_t *kb = (const uint8_t *)keys, *vb = (const uint8_t *)vals;
-    if (s.type == GX_MAP_RINGBUF) return set_err(rt, -EINVAL, "ring buffers have no keys");
+    if (s.type == GX_MAP_RINGBUF || s.type == GX_MAP_PREFETCH_QUEUE)
+        return set_err(rt, -EINVAL, "ring buffers and prefetch queues have no keys");
     if (flags > 2) return -EINVAL;
     if (s.type == GX_MAP_ARRAY || s.type == GX_MAP_PERTHREAD_ARRAY) {
         int first = 0;
@@ -700,6 +843,26 @@ int gx_ringbuf_drain(gx_rt *rt, int fd, void *buf, uint64_t cap, uint64_t *n_byt
     return 0;
 }
 
+int gx_prefetch_drain(gx_rt *rt, int fd, uint64_t *reqs, uint64_t cap, uint64_t *n_req) {
+    if (!check_map(rt, fd)) return -ENOENT;
+    Map &m = rt->maps[fd];
+    if (m.spec.type != GX_MAP_PREFETCH_QUEUE || !n_req) return -EINVAL;
+    int rc0 = sync(rt);
+    if (rc0) return rc0;
+    uint64_t reserved = 0;
+    CK(cudaMemcpy(&reserved, m.aux, 8, cudaMemcpyDeviceToHost), "prefetch queue counter");
+    const uint64_t n = std::min<uint64_t>(reserved, m.cap);
+    if (n > cap || (n && !reqs)) {
+        *n_req = n;
+        return -E2BIG;
+    }
+    if (n) CK(cudaMemcpy(reqs, m.data, 16 * n, cudaMemcpyDeviceToHost), "prefetch queue data");
+    CK(cudaMemset(m.aux, 0, 8), "prefetch queue reset");
+    for (uint64_t i = 0; i < n; i++) reqs[2 * i + 1] &= 0xFFFFFFFFull; /* {first_page, npages} */
+    *n_req = n;
+    return 0;
+}
+
 int gx_load_prog(gx_rt *rt, uint32_t hook, const void *insn_slots, uint32_t n_slots, int *prog_fd) {
     if (!rt || !insn_slots || !prog_fd || n_slots == 0) return -EINVAL;
     if (n_slots > 4096) return set_err(rt, -E2BIG, "program has %u slots (max 4096)", n_slots);
@@ -800,7 +963,8 @@ int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *
         d.value_size = maps[i].value_size;
         d.max_entries = maps[i].max_entries;
         d.nshards = 303104;
-        d.cap_mask = maps[i].type == GX_MAP_RINGBUF ? maps[i].max_entries - 1 : 2 * maps[i].max_entries - 1;
+        d.cap_mask = (maps[i].type == GX_MAP_RINGBUF || maps[i].type == GX_MAP_PREFETCH_QUEUE) ? maps[i].max_entries - 1
+                                                                                              : 2 * maps[i].max_entries - 1;
         d.priv_off = 0xFFFFFFFFu;
         d.coherent = 1;
     }
@@ -892,6 +1056,127 @@ int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, 
     return 0;
 }
 
+int gx_daemon_watch(gx_rt *rt, int fd) {
+    if (!rt || !check_map(rt, fd)) return -ENOENT;
+    const uint32_t t = rt->maps[fd].spec.type;
+    if (t != GX_MAP_ARRAY && t != GX_MAP_PERTHREAD_ARRAY)
+        return set_err(rt, -EINVAL, "only ARRAY and PERTHREAD_ARRAY maps are snapshotted");
+    if (rt->dmn.running) return set_err(rt, -EBUSY, "watch maps before gx_daemon_start");
+    for (int w : rt->dmn.watched)
+        if (w == fd) return 0;
+    rt->dmn.watched.push_back(fd);
+    return 0;
+}
+
+int gx_daemon_prefetch_range(gx_rt *rt, void *managed_ptr, uint64_t bytes) {
+    if (!rt) return -EINVAL;
+    rt->dmn.managed_ptr = (uint64_t)managed_ptr;
+    rt->dmn.managed_bytes = managed_ptr ? bytes : 0;
+    return 0;
+}
+
+int gx_daemon_start(gx_rt *rt, gx_prefetch_handler handler, void *user) {
+    if (!rt) return -EINVAL;
+    Daemon &D = rt->dmn;
+    if (D.running) return set_err(rt, -EBUSY, "daemon already running");
+    D.items.clear();
+    D.item_fd.clear();
+    uint64_t off = 0;
+    for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+        const Map &m = rt->maps[fd];
+        if (!m.valid || m.spec.type != GX_MAP_PREFETCH_QUEUE) continue;
+        GxPublishItem it{};
+        it.data = (uint64_t)m.data;
+        it.aux = (uint64_t)m.aux;
+        it.cap = m.cap;
+        it.kind = 0;
+        it.host_off = off;
+        off += 8 + 16 * m.cap;
+        D.items.push_back(it);
+        D.item_fd.push_back(fd);
+    }
+    for (int fd : D.watched) {
+        const Map &m = rt->maps[fd];
+        if (!m.valid) continue;
+        GxPublishItem it{};
+        it.data = (uint64_t)m.data;
+        it.kind = m.spec.type == GX_MAP_ARRAY ? 1 : 2;
+        it.K = m.spec.max_entries;
+        it.W = m.spec.value_size / 8;
+        it.nshards = m.nshards;
+        it.host_off = off;
+        off += 8ull * it.K * it.W;
+        D.items.push_back(it);
+        D.item_fd.push_back(fd);
+    }
+    D.slot_bytes = std::max<uint64_t>(off, 64);
+    for (auto &sl : D.slots) {
+        CK(cudaHostAlloc((void **)&sl.host, D.slot_bytes, cudaHostAllocMapped), "daemon slot");
+        CK(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming), "daemon event");
+        sl.busy = false;
+    }
+    if (!D.items.empty()) {
+        CK(cudaMalloc(&D.d_items, sizeof(GxPublishItem) * D.items.size()), "daemon items");
+        CK(cudaMemcpy(D.d_items, D.items.data(), sizeof(GxPublishItem) * D.items.size(), cudaMemcpyHostToDevice), "daemon items");
+    }
+    CK(cudaStreamCreateWithFlags(&D.s_prefetch, cudaStreamNonBlocking), "daemon stream");
+    D.fn = handler;
+    D.user = user;
+    D.stopping = false;
+    D.pending.clear();
+    D.snap.clear();
+    D.version = 0;
+    D.st = gx_daemon_stats{};
+    D.running = true;
+    D.th = std::thread(daemon_main, rt);
+    return 0;
+}
+
+int gx_daemon_stop(gx_rt *rt) {
+    if (!rt) return -EINVAL;
+    Daemon &D = rt->dmn;
+    if (!D.running) return 0;
+    {
+        std::lock_guard<std::mutex> lk(D.mu);
+        D.stopping = true;
+    }
+    D.cv_work.notify_all();
+    D.th.join();
+    D.running = false;
+    cudaStreamSynchronize(D.s_prefetch);
+    cudaStreamDestroy(D.s_prefetch);
+    for (auto &sl : D.slots) {
+        cudaFreeHost(sl.host);
+        cudaEventDestroy(sl.ev);
+        sl = DaemonSlot{};
+    }
+    cudaFree(D.d_items);
+    D.d_items = nullptr;
+    return 0;
+}
+
+int gx_snapshot_read(gx_rt *rt, int fd, void *buf, uint64_t cap, uint64_t *version) {
+    if (!rt || !version) return -EINVAL;
+    Daemon &D = rt->dmn;
+    std::lock_guard<std::mutex> lk(D.mu);
+    bool watched = false;
+    for (int w : D.watched) watched |= w == fd;
+    if (!watched) return -ENOENT;
+    auto it = D.snap.find(fd);
+    *version = it == D.snap.end() ? 0 : D.version;
+    if (it == D.snap.end()) return 0;
+    if (cap < it->second.size() || !buf) return -E2BIG;
+    memcpy(buf, it->second.data(), it->second.size());
+    return 0;
+}
+
+int gx_daemon_get_stats(gx_rt *rt, gx_daemon_stats *out) {
+    if (!rt || !out) return -EINVAL;
+    std::lock_guard<std::mutex> lk(rt->dmn.mu);
+    *out = rt->dmn.st;
+    return 0;
+}
+
 int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
     if (!rt || !out) return -EINVAL;
     int rc0 = sync(rt);
@@ -979,7 +1264,7 @@ static int ensure_base(gx_rt *rt, Map &m, bool retake = false) {
 int gx_merge_snapshot(gx_rt *rt, int fd) {
     if (!check_map(rt, fd)) return -ENOENT;
     Map &m = rt->maps[fd];
-    if (m.spec.type == GX_MAP_RINGBUF) return -EINVAL;
+    if (m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) return -EINVAL;
     return ensure_base(rt, m, true);
 }
 

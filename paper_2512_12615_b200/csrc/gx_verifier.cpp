@@ -29,7 +29,7 @@ namespace {
 
 /* --------------------------------------------------------------------------- encoding */
 enum { CL_LD = 0, CL_LDX = 1, CL_ST = 2, CL_STX = 3, CL_ALU = 4, CL_JMP = 5, CL_JMP32 = 6, CL_ALU64 = 7 };
-enum { HASH = 1, ARRAY = 2, PT = 6, RINGBUF = 27 };
+enum { HASH = 1, ARRAY = 2, PT = 6, RINGBUF = 27, PFQ = GX_MAP_TYPE_PFQ };
 
 struct Raw {
     uint8_t code, dst, src;
@@ -1362,7 +1362,7 @@ struct Verifier {
         int32_t id = ins[pc].imm;
         char msg[128];
         if (id == 93 || id == 94) return fail(pc, GX_FORBIDDEN_SYNC, "bpf_spin_lock/unlock: GPU-wide synchronisation is forbidden on device hooks");
-        if (id != 1 && id != 2 && id != 130) {
+        if (id != 1 && id != 2 && id != 130 && id != GX_FN_MEM_PREFETCH) {
             snprintf(msg, sizeof msg, "helper %d is not available to device programs", id);
             return fail(pc, GX_BAD_HELPER, msg);
         }
@@ -1376,7 +1376,8 @@ struct Verifier {
         GxMapUse &u = out.use[m];
         u.used = true;
         if (id == 1 || id == 2) {
-            if (mi.type == RINGBUF) return fail(pc, GX_BAD_HELPER, "map lookup/update on a ring buffer");
+            if (mi.type == RINGBUF || mi.type == PFQ)
+                return fail(pc, GX_BAD_HELPER, "map lookup/update on a ring buffer / prefetch queue");
             if (!check_arg_mem(pc, st, st.r[2], mi.key_size, mi.key_size, "key", kk, ka)) return false;
             if (kk == MK_MAPV) out.use[st.r[2].map].reads = true;
             if (id == 2) {
@@ -1389,6 +1390,16 @@ struct Verifier {
             } else {
                 P.ch += 1;
             }
+        } else if (id == GX_FN_MEM_PREFETCH) {
+            /* gdev_mem_prefetch(queue, addr, len) (F-1): addr and len are
+             * plain scalars (no memory is touched), range errors are run-time -EINVAL */
+            if (mi.type != PFQ) return fail(pc, GX_BAD_HELPER, "gdev_mem_prefetch needs a prefetch-queue map");
+            for (int a = 2; a <= 3; a++)
+                if (st.r[a].type != SCALAR)
+                    return fail(pc, st.r[a].type == NOT_INIT ? GX_UNINIT_READ : GX_BAD_HELPER,
+                                a == 2 ? "prefetch address must be a scalar" : "prefetch length must be a scalar");
+            u.writes = true;
+            P.ch += 1;
         } else {
             if (mi.type != RINGBUF) return fail(pc, GX_BAD_HELPER, "bpf_ringbuf_output needs a ring buffer map");
             Reg &R3 = st.r[3], &R4 = st.r[4];
@@ -1729,6 +1740,8 @@ struct Verifier {
                     else if (id == 2) {
                         g.op = mi.type == ARRAY ? GX_CALL_UPDATE_ARRAY : mi.type == PT ? GX_CALL_UPDATE_PT : GX_CALL_UPDATE_HASH;
                         g.imm = (uint64_t)(uint32_t)f.val_addr;
+                    } else if (id == GX_FN_MEM_PREFETCH) {
+                        g.op = GX_CALL_MEM_PREFETCH;
                     } else {
                         g.op = GX_CALL_RINGBUF_OUTPUT;
                         g.off = (int16_t)f.val_addr;
@@ -1840,6 +1853,11 @@ struct Verifier {
             break;
         case GX_CALL_RINGBUF_OUTPUT:
             u.use = (g.flags & GXF_VAL_MAPV) ? R(2) : 0;
+            u.def = 0x3F;
+            u.effect = true;
+            break;
+        case GX_CALL_MEM_PREFETCH:
+            u.use = R(2) | R(3);
             u.def = 0x3F;
             u.effect = true;
             break;
@@ -2040,7 +2058,7 @@ int gx_verify_program(const uint8_t *slots, uint32_t n, const GxMapInfo *maps, c
     uint32_t comm = 1;
     for (int m = 0; m < GX_MAX_MAPS; m++) {
         const GxMapUse &u = out.use[m];
-        if (!u.used || !maps[m].valid || maps[m].type == PT || maps[m].type == RINGBUF) continue;
+        if (!u.used || !maps[m].valid || maps[m].type == PT || maps[m].type == RINGBUF || maps[m].type == PFQ) continue;
         if (u.writes && (u.non_add_write && !u.update_call)) comm = 0;
         if (u.reads && u.writes) comm = 0;
     }

@@ -6,7 +6,7 @@ import numpy as np
 
 from gxin import configs
 
-RINGBUF = 27
+RINGBUF, PREFETCH_QUEUE = 27, 64
 
 
 def outputs(engine, setup):
@@ -15,6 +15,8 @@ def outputs(engine, setup):
     for (tenant, name), fd in sorted(setup.fds.items()):
         if engine.specs[fd][0] == RINGBUF:
             out[(tenant, name)] = tuple(engine.ringbuf_records(fd))
+        elif engine.specs[fd][0] == PREFETCH_QUEUE:   # canonical content: the request set (F-2)
+            out[(tenant, name)] = tuple(engine.prefetch_requests(fd))
         else:
             out[(tenant, name)] = engine.dump(fd)
     return out

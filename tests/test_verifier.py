@@ -5,10 +5,10 @@ import pytest
 import paper_2512_12615_b200 as gx
 from gxin import asm, programs
 
-HASH, ARRAY, PT, RINGBUF = 1, 2, 6, 27
+HASH, ARRAY, PT, RINGBUF, PFQ = 1, 2, 6, 27, 64
 MAPS = {0: (ARRAY, 4, 8, 16), 1: (HASH, 8, 8, 64), 2: (PT, 4, 16, 32), 3: (RINGBUF, 0, 0, 4096),
-        4: (ARRAY, 4, 2048, 1)}
-NAMES = {"arr": 0, "h": 1, "pt": 2, "rb": 3, "g": 4}
+        4: (ARRAY, 4, 2048, 1), 5: (PFQ, 0, 0, 64)}
+NAMES = {"arr": 0, "h": 1, "pt": 2, "rb": 3, "g": 4, "pfq": 5}
 
 
 def verify(text, strict=False, **kw):
@@ -33,6 +33,8 @@ ACCEPT = {
     "var_offset_in_bounds": "ldxdw r2, [r1+0]\nand64 r2, 0xf8\nlddw r1, mapval:g+0\nadd64 r1, r2\nldxdw r0, [r1+0]\nexit",
     "atomic_fetch": LOOKUP + "jeq r0, 0, +4\nmov64 r1, 1\natomic_fetch_add64 [r0+0], r1\nmov64 r0, r1\nexit\nmov64 r0, 0\nexit",
     "hash_update": "stdw [r10-8], 5\nstdw [r10-16], 7\nlddw r1, map:h\nmov64 r2, r10\nadd64 r2, -8\nmov64 r3, r10\nadd64 r3, -16\nmov64 r4, 0\ncall 2\nexit",
+    "mem_prefetch": "ldxdw r2, [r1+0]\nmov64 r3, 4096\nlddw r1, map:pfq\ncall 1000\nexit",
+    "mem_prefetch_policy": programs.P6.replace("map:pfq", "map:pfq").replace("mapval:pstat+0", "mapval:g+0"),
     "ringbuf": "stdw [r10-16], 1\nstdw [r10-8], 2\nlddw r1, map:rb\nmov64 r2, r10\nadd64 r2, -16\nmov64 r3, 16\nmov64 r4, 0\ncall 130\nexit",
     "percpu_rmw": "stw [r10-4], 3\nlddw r1, map:pt\nmov64 r2, r10\nadd64 r2, -4\ncall 1\njeq r0, 0, +3\nldxdw r1, [r0+8]\nadd64 r1, 1\nstxdw [r0+8], r1\nmov64 r0, 0\nexit",
     "jmp32_ok": "ldxw r2, [r1+16]\nmov64 r0, 0\njgt32 r2, 5, +1\nmov64 r0, 1\nexit",
@@ -71,6 +73,10 @@ REJECT = {
     "bad_helper": ("call 6\nmov64 r0, 0\nexit", False, "BAD_HELPER"),
     "spin_lock": ("call 93\nmov64 r0, 0\nexit", False, "FORBIDDEN_SYNC"),
     "helper_bad_map_arg": ("mov64 r1, 1\nmov64 r2, r10\ncall 1\nmov64 r0, 0\nexit", False, "BAD_HELPER"),
+    "prefetch_on_array": ("mov64 r2, 0\nmov64 r3, 64\nlddw r1, map:arr\ncall 1000\nexit", False, "BAD_HELPER"),
+    "prefetch_uninit_len": ("mov64 r2, 0\nlddw r1, map:pfq\ncall 1000\nexit", False, "UNINIT_READ"),
+    "prefetch_ptr_len": ("mov64 r2, 0\nmov64 r3, r10\nlddw r1, map:pfq\ncall 1000\nexit", False, "BAD_HELPER"),
+    "lookup_on_prefetch_queue": ("stw [r10-4], 0\nlddw r1, map:pfq\nmov64 r2, r10\nadd64 r2, -4\ncall 1\nmov64 r0, 0\nexit", False, "BAD_HELPER"),
     "ringbuf_var_size": ("ldxdw r3, [r1+0]\nstdw [r10-8], 1\nlddw r1, map:rb\nmov64 r2, r10\nadd64 r2, -8\nmov64 r4, 0\ncall 130\nexit", False, "BAD_HELPER"),
     "bad_reg": (".raw 0xb7 11 0 0 0\nexit", False, "BAD_REG"),
     "write_r10": ("mov64 r10, 0\nmov64 r0, 0\nexit", False, "BAD_REG"),
