@@ -289,7 +289,8 @@ def gx_read_map(rt, fd, spec):
         keys = C.create_string_buffer(ks * me + 8)
         vals = C.create_string_buffer(vs * me + 8)
         _check(lib().gx_read_map(rt, fd, keys, vals, me, C.byref(n)), "gx_read_map", rt)
-        return [(int.from_bytes(keys.raw[i * ks:(i + 1) * ks], "little"), vals.raw[i * vs:(i + 1) * vs])
+        kr, vr = keys.raw, vals.raw   # .raw copies the whole buffer: take it once
+        return [(int.from_bytes(kr[i * ks:(i + 1) * ks], "little"), vr[i * vs:(i + 1) * vs])
                 for i in range(n.value)]
     vals = C.create_string_buffer(vs * me)
     _check(lib().gx_read_map(rt, fd, None, vals, me, C.byref(n)), "gx_read_map", rt)
