@@ -17,6 +17,9 @@
 #define GX_NREGS 11
 #define GX_FN_MEM_PREFETCH 1000   /* gdev_mem_prefetch helper id (F-1) */
 #define GX_MAP_TYPE_PFQ 64        /* prefetch queue map type (F-2) */
+/* request filter after a queue's records (F-2 set semantics): clamp(capacity, 2^12, 2^20) words,
+ * the count carried in GxMapDesc.nshards / GxPublishItem.nshards */
+#define GX_PFQ_FILTER_WORDS(cap) ((cap) < 4096u ? 4096u : (cap) > (1u << 20) ? (1u << 20) : (cap))
 
 /* ---- pre-decoded instruction (16 B), produced by the verifier for the executor ----
  * Every field is warp-uniform on the fast path, so decode costs one broadcast LDS.128. */
@@ -86,7 +89,7 @@ struct GxMapDesc {
     uint64_t aux;          /* HASH: u64 counters {count}; RINGBUF: u64 {prod, used};
                               PREFETCH QUEUE: u64 {reserved} */
     uint32_t type, key_size, value_size, max_entries;
-    uint32_t nshards;      /* PT */
+    uint32_t nshards;      /* PT: shards; PREFETCH QUEUE: request-filter words (a power of two) */
     uint32_t cap_mask;     /* HASH: capacity-1; RINGBUF: capacity-1; PREFETCH QUEUE: capacity-1 */
     uint32_t priv_off;     /* byte offset of the privatized copy in shared memory, or ~0u */
     uint32_t coherent;     /* 1: written during this launch -> loads bypass L1 */
@@ -118,7 +121,7 @@ struct GxPublishItem {
     uint64_t data, aux;    /* device storage / counters of the map */
     uint64_t host_off;     /* byte offset in the host slot */
     uint64_t cap;          /* prefetch queue capacity (requests) */
-    uint32_t kind;         /* 0 prefetch queue, 1 ARRAY, 2 PERTHREAD */
+    uint32_t kind;         /* 0 prefetch queue, 1 ARRAY (or a folded PERTHREAD staging copy) */
     uint32_t K, W;         /* entries, u64 words per value */
     uint32_t nshards;
 };

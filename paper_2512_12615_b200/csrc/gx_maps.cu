@@ -27,6 +27,30 @@ __global__ void pt_fold_kernel(const uint64_t *__restrict__ data, uint32_t nshar
     }
 }
 
+/* the same fold as a streaming pass: the shard blocks (K*W*32 contiguous words per 32 shards) are
+ * read coalesced by the whole grid, each block accumulates the K*W canonical words in shared
+ * memory (un-rotating the lane-rotated key index) and adds them to `out` (zeroed first) once */
+__global__ void pt_fold_stream_kernel(const uint64_t *__restrict__ data, uint32_t nshards, uint32_t K, uint32_t W,
+                                      unsigned long long *__restrict__ out) {
+    extern __shared__ unsigned long long acc[];
+    const uint32_t KW = K * W;
+    for (uint32_t j = threadIdx.x; j < KW; j += blockDim.x) acc[j] = 0;
+    __syncthreads();
+    const uint64_t total = (uint64_t)nshards * KW;   /* = (nshards / 32) * KW * 32 */
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += gridDim.x * (uint64_t)blockDim.x) {
+        const uint32_t l = (uint32_t)(i & 31);
+        const uint32_t wq = (uint32_t)((i >> 5) % KW);   /* kk * W + w within the 32-shard block */
+        const uint32_t kk = wq / W, w = wq % W;
+        const uint32_t r = l % K;
+        const uint32_t k = kk + r >= K ? kk + r - K : kk + r;
+        const uint64_t v = data[i];
+        if (v) atomicAdd(&acc[k * W + w], (unsigned long long)v);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < KW; j += blockDim.x)
+        if (acc[j]) atomicAdd(&out[j], acc[j]);
+}
+
 /* host write of key k: shard 0 = value, every other shard's copy of key k = 0 */
 __global__ void pt_set_kernel(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)W * nshards;
@@ -47,36 +71,31 @@ __global__ void pt_store_canonical_kernel(uint64_t *data, uint32_t nshards, uint
 }
 
 /* Runtime-daemon publish point (include/gx.h): runs on the batch's stream
- * right after its kernel and writes into a pinned, device-mapped host slot -- block b handles
- * item b: a prefetch queue (u64 count, then count x 16-B requests; the queue is emptied) or a
- * watched map's canonical snapshot (ARRAY copy, PERTHREAD SUM fold). */
+ * right after its kernel and writes into a pinned, device-mapped host slot.  blockIdx.y = item: a
+ * prefetch queue (u64 count, then count x 16-B requests) or an ARRAY-shaped snapshot (an ARRAY,
+ * or a per-thread map already SUM-folded into a device staging copy by gx_k_pt_fold); the blocks
+ * of x stride over the item.  publish_reset_kernel (stream-ordered after it) empties the queues
+ * and their request filters. */
 __global__ void publish_kernel(const GxPublishItem *__restrict__ items, uint8_t *__restrict__ host) {
-    const GxPublishItem it = items[blockIdx.x];
+    const GxPublishItem it = items[blockIdx.y];
     uint64_t *out = reinterpret_cast<uint64_t *>(host + it.host_off);
-    if (it.kind == 0) { /* prefetch queue */
-        unsigned long long *ctr = reinterpret_cast<unsigned long long *>(it.aux);
-        const uint64_t n = min((uint64_t)*ctr, it.cap);
-        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
-        for (uint64_t i = threadIdx.x; i < 2 * n; i += blockDim.x) out[1 + i] = src[i];
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            out[0] = n;
-            *ctr = 0;
-        }
-    } else if (it.kind == 1) { /* ARRAY */
-        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
-        for (uint64_t i = threadIdx.x; i < (uint64_t)it.K * it.W; i += blockDim.x) out[i] = src[i];
-    } else { /* PERTHREAD: canonical value = SUM over shards (S4) */
-        const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
-        const uint32_t lane = threadIdx.x & 31;
-        for (uint64_t j = threadIdx.x >> 5; j < (uint64_t)it.K * it.W; j += blockDim.x >> 5) {
-            const uint32_t k = (uint32_t)(j / it.W), w = (uint32_t)(j % it.W);
-            uint64_t acc = 0;
-            for (uint32_t sh = lane; sh < it.nshards; sh += 32) acc += src[gxd::pt_word_index(it.K, it.W, k, w, sh)];
-            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(GX_FULL, acc, o);
-            if (lane == 0) out[j] = acc;
-        }
+    const uint64_t *src = reinterpret_cast<const uint64_t *>(it.data);
+    const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, step = gridDim.x * (uint64_t)blockDim.x;
+    if (it.kind == 0) {
+        const uint64_t n = min((uint64_t)*reinterpret_cast<const unsigned long long *>(it.aux), it.cap);
+        for (uint64_t i = t0; i < 2 * n; i += step) out[1 + i] = src[i];
+        if (t0 == 0) out[0] = n;
+    } else {
+        for (uint64_t i = t0; i < (uint64_t)it.K * it.W; i += step) out[i] = src[i];
     }
+}
+__global__ void publish_reset_kernel(const GxPublishItem *__restrict__ items) {
+    const GxPublishItem it = items[blockIdx.y];
+    if (it.kind != 0) return;
+    uint64_t *filt = reinterpret_cast<uint64_t *>(it.data) + 2 * it.cap;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < it.nshards; i += gridDim.x * (uint64_t)blockDim.x)
+        filt[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<unsigned long long *>(it.aux) = 0;
 }
 
 __global__ void hash_init_kernel(uint64_t *slots, uint64_t cap) {
@@ -176,7 +195,16 @@ inline uint32_t grid_for(uint64_t n, uint32_t block) {
 extern "C" {
 
 int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint64_t *out, cudaStream_t s) {
-    pt_fold_kernel<<<grid_for((uint64_t)K * W * 32, 256), 256, 0, s>>>(data, nshards, K, W, out);
+    if (nshards % 32 == 0 && (uint64_t)K * W * 8 <= 48 * 1024) {
+        cudaError_t e = cudaMemsetAsync(out, 0, 8ull * K * W, s);
+        if (e) return (int)e;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        pt_fold_stream_kernel<<<nsm * 4, 512, 8ull * K * W, s>>>(data, nshards, K, W, (unsigned long long *)out);
+    } else {
+        pt_fold_kernel<<<grid_for((uint64_t)K * W * 32, 256), 256, 0, s>>>(data, nshards, K, W, out);
+    }
     return (int)cudaGetLastError();
 }
 int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals,
@@ -191,7 +219,8 @@ int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32
 }
 int gx_k_publish(const GxPublishItem *items, uint32_t n_items, uint8_t *host_slot, cudaStream_t s) {
     if (!n_items) return 0;
-    publish_kernel<<<n_items, 256, 0, s>>>(items, host_slot);
+    publish_kernel<<<dim3(148, n_items), 256, 0, s>>>(items, host_slot);
+    publish_reset_kernel<<<dim3(64, n_items), 256, 0, s>>>(items);
     return (int)cudaGetLastError();
 }
 

@@ -165,6 +165,8 @@ struct Daemon {
     std::vector<GxPublishItem> items;      /* frozen layout at start */
     std::vector<int> item_fd;
     GxPublishItem *d_items = nullptr;
+    struct Fold { const uint64_t *data; uint32_t nshards, K, W; uint64_t *staging; };
+    std::vector<Fold> folds;                /* watched per-thread maps: SUM fold before publishing */
     std::map<int, std::vector<uint8_t>> snap; /* latest published canonical snapshots */
     uint64_t version = 0;
     gx_daemon_stats st{};
@@ -426,6 +428,10 @@ int daemon_publish(gx_rt *rt, cudaStream_t stream) {
         }
         D.slots[slot].busy = true;
     }
+    for (const Daemon::Fold &f : D.folds) {
+        int e = gx_k_pt_fold(f.data, f.nshards, f.K, f.W, f.staging, stream);
+        if (e) return cuda_err(rt, (cudaError_t)e, "daemon fold");
+    }
     int e = gx_k_publish(D.d_items, (uint32_t)D.items.size(), D.slots[slot].host, stream);
     if (e) return cuda_err(rt, (cudaError_t)e, "daemon publish");
     CK(cudaEventRecord(D.slots[slot].ev, stream), "daemon event");
@@ -679,7 +685,8 @@ int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
             (s.max_entries & (s.max_entries - 1)))
             return set_err(rt, -EINVAL, "bad PREFETCH_QUEUE spec (capacity in requests: power of two in [64, 2^24])");
         m.cap = s.max_entries;
-        m.data_bytes = 16ull * s.max_entries;
+        m.nshards = GX_PFQ_FILTER_WORDS(s.max_entries);
+        m.data_bytes = 16ull * s.max_entries + 8ull * m.nshards; /* records + request filter */
         break;
     default:
         return set_err(rt, -EINVAL, "unknown map type %u", s.type);
@@ -858,6 +865,7 @@ int gx_prefetch_drain(gx_rt *rt, int fd, uint64_t *reqs, uint64_t cap, uint64_t 
     }
     if (n) CK(cudaMemcpy(reqs, m.data, 16 * n, cudaMemcpyDeviceToHost), "prefetch queue data");
     CK(cudaMemset(m.aux, 0, 8), "prefetch queue reset");
+    CK(cudaMemset((uint8_t *)m.data + 16 * m.cap, 0, 8ull * m.nshards), "prefetch filter reset");
     for (uint64_t i = 0; i < n; i++) reqs[2 * i + 1] &= 0xFFFFFFFFull; /* {first_page, npages} */
     *n_req = n;
     return 0;
@@ -962,7 +970,7 @@ int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *
         d.key_size = maps[i].key_size;
         d.value_size = maps[i].value_size;
         d.max_entries = maps[i].max_entries;
-        d.nshards = 303104;
+        d.nshards = maps[i].type == GX_MAP_PREFETCH_QUEUE ? GX_PFQ_FILTER_WORDS(maps[i].max_entries) : 303104;
         d.cap_mask = (maps[i].type == GX_MAP_RINGBUF || maps[i].type == GX_MAP_PREFETCH_QUEUE) ? maps[i].max_entries - 1
                                                                                               : 2 * maps[i].max_entries - 1;
         d.priv_off = 0xFFFFFFFFu;
@@ -1081,6 +1089,7 @@ int gx_daemon_start(gx_rt *rt, gx_prefetch_handler handler, void *user) {
     if (D.running) return set_err(rt, -EBUSY, "daemon already running");
     D.items.clear();
     D.item_fd.clear();
+    D.folds.clear();
     uint64_t off = 0;
     for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
         const Map &m = rt->maps[fd];
@@ -1089,6 +1098,7 @@ int gx_daemon_start(gx_rt *rt, gx_prefetch_handler handler, void *user) {
         it.data = (uint64_t)m.data;
         it.aux = (uint64_t)m.aux;
         it.cap = m.cap;
+        it.nshards = m.nshards;
         it.kind = 0;
         it.host_off = off;
         off += 8 + 16 * m.cap;
@@ -1100,10 +1110,16 @@ int gx_daemon_start(gx_rt *rt, gx_prefetch_handler handler, void *user) {
         if (!m.valid) continue;
         GxPublishItem it{};
         it.data = (uint64_t)m.data;
-        it.kind = m.spec.type == GX_MAP_ARRAY ? 1 : 2;
+        it.kind = 1;
         it.K = m.spec.max_entries;
         it.W = m.spec.value_size / 8;
         it.nshards = m.nshards;
+        if (m.spec.type == GX_MAP_PERTHREAD_ARRAY) { /* folded into a staging copy first */
+            uint64_t *stg = nullptr;
+            CK(cudaMalloc(&stg, 8ull * it.K * it.W), "daemon fold staging");
+            D.folds.push_back({(const uint64_t *)m.data, m.nshards, it.K, it.W, stg});
+            it.data = (uint64_t)stg;
+        }
         it.host_off = off;
         off += 8ull * it.K * it.W;
         D.items.push_back(it);
@@ -1152,6 +1168,8 @@ int gx_daemon_stop(gx_rt *rt) {
     }
     cudaFree(D.d_items);
     D.d_items = nullptr;
+    for (auto &f : D.folds) cudaFree(f.staging);
+    D.folds.clear();
     return 0;
 }
 

@@ -36,6 +36,8 @@ __global__ void kern(unsigned long long *buf, uint64_t mask, int iters, unsigned
             atomicAdd(&buf[w & mask], 1ull);
         }
         if (MODE == 5) acc += atomicAdd(&buf[0], 1ull);                         // one address
+        if (MODE == 6 && (threadIdx.x & 31) == 0) acc += atomicAdd(&buf[0], 32ull); // one address, one returning op per warp
+        if (MODE == 7 && (threadIdx.x & 31) == 0) atomicAdd(&buf[0], 32ull);        // one address, one RED per warp
     }
     if (acc == 0x123456789ull) sink[0] = acc;
 }
@@ -74,10 +76,13 @@ int main() {
     double r3 = run<3>(buf, words - 1, sink, blocks, iters);
     double r4 = run<4>(buf, words - 1, sink, blocks, iters);
     double r5 = run<5>(buf, words - 1, sink, sms, 16);
+    double r6 = run<6>(buf, words - 1, sink, sms * 8, 16) / 32;   /* warp-level ops */
+    double r7 = run<7>(buf, words - 1, sink, sms * 8, 16) / 32;
     printf("{\"device\": \"B200\", \"buffer_bytes\": %llu, \"atom_add_u64_random_per_s\": %.4g, "
            "\"red_add_u64_random_per_s\": %.4g, \"atom_cas_b64_random_per_s\": %.4g, "
            "\"atom_cas_b128_random_per_s\": %.4g, \"red_add_u64_warp_uniform_per_s\": %.4g, "
-           "\"atom_add_u64_same_address_per_s\": %.4g}\n",
-           (unsigned long long)(words * 8), r0, r1, r2, r3, r4, r5);
+           "\"atom_add_u64_same_address_per_s\": %.4g, \"atom_add_u64_same_address_warp_ops_per_s\": %.4g, "
+           "\"red_add_u64_same_address_warp_ops_per_s\": %.4g}\n",
+           (unsigned long long)(words * 8), r0, r1, r2, r3, r4, r5, r6, r7);
     return cudaGetLastError() != cudaSuccess;
 }
