@@ -317,6 +317,7 @@ def main():
         if args.extra:
             extra_lines(rt, args)
             f2_lines()
+            f4_lines()
     if world > 1:
         dist.destroy_process_group()
 
@@ -483,6 +484,45 @@ def f2_lines():
             print(json.dumps(line), file=sys.stderr, flush=True)
             rt.close()
         del ev
+
+
+def f4_lines():
+    """the paper's hook-overhead microbenchmark shape (PAPER.md:466-471,
+    530): c = a + b over 2^28 floats with the counter policy inlined as a hook on both loads
+    (gx_instrument), against the same kernel compiled without hooks."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import asm, instrument
+    n = 1 << 28
+    a = torch.randn(n, device="cuda")
+    b = torch.randn(n, device="cuda")
+    c = torch.empty(n, device="cuda")
+    rt = gx.Runtime(0)
+    counts = rt.create_map(gx.GX_MAP_ARRAY, 4, 8, 256)
+    prog = rt.load_prog(asm.assemble(instrument.PI, {"counts": counts}))
+    res = {}
+    for hooks in (0, 1):
+        k = gx.gx_instrument(rt.rt, prog, f"#define GX_HOOKS {hooks}\n" + instrument.VADD)
+        launch = lambda: gx.gx_kernel_launch(rt.rt, k, "vadd", ((n + 255) // 256,), (256,), [a, b, c, 0, n])
+        for _ in range(3):
+            launch()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            launch()
+        e1.record()
+        torch.cuda.synchronize()
+        res[hooks] = e0.elapsed_time(e1) / 10
+        gx.gx_kernel_free(rt.rt, k)
+    total = int(rt.array_u64(counts).sum())
+    hooks_per_launch = 2 * n
+    print(json.dumps({"f4": "vadd", "elements": n, "ms_no_hooks": res[0], "ms_hooks": res[1],
+                      "overhead_pct": (res[1] - res[0]) / res[0] * 100,
+                      "hook_events_per_s": hooks_per_launch / (res[1] / 1e3),
+                      "added_ns_per_hook": (res[1] - res[0]) * 1e6 / hooks_per_launch,
+                      "counter_total_ok": total == 13 * hooks_per_launch}), file=sys.stderr, flush=True)
+    rt.close()
 
 
 if __name__ == "__main__":

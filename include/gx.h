@@ -146,6 +146,29 @@ int  gx_ringbuf_drain(gx_rt *rt, int map_fd, void *buf, uint64_t cap, uint64_t *
  * (With a daemon running, the daemon drains the queues instead.) */
 int  gx_prefetch_drain(gx_rt *rt, int map_fd, uint64_t *reqs, uint64_t cap, uint64_t *n_req);
 
+/* ---------------------------------------------------------------- inline instrumentation (§8f f4)
+ * "Trampolines, placed at GPU kernel entry, selected memory instructions (such as global loads and
+ * atomic operations) ... verified eBPF code executes after kernel launch" (§5.3);
+ * the vector-add hook-overhead microbenchmark.  Here the trampoline is made
+ * at compile time: gx_instrument JIT-compiles the verified program prog_fd as inline __device__ hooks
+ * together with user_src (CUDA C++ with extern "C" __global__ kernels) in one NVRTC sm_100a module:
+ *     uint64_t gx_hook_access(unsigned group, const void *addr, uint32_t size, bool is_write);
+ *     uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost);
+ * Each call runs the program once per lane of `group` on an event record built in registers
+ * (addr, globaltimer ts, hook word, linear block id, %smid, hardware warp slot, lane, size) and
+ * returns that lane's R0 (the policy decision).  `group` must be exactly the set of lanes making the
+ * call together -- e.g. __ballot_sync(~0u, pred) taken where the warp is converged, then the call
+ * under `if (pred)` -- because the helpers' warp collectives name it.  Per-thread maps are sharded by
+ * (SM, warp slot, lane); maps are never privatised in shared memory; map addresses are baked into
+ * the module (the maps must outlive the handle).  Errors: -ENOENT (no program), -EPERM (not
+ * verified), -EINVAL (module does not compile; log holds the NVRTC log). */
+typedef struct gx_kernel gx_kernel;
+int  gx_instrument(gx_rt *rt, int prog_fd, const char *user_src, gx_kernel **out, char *log, uint64_t log_len);
+/* Launches kernel `name` of the module (cuLaunchKernel argument conventions; async on the stream). */
+int  gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t grid[3], const uint32_t block[3],
+                      uint32_t smem, void **args, void *cuda_stream);
+void gx_kernel_free(gx_rt *rt, gx_kernel *k);
+
 /* ---------------------------------------------------------------- runtime daemon (§8f f2)
  * "A runtime daemon asynchronously flushes GPU-local shards to host-visible canonical map
  * instances, providing coherent snapshots to host-side policies without synchronization

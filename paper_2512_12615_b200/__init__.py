@@ -31,7 +31,8 @@ EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_m
            "gx_ringbuf_drain", "gx_load_prog", "gx_verify", "gx_verify_offline", "gx_jit_offline", "gx_attach", "gx_run_batch", "gx_run_batch_ex", "gx_run_batch_host",
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply", "gx_prefetch_drain", "gx_daemon_start", "gx_daemon_stop", "gx_daemon_watch",
-           "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range")
+           "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range", "gx_instrument",
+           "gx_kernel_launch", "gx_kernel_free")
 
 
 class gx_map_spec(C.Structure):
@@ -103,6 +104,9 @@ def lib():
         "gx_snapshot_read": (i32, [vp, i32, vp, u64, p64]),
         "gx_daemon_get_stats": (i32, [vp, C.POINTER(gx_daemon_stats)]),
         "gx_daemon_prefetch_range": (i32, [vp, vp, u64]),
+        "gx_instrument": (i32, [vp, i32, C.c_char_p, C.POINTER(vp), C.c_char_p, u64]),
+        "gx_kernel_launch": (i32, [vp, vp, C.c_char_p, C.POINTER(u32), C.POINTER(u32), u32, C.POINTER(vp), vp]),
+        "gx_kernel_free": (None, [vp, vp]),
         "gx_load_prog": (i32, [vp, u32, vp, u32, C.POINTER(i32)]),
         "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
         "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
@@ -342,6 +346,35 @@ def gx_daemon_get_stats(rt) -> dict:
 
 def gx_daemon_prefetch_range(rt, ptr, nbytes):
     _check(lib().gx_daemon_prefetch_range(rt, ptr, nbytes), "gx_daemon_prefetch_range", rt)
+
+
+def gx_instrument(rt, prog_fd, user_src: str):
+    """f4: the verified program as inline device hooks linked into user_src; returns a handle."""
+    h = C.c_void_p()
+    log = C.create_string_buffer(1 << 16)
+    _check(lib().gx_instrument(rt, prog_fd, user_src.encode(), C.byref(h), log, len(log)), "gx_instrument", rt)
+    return h
+
+
+def gx_kernel_launch(rt, handle, name: str, grid, block, args, smem=0, stream=None):
+    """args: torch tensors (passed as device pointers), Python ints (u64) or ctypes values."""
+    keep = []
+    for a in args:
+        if hasattr(a, "data_ptr"):
+            keep.append(C.c_void_p(a.data_ptr()))
+        elif isinstance(a, int):
+            keep.append(C.c_uint64(a))
+        else:
+            keep.append(a)
+    argv = (C.c_void_p * max(len(keep), 1))(*[C.cast(C.pointer(k), C.c_void_p) for k in keep])
+    g = (C.c_uint32 * 3)(*(list(grid) + [1, 1, 1])[:3])
+    b = (C.c_uint32 * 3)(*(list(block) + [1, 1, 1])[:3])
+    _check(lib().gx_kernel_launch(rt, handle, name.encode(), g, b, smem, argv, _stream_handle(stream)),
+           "gx_kernel_launch", rt)
+
+
+def gx_kernel_free(rt, handle):
+    lib().gx_kernel_free(rt, handle)
 
 
 def gx_ringbuf_drain(rt, fd) -> list[bytes]:

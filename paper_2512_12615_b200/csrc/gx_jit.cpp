@@ -643,6 +643,7 @@ struct Gen {
         ptc_ = getenv("GX_JIT_PTCACHE") && atoi(getenv("GX_JIT_PTCACHE")) != 0;
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
+        if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         /* two launch bodies: event ingest through the block-wide TMA ring (large batches of light
@@ -657,6 +658,52 @@ struct Gen {
           << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_r" << args << " {\n  gx_body_ring<true>(ev, n, ret, gstats);\n}\n"
           << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_g" << args << " {\n  gx_body_reg<false>(ev, n, ret, gstats);\n}\n"
           << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_gr" << args << " {\n  gx_body_reg<true>(ev, n, ret, gstats);\n}\n";
+    }
+
+    /* f4: the program as __device__ hooks a user kernel calls inline -- the paper's
+     * "trampolines ... at GPU kernel entry, selected memory instructions" made at
+     * compile time.  The hooking lanes pass their group explicitly (a ballot taken where the warp
+     * is converged): the helpers' warp collectives need the exact set of lanes that reach them.
+     * The ctx is built in registers from the call site; per-thread shards are keyed by the
+     * hardware slot (SM, warp slot, lane), unique among resident threads. */
+    void instrument(const GxInsn *image, uint32_t n, const std::string &user) {
+        ptc_ = false;
+        ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
+        o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
+        program(0, image, n);
+        o << "__device__ __forceinline__ uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size) {\n"
+             "  uint32_t smid, wslot;\n"
+             "  asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid));\n"
+             "  asm volatile(\"mov.u32 %0, %%warpid;\" : \"=r\"(wslot));\n"
+             "  uint64_t ts;\n"
+             "  asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(ts));\n"
+             "  const uint32_t lane = threadIdx.x & 31;\n"
+             "  const uint32_t blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);\n"
+             "  Ctx c;\n"
+             "  c.w[0] = (uint32_t)addr; c.w[1] = (uint32_t)(addr >> 32); c.w[2] = (uint32_t)ts; c.w[3] = (uint32_t)(ts >> 32);\n"
+             "  c.w[4] = hook; c.w[5] = blk; c.w[6] = (smid & 0xFFFF) | ((wslot & 63) << 16) | (lane << 24); c.w[7] = size;\n"
+             "  const uint32_t shard = (smid * 64 + (wslot & 63)) * 32 + lane;\n"
+             "  uint64_t retv = 0;\n"
+             "  unsigned long long herr = 0, drop = 0, rbb = 0, hfull = 0;\n"
+             "  PtCache ptc;\n"
+             "  if (group == GX_ALL) prog0<true>(c, GX_ALL, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
+             "  else prog0<false>(c, group, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
+             "  unsigned long long *st = (unsigned long long *)" << hex(L.stats) << ";\n"
+             "  if (herr) atomicAdd(&st[" << GXS_HERR << "], herr);\n"
+             "  if (drop) atomicAdd(&st[" << GXS_RB_DROPS << "], drop);\n"
+             "  if (rbb) atomicAdd(&st[" << GXS_RB_BYTES << "], rbb);\n"
+             "  if (hfull) atomicAdd(&st[" << GXS_HFULL << "], hfull);\n"
+             "  return retv;\n"
+             "}\n"
+             "/* memory-access hook (gdev_mem_ops.access, PAPER.md:225-230): returns the program's R0 */\n"
+             "__device__ __forceinline__ uint64_t gx_hook_access(unsigned group, const void *addr, uint32_t size, bool is_write) {\n"
+             "  return gx_hook_event(group, (uint64_t)addr, " << 0 << "u | (is_write ? 0x10000u : 0u), size);\n"
+             "}\n"
+             "/* block-entry hook (gdev_sched_ops.enter, PAPER.md:260-262) */\n"
+             "__device__ __forceinline__ uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost) {\n"
+             "  return gx_hook_event(group, unit, 1u, cost);\n"
+             "}\n\n#line 1 \"user.cu\"\n"
+          << user << "\n";
     }
 
     /* one launch body (template on WANT_RET: write per-event R0) with S-stage ring ingest (S >= 2)
@@ -916,6 +963,12 @@ std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &
                           int block) {
     Gen g(L);
     g.kernel(images, sizes, block);
+    return g.o.str();
+}
+
+std::string gx_jit_instrument_source(const GxLaunch &L, const GxInsn *image, uint32_t n, const std::string &user) {
+    Gen g(L);
+    g.instrument(image, n, user);
     return g.o.str();
 }
 

@@ -8,6 +8,9 @@
 /* CUDA C++ source of one launch configuration (programs in launch-slot order). */
 std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images,
                           const std::vector<uint32_t> &sizes, int block);
+/* f4: CUDA C++ of the program as inline __device__ hooks (gx_hook_access / gx_hook_block_enter)
+ * followed by the user's kernels; no privatised maps (L must have none). */
+std::string gx_jit_instrument_source(const GxLaunch &L, const GxInsn *image, uint32_t n, const std::string &user);
 /* NVRTC -> sm_100a cubin.  Returns 0, or -1 with the compiler log. */
 int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string &log);
 /* preferred threads per block of the generated kernel (1024; GX_JIT_BLOCK = 256 / 512 for experiments);

@@ -1195,6 +1195,71 @@ int gx_daemon_get_stats(gx_rt *rt, gx_daemon_stats *out) {
     return 0;
 }
 
+struct gx_kernel {
+    CUmodule mod = nullptr;
+    std::string log;
+};
+
+int gx_instrument(gx_rt *rt, int prog_fd, const char *user_src, gx_kernel **out, char *log, uint64_t log_len) {
+    if (!rt || !user_src || !out) return -EINVAL;
+    *out = nullptr;
+    if (!check_prog(rt, prog_fd)) return -ENOENT;
+    LaunchCfg *cfg;
+    int rc = get_launch(rt, prog_fd, cfg);
+    if (rc) return rc;
+    Drv &d = drv();
+    if (!d.ok) return set_err(rt, -ENOSYS, "driver entry points unavailable");
+    GxLaunch h = cfg->h; /* no shared-memory privatisation inside a user kernel */
+    for (auto &m : h.maps) m.priv_off = 0xFFFFFFFFu;
+    h.n_priv = 0;
+    h.priv_bytes = 0;
+    const Prog &p = rt->progs[prog_fd];
+    std::string src = gx_jit_instrument_source(h, p.vr.image.data(), (uint32_t)p.vr.image.size(), user_src);
+    if (const char *dump = getenv("GX_JIT_DUMP")) {
+        if (FILE *f = fopen(dump, "w")) {
+            fputs(src.c_str(), f);
+            fclose(f);
+        }
+    }
+    std::vector<char> cubin;
+    std::string lg;
+    const int crc = gx_jit_compile(src, cubin, lg);
+    if (log && log_len) {
+        size_t k = std::min<size_t>(log_len - 1, lg.size());
+        memcpy(log, lg.data(), k);
+        log[k] = 0;
+    }
+    if (crc) return set_err(rt, -EINVAL, "instrumented module does not compile: %s", lg.c_str());
+    gx_kernel *k = new gx_kernel();
+    if (d.moduleLoadData(&k->mod, cubin.data()) != CUDA_SUCCESS) {
+        delete k;
+        return set_err(rt, -EFAULT, "cuModuleLoadData failed");
+    }
+    k->log = lg;
+    *out = k;
+    return 0;
+}
+
+int gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t grid[3], const uint32_t block[3],
+                     uint32_t smem, void **args, void *stream) {
+    if (!rt || !k || !name || !grid || !block) return -EINVAL;
+    CUfunction fn = nullptr;
+    if (drv().moduleGetFunction(&fn, k->mod, name) != CUDA_SUCCESS)
+        return set_err(rt, -ENOENT, "no kernel '%s' in the instrumented module", name);
+    if (drv().launchKernel(fn, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)stream, args,
+                           nullptr) != CUDA_SUCCESS)
+        return set_err(rt, -EFAULT, "instrumented kernel launch failed");
+    rt->n_launches++;
+    return 0;
+}
+
+void gx_kernel_free(gx_rt *rt, gx_kernel *k) {
+    (void)rt;
+    if (!k) return;
+    if (k->mod && drv().moduleUnload) drv().moduleUnload(k->mod);
+    delete k;
+}
+
 int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
     if (!rt || !out) return -EINVAL;
     int rc0 = sync(rt);
