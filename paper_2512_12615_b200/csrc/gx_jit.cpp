@@ -710,6 +710,7 @@ struct Gen {
      * or register ingest (S == 0) */
     void body(const std::string &fname, int S, int B, int U, bool punroll, const std::vector<const GxInsn *> &images) {
         const uint32_t priv_words = (L.priv_bytes + 3) / 4;
+        bool two_level = S < 2; /* record loop nested in a batch loop (register ingest, ring claims) */
         o << "template <bool WANT_RET>\n__device__ __forceinline__ void " << fname << "(const uint4 *__restrict__ ev, "
              "uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats) {\n";
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
@@ -736,6 +737,10 @@ struct Gen {
              * not stall the ring); the warp that reads a stage's last record (shared counter)
              * refills it with chunk c + S -- no producer warp, no empty-barrier waits. */
             const int W = B / 32;
+            int P = 2; /* records per claim (GX_JIT_CLAIM = 1, 2 or 4) */
+            if (const char *e = getenv("GX_JIT_CLAIM")) P = atoi(e);
+            if (P != 1 && P != 2 && P != 4) P = 2;
+            two_level = true;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
@@ -766,22 +771,29 @@ struct Gen {
                  "    /* claim the block's next record: warps are not tied to a slot, so a slow record\n"
                  "     * (a long program, a diverged warp) does not hold back the stage refills */\n"
                  "    uint32_t r_ = 0;\n"
-                 "    if (lane == 0) r_ = atoms_add(next_s, 1u);\n"
+                 "    if (lane == 0) r_ = atoms_add(next_s, " << P << "u);\n"
                  "    r_ = __shfl_sync(GX_ALL, r_, 0);\n"
                  "    const uint32_t c_ = r_ / " << W << "u, w_ = r_ % " << W << "u;\n"
                  "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
                  "    if (rbase >= nrec) break;\n"
-                 "    const uint64_t rec = rbase + w_;\n"
                  "    const uint32_t st = c_ % " << S << "u;\n"
                  "    mbar_wait(full_s + st * 8u, (c_ / " << S << "u) & 1u);\n"
                  "    const uint32_t ra_ = my_ring + st * " << 1024 * W << "u + w_ * 1024u;\n"
-                 "    const uint4 a = lds128(ra_), b = lds128(ra_ + 16u);\n"
+                 "    uint4 ea_[" << P << "], eb_[" << P << "];\n"
+                 "    #pragma unroll\n"
+                 "    for (int u = 0; u < " << P << "; u++) { ea_[u] = lds128(ra_ + u * 1024u); eb_[u] = lds128(ra_ + u * 1024u + 16u); }\n"
                  "    __syncwarp();\n"
-                 "    if (lane == 0 && atoms_add(used_s + st * 4u, 1u) == " << W - 1 << "u) {\n"
+                 "    if (lane == 0 && atoms_add(used_s + st * 4u, " << P << "u) == " << W - P << "u) {\n"
                  "      gx_used[st] = 0;\n"
                  "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
                  "      stage_issue(st, rbase + " << S << " * gstride);\n"
-                 "    }\n";
+                 "    }\n"
+                 "    /* " << P << " records per claim: one claim and one release atomic per " << P << " */\n"
+                 "    #pragma unroll\n"
+                 "    for (int u = 0; u < " << P << "; u++) {\n"
+                 "    const uint64_t rec = rbase + w_ + u;\n"
+                 "    if (rec >= nrec) break;\n"
+                 "    const uint4 a = ea_[u], b = eb_[u];\n";
         } else if (S >= 2) {
             /* a1 through a per-warp ring of S one-record (1 KiB) slots in dynamic shared memory:
              * record k+S-1 is in flight while record k runs.  Modes (GX_JIT_STAGE_MODE):
@@ -901,7 +913,7 @@ struct Gen {
             o << "      default: break;\n      }\n    }\n"
                  "    if (WANT_RET && valid) ret[i] = retv;\n";
         }
-        o << (S >= 2 ? "  }\n" : "    }\n  }\n");
+        o << (two_level ? "    }\n  }\n" : "  }\n");
         o << "  ptc_flush(ptc);\n"
              "  for (int s = 16; s; s >>= 1) {\n"
              "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
@@ -932,22 +944,17 @@ struct Gen {
 
 }  // namespace
 
+/* read at every compile (a compiled configuration keeps its shared-memory size in LaunchCfg) */
 int gx_jit_stages() {
-    static int s = [] {
-        int v = 3; /* profiles/r1_jit_variants.md: 3 stages of 32 KiB beat 4 and 6 (L1 carve-out) */
-        if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
-        return std::max(0, std::min(8, v));
-    }();
-    return s;
+    int v = 3; /* profiles/r1_jit_variants.md: 3 stages of 32 KiB beat 4 and 6 (L1 carve-out) */
+    if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
+    return std::max(0, std::min(8, v));
 }
 
 int gx_jit_stage_mode() {
-    static int m = [] {
-        int v = 3;
-        if (const char *e = getenv("GX_JIT_STAGE_MODE")) v = atoi(e);
-        return (v >= 0 && v <= 3) ? v : 3;
-    }();
-    return m;
+    int v = 3;
+    if (const char *e = getenv("GX_JIT_STAGE_MODE")) v = atoi(e);
+    return (v >= 0 && v <= 3) ? v : 3;
 }
 
 int gx_jit_block() {

@@ -103,6 +103,7 @@ struct LaunchCfg {
     CUfunction jfunc = nullptr;   /* gx_jit_kernel: no per-event R0 */
     CUfunction jfunc_r = nullptr; /* gx_jit_kernel_r: writes d_ret */
     CUfunction jfunc_g = nullptr, jfunc_gr = nullptr; /* register-ingest instances */
+    unsigned jsmem = 0;           /* dynamic shared bytes of the ring instances (fixed at compile) */
     bool ring_ok = true;
     uint32_t jgrid = 0, jblock = 256;
     std::string jit_log;
@@ -389,6 +390,7 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
             continue;
         }
         cfg.jmod = mod;
+        cfg.jsmem = smem;
         cfg.jfunc = fn[0];
         cfg.jfunc_r = fn[1];
         cfg.jfunc_g = fn[2];
@@ -534,7 +536,7 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         const int force = !fe ? 0 : strcmp(fe, "ring") == 0 ? 1 : strcmp(fe, "reg") == 0 ? 2 : 0;
         const bool ring = force == 1 || (force == 0 && cfg.ring_ok && n >= (1ull << 22));
         CUfunction fnl = ring ? (d_ret ? cfg.jfunc_r : cfg.jfunc) : (d_ret ? cfg.jfunc_gr : cfg.jfunc_g);
-        const unsigned smem = ring ? gx_jit_smem((int)B) : 0u;
+        const unsigned smem = ring ? cfg.jsmem : 0u;
         if ((flags & GX_RUN_OVERLAP) && drv().launchKernelEx) {
             /* programmatic dependent launch: the grid may start while the previous kernel on the
              * stream drains; it stages its first records, then griddepcontrol.wait holds every map
