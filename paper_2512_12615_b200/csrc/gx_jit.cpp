@@ -737,9 +737,12 @@ struct Gen {
              * not stall the ring); the warp that reads a stage's last record (shared counter)
              * refills it with chunk c + S -- no producer warp, no empty-barrier waits. */
             const int W = B / 32;
-            int P = 2; /* records per claim (GX_JIT_CLAIM = 1, 2 or 4) */
-            if (const char *e = getenv("GX_JIT_CLAIM")) P = atoi(e);
-            if (P != 1 && P != 2 && P != 4) P = 2;
+            /* ONE record per claim.  Stage phases are told apart by parity only, so a warp must never
+             * claim a record S or more chunks past a stage that has not been refilled: with one record
+             * per claim the W warps can at most cover one whole unloaded chunk (and then all wait on
+             * it); claiming 2 records let half the warps block a chunk while the rest ran two chunks
+             * ahead onto a stale phase (measured: corrupted ring, launch failure at 2^24 events). */
+            const int P = 1;
             two_level = true;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
