@@ -169,6 +169,24 @@ int  gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t 
                       uint32_t smem, void **args, void *cuda_stream);
 void gx_kernel_free(gx_rt *rt, gx_kernel *k);
 
+/* ---------------------------------------------------------------- block scheduling (§8f f3)
+ * The work-stealing thread-block scheduler of PAPER.md §4.3.2 ("Return whether to steal work (TB
+ * scheduler)") and §6.2.1 (persistent worker blocks pull work units; FixedWork / Greedy /
+ * LatencyBudget): n_workers persistent worker blocks, unit u initially in the deque of home[u]
+ * (unit order).  A worker pops its own deque's head: ENTER hook, cost_us[u] microseconds of work
+ * (a globaltimer spin standing for the unit's kernel body), EXIT hook; with an empty deque it runs
+ * the STEAL hook -- R0 == 0 retires the worker, otherwise it takes the tail unit of the largest
+ * deque (lowest id on ties; a CAS per attempt), spins steal_cost_us, and runs it with the stolen bit.
+ * Hook records (F-5): addr = unit (STEAL: 0), ts = %globaltimer, hook = kind
+ * (GX_HOOK_BLOCK_ENTER 1, GX_HOOK_BLOCK_EXIT 4, GX_HOOK_STEAL 5) | stolen << 16, block_id =
+ * worker, size = cost_us.  prog_fd (verified) is compiled into the worker kernel (gx_instrument).
+ * Outputs (host arrays): executed_by[n_units] (worker), stolen[n_units], busy_ns / end_ns (from
+ * the first worker's start) / steals [n_workers], *makespan_ns (device globaltimer).  Synchronous. */
+enum { GX_HOOK_BLOCK_EXIT = 4, GX_HOOK_STEAL = 5 };
+int  gx_sched_run(gx_rt *rt, int prog_fd, uint32_t n_units, const uint32_t *cost_us, const uint32_t *home,
+                  uint32_t n_workers, uint32_t steal_cost_us, uint32_t *executed_by, uint8_t *stolen,
+                  uint64_t *busy_ns, uint64_t *end_ns, uint32_t *steals, uint64_t *makespan_ns);
+
 /* ---------------------------------------------------------------- runtime daemon (§8f f2)
  * "A runtime daemon asynchronously flushes GPU-local shards to host-visible canonical map
  * instances, providing coherent snapshots to host-side policies without synchronization

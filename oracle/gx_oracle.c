@@ -837,6 +837,85 @@ ORA_EXPORT int ora_run(ora_env *e, const void *events, uint64_t n, int prog, uin
     return 0;
 }
 
+/* ------------------------------------------------------------------ f3: block scheduling
+ * The work-stealing thread-block scheduler of PAPER.md §4.3.2 ("Return whether to steal work (TB
+ * scheduler)", should_try_steal) and §6.2.1 (persistent workers pull work units; FixedWork /
+ * Greedy / LatencyBudget), as the discrete-event simulation of SPEC.md:374-424 (F-5):
+ *   every worker pops its own deque from the head: ENTER hook, cost_us of work, EXIT hook;
+ *   when its deque is empty it fires the STEAL hook: R0 == 0 -> the worker retires; else it steals
+ *   the TAIL unit of the worker with the largest deque (lowest id on ties), paying steal_cost_us,
+ *   and runs it (ENTER/EXIT with the stolen bit); no victim -> it retires.
+ * Workers advance on one simulated clock: the next step is taken by the worker with the smallest
+ * time (lowest id on ties).  Hook records: addr = unit id (STEAL: 0), ts = simulated ns,
+ * hook = kind | stolen << 16, block_id = worker, size = cost_us (STEAL: 0). */
+enum { HK_ENTER = 1, HK_EXIT = 4, HK_STEAL = 5 };
+
+static int sched_hook(ora_env *e, int prog, uint32_t kind, uint32_t stolen, uint32_t worker, uint64_t unit,
+                      uint64_t t_us, uint32_t cost, uint64_t seq, uint64_t *r0) {
+    uint8_t ctx[32] = {0};
+    const uint64_t ts = t_us * 1000;
+    const uint32_t hook = kind | (stolen << 16);
+    memcpy(ctx + 0, &unit, 8);
+    memcpy(ctx + 8, &ts, 8);
+    memcpy(ctx + 16, &hook, 4);
+    memcpy(ctx + 20, &worker, 4);
+    memcpy(ctx + 28, &cost, 4);
+    if (run_one(e, &e->progs[prog], ctx, seq, r0)) return -1;
+    e->stats[ST_RUN]++;
+    return 0;
+}
+
+ORA_EXPORT int ora_sched_run(ora_env *e, int prog, uint32_t n_units, const uint32_t *cost_us, const uint32_t *home,
+                             uint32_t n_workers, uint32_t steal_cost_us, uint32_t *executed_by, uint8_t *stolen,
+                             uint64_t *busy_us, uint64_t *end_us, uint32_t *steals, uint64_t *makespan_us) {
+    if (prog < 0 || prog >= MAX_PROGS || !e->progs[prog].used || !n_workers) return -E_INVAL;
+    uint32_t *cnt = calloc(n_workers + 1, sizeof *cnt), *off = calloc(n_workers + 1, sizeof *off);
+    uint32_t *seg = malloc((n_units + 1) * sizeof *seg), *head = calloc(n_workers, sizeof *head),
+             *tail = calloc(n_workers, sizeof *tail), *fill = calloc(n_workers, sizeof *fill);
+    uint64_t *t = calloc(n_workers, sizeof *t);
+    uint8_t *done = calloc(n_workers, 1);
+    for (uint32_t u = 0; u < n_units; u++) cnt[home[u]]++;
+    for (uint32_t w = 0; w < n_workers; w++) off[w + 1] = off[w] + cnt[w];
+    for (uint32_t u = 0; u < n_units; u++) seg[off[home[u]] + fill[home[u]]++] = u;   /* deque in unit order */
+    for (uint32_t w = 0; w < n_workers; w++) { head[w] = off[w]; tail[w] = off[w + 1]; busy_us[w] = 0; steals[w] = 0; }
+    uint64_t seq = 0;
+    int rc = 0;
+    for (;;) {
+        int w = -1;
+        for (uint32_t k = 0; k < n_workers; k++)
+            if (!done[k] && (w < 0 || t[k] < t[w])) w = (int)k;
+        if (w < 0) break;
+        uint32_t u, st = 0;
+        if (head[w] < tail[w]) {
+            u = seg[head[w]++];
+        } else {
+            uint64_t r0;
+            if (sched_hook(e, prog, HK_STEAL, 0, (uint32_t)w, 0, t[w], 0, seq++, &r0)) { rc = -1; break; }
+            if (r0 == 0) { done[w] = 1; continue; }
+            int v = -1;
+            for (uint32_t k = 0; k < n_workers; k++)
+                if (tail[k] > head[k] && (v < 0 || tail[k] - head[k] > tail[v] - head[v])) v = (int)k;
+            if (v < 0) { done[w] = 1; continue; }
+            u = seg[--tail[v]];
+            st = 1;
+            t[w] += steal_cost_us;
+            steals[w]++;
+        }
+        uint64_t r0;
+        if (sched_hook(e, prog, HK_ENTER, st, (uint32_t)w, u, t[w], cost_us[u], seq++, &r0)) { rc = -1; break; }
+        t[w] += cost_us[u];
+        busy_us[w] += cost_us[u];
+        if (sched_hook(e, prog, HK_EXIT, st, (uint32_t)w, u, t[w], cost_us[u], seq++, &r0)) { rc = -1; break; }
+        executed_by[u] = (uint32_t)w;
+        stolen[u] = (uint8_t)st;
+    }
+    uint64_t ms = 0;
+    for (uint32_t w = 0; w < n_workers; w++) { end_us[w] = t[w]; if (t[w] > ms) ms = t[w]; }
+    *makespan_us = ms;
+    free(cnt); free(off); free(seg); free(head); free(tail); free(fill); free(t); free(done);
+    return rc;
+}
+
 /* ------------------------------------------------------------------ canonical dumps (O8) */
 
 static int cmp_key_le(const uint8_t *a, const uint8_t *b, uint32_t n) {

@@ -54,6 +54,9 @@ def lib():
         L.ora_ringbuf_used.restype = u64
         L.ora_pfq_dump.argtypes = [vp, i32, p64, u64, p64, p64]
         L.ora_pfq_reset.argtypes = [vp, i32]
+        u32p = C.POINTER(C.c_uint32)
+        L.ora_sched_run.argtypes = [vp, i32, C.c_uint32, u32p, u32p, C.c_uint32, C.c_uint32, u32p,
+                                    C.POINTER(C.c_uint8), p64, p64, u32p, p64]
         L.ora_clone.argtypes = [vp]
         L.ora_clone.restype = vp
         L.ora_merge.argtypes = [vp, C.POINTER(vp), i32]
@@ -178,6 +181,27 @@ class Oracle:
 
     def prefetch_reset(self, fd):
         self.L.ora_pfq_reset(self.h, fd)
+
+    def sched_run(self, prog, cost_us, home, n_workers, steal_cost_us=0) -> dict:
+        """f3 (F-5): the work-stealing scheduler as a discrete-event simulation, the hooks
+        run by this oracle.  Returns executed_by, stolen, busy_us, end_us, steals, makespan_us."""
+        import numpy as np
+        cost = np.ascontiguousarray(cost_us, dtype=np.uint32)
+        hm = np.ascontiguousarray(home, dtype=np.uint32)
+        U = len(cost)
+        ex = np.zeros(U, dtype=np.uint32)
+        st = np.zeros(U, dtype=np.uint8)
+        busy = np.zeros(n_workers, dtype=np.uint64)
+        end = np.zeros(n_workers, dtype=np.uint64)
+        steals = np.zeros(n_workers, dtype=np.uint32)
+        ms = C.c_uint64()
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        rc = self.L.ora_sched_run(self.h, prog, U, P(cost, C.c_uint32), P(hm, C.c_uint32), n_workers, steal_cost_us,
+                                  P(ex, C.c_uint32), P(st, C.c_uint8), P(busy, C.c_uint64), P(end, C.c_uint64),
+                                  P(steals, C.c_uint32), C.byref(ms))
+        if rc:
+            raise OSError(-rc if rc < 0 else rc, "ora_sched_run: " + self.fault())
+        return dict(executed_by=ex, stolen=st, busy_us=busy, end_us=end, steals=steals, makespan_us=ms.value)
 
     def clone(self) -> "Oracle":
         c = Oracle(self.L.ora_clone(self.h))

@@ -32,7 +32,7 @@ EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_m
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply", "gx_prefetch_drain", "gx_daemon_start", "gx_daemon_stop", "gx_daemon_watch",
            "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range", "gx_instrument",
-           "gx_kernel_launch", "gx_kernel_free")
+           "gx_kernel_launch", "gx_kernel_free", "gx_sched_run")
 
 
 class gx_map_spec(C.Structure):
@@ -107,6 +107,8 @@ def lib():
         "gx_instrument": (i32, [vp, i32, C.c_char_p, C.POINTER(vp), C.c_char_p, u64]),
         "gx_kernel_launch": (i32, [vp, vp, C.c_char_p, C.POINTER(u32), C.POINTER(u32), u32, C.POINTER(vp), vp]),
         "gx_kernel_free": (None, [vp, vp]),
+        "gx_sched_run": (i32, [vp, i32, u32, C.POINTER(u32), C.POINTER(u32), u32, u32, C.POINTER(u32),
+                               C.POINTER(C.c_uint8), p64, p64, C.POINTER(u32), p64]),
         "gx_load_prog": (i32, [vp, u32, vp, u32, C.POINTER(i32)]),
         "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
         "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
@@ -371,6 +373,24 @@ def gx_kernel_launch(rt, handle, name: str, grid, block, args, smem=0, stream=No
     b = (C.c_uint32 * 3)(*(list(block) + [1, 1, 1])[:3])
     _check(lib().gx_kernel_launch(rt, handle, name.encode(), g, b, smem, argv, _stream_handle(stream)),
            "gx_kernel_launch", rt)
+
+
+def gx_sched_run(rt, prog_fd, cost_us, home, n_workers, steal_cost_us=0) -> dict:
+    """f3: the work-stealing block scheduler on the GPU with the policy prog_fd (include/gx.h)."""
+    cost = np.ascontiguousarray(cost_us, dtype=np.uint32)
+    hm = np.ascontiguousarray(home, dtype=np.uint32)
+    U = len(cost)
+    ex = np.zeros(U, dtype=np.uint32)
+    st = np.zeros(U, dtype=np.uint8)
+    busy = np.zeros(n_workers, dtype=np.uint64)
+    end = np.zeros(n_workers, dtype=np.uint64)
+    steals = np.zeros(n_workers, dtype=np.uint32)
+    ms = C.c_uint64()
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+    _check(lib().gx_sched_run(rt, prog_fd, U, P(cost, C.c_uint32), P(hm, C.c_uint32), n_workers, steal_cost_us,
+                              P(ex, C.c_uint32), P(st, C.c_uint8), P(busy, C.c_uint64), P(end, C.c_uint64),
+                              P(steals, C.c_uint32), C.byref(ms)), "gx_sched_run", rt)
+    return dict(executed_by=ex, stolen=st, busy_ns=busy, end_ns=end, steals=steals, makespan_ns=ms.value)
 
 
 def gx_kernel_free(rt, handle):

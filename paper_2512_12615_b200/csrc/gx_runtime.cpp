@@ -1255,6 +1255,144 @@ int gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t g
     return 0;
 }
 
+/* f3: the work-stealing thread-block scheduler (§4.3.2, §6.2.1; F-5) as a
+ * persistent kernel: one worker per block, lane 0 drives it and calls the policy through the
+ * inline hooks (gx_instrument).  Deques are [head, tail) index pairs packed in one u64 per worker:
+ * the owner pops the head, thieves pop the tail, each with one CAS. */
+static const char *kSchedSrc = R"CUDA(
+__device__ __forceinline__ unsigned long long gx_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void gx_spin_ns(unsigned long long ns) {
+    const unsigned long long a = gx_now();
+    while (gx_now() - a < ns) { }
+}
+extern "C" __global__ void gx_sched_worker(const unsigned *seg, const unsigned *off, unsigned long long *ht, unsigned W,
+                                           const unsigned *cost_us, unsigned steal_cost_us, unsigned *executed_by,
+                                           unsigned char *stolen, unsigned long long *busy_ns, unsigned long long *start_ns,
+                                           unsigned long long *end_ns, unsigned *steals) {
+    if (threadIdx.x != 0) return;      /* lane 0 is the worker; hooks run for the group {lane 0} */
+    const unsigned w = blockIdx.x;
+    start_ns[w] = gx_now();
+    unsigned long long busy = 0;
+    unsigned nst = 0;
+    for (;;) {
+        unsigned u = 0, st = 0;
+        bool got = false;
+        for (;;) {                     /* own deque: pop the head */
+            const unsigned long long old = *(volatile unsigned long long *)&ht[w];
+            const unsigned h = (unsigned)old, t = (unsigned)(old >> 32);
+            if (h >= t) break;
+            if (atomicCAS(&ht[w], old, (unsigned long long)(h + 1) | ((unsigned long long)t << 32)) == old) {
+                u = seg[off[w] + h];
+                got = true;
+                break;
+            }
+        }
+        if (!got) {
+            if (gx_hook_event(1u, 0ull, 5u, 0u) == 0) break;      /* should_try_steal -> no */
+            for (;;) {                 /* victim: largest deque, lowest id; take its tail */
+                int v = -1;
+                unsigned best = 0;
+                unsigned long long vold = 0;
+                for (unsigned k = 0; k < W; k++) {
+                    const unsigned long long o = *(volatile unsigned long long *)&ht[k];
+                    const unsigned len = (unsigned)(o >> 32) - (unsigned)o;
+                    if ((unsigned)(o >> 32) > (unsigned)o && len > best) { best = len; v = (int)k; vold = o; }
+                }
+                if (v < 0) break;
+                const unsigned h = (unsigned)vold, t = (unsigned)(vold >> 32);
+                if (atomicCAS(&ht[v], vold, (unsigned long long)h | ((unsigned long long)(t - 1) << 32)) == vold) {
+                    u = seg[off[v] + t - 1];
+                    got = true;
+                    break;
+                }
+            }
+            if (!got) break;
+            gx_spin_ns(1000ull * steal_cost_us);
+            st = 1;
+            nst++;
+        }
+        gx_hook_event(1u, (unsigned long long)u, 1u | (st << 16), cost_us[u]);
+        const unsigned long long a = gx_now();
+        gx_spin_ns(1000ull * cost_us[u]);
+        busy += gx_now() - a;
+        gx_hook_event(1u, (unsigned long long)u, 4u | (st << 16), cost_us[u]);
+        executed_by[u] = w;
+        stolen[u] = (unsigned char)st;
+    }
+    busy_ns[w] = busy;
+    steals[w] = nst;
+    end_ns[w] = gx_now();
+}
+)CUDA";
+
+int gx_sched_run(gx_rt *rt, int prog_fd, uint32_t n_units, const uint32_t *cost_us, const uint32_t *home, uint32_t n_workers,
+                 uint32_t steal_cost_us, uint32_t *executed_by, uint8_t *stolen, uint64_t *busy_ns, uint64_t *end_ns,
+                 uint32_t *steals, uint64_t *makespan_ns) {
+    if (!rt || !cost_us || !home || !n_workers || !n_units || !executed_by || !stolen || !busy_ns || !end_ns || !steals ||
+        !makespan_ns)
+        return -EINVAL;
+    for (uint32_t u = 0; u < n_units; u++)
+        if (home[u] >= n_workers) return set_err(rt, -EINVAL, "unit %u homed on worker %u >= %u", u, home[u], n_workers);
+    gx_kernel *k = nullptr;
+    int rc = gx_instrument(rt, prog_fd, kSchedSrc, &k, nullptr, 0);
+    if (rc) return rc;
+    std::vector<uint32_t> off(n_workers + 1, 0), seg(n_units), fill(n_workers, 0);
+    for (uint32_t u = 0; u < n_units; u++) off[home[u] + 1]++;
+    for (uint32_t w = 0; w < n_workers; w++) off[w + 1] += off[w];
+    for (uint32_t u = 0; u < n_units; u++) seg[off[home[u]] + fill[home[u]]++] = u; /* deque in unit order */
+    std::vector<unsigned long long> ht(n_workers);
+    for (uint32_t w = 0; w < n_workers; w++) ht[w] = (unsigned long long)(off[w + 1] - off[w]) << 32;
+    uint32_t *d_seg, *d_off, *d_cost, *d_exec, *d_steals;
+    unsigned long long *d_ht, *d_busy, *d_start, *d_end;
+    uint8_t *d_stolen;
+    CK(cudaMalloc(&d_seg, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_off, 4ull * (n_workers + 1)), "sched");
+    CK(cudaMalloc(&d_cost, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_exec, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_stolen, n_units), "sched");
+    CK(cudaMalloc(&d_steals, 4ull * n_workers), "sched");
+    CK(cudaMalloc(&d_ht, 8ull * n_workers), "sched");
+    CK(cudaMalloc(&d_busy, 8ull * n_workers), "sched");
+    CK(cudaMalloc(&d_start, 8ull * n_workers), "sched");
+    CK(cudaMalloc(&d_end, 8ull * n_workers), "sched");
+    CK(cudaMemcpy(d_seg, seg.data(), 4ull * n_units, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_off, off.data(), 4ull * (n_workers + 1), cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_cost, cost_us, 4ull * n_units, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_ht, ht.data(), 8ull * n_workers, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemset(d_exec, 0xFF, 4ull * n_units), "sched");
+    CK(cudaMemset(d_stolen, 0, n_units), "sched");
+    uint32_t W = n_workers;
+    void *args[] = {&d_seg, &d_off, &d_ht, &W, &d_cost, &steal_cost_us, &d_exec, &d_stolen, &d_busy, &d_start, &d_end, &d_steals};
+    const uint32_t grid[3] = {n_workers, 1, 1}, block[3] = {32, 1, 1};
+    rc = gx_kernel_launch(rt, k, "gx_sched_worker", grid, block, 0, args, nullptr);
+    if (!rc) {
+        CK(cudaDeviceSynchronize(), "sched run");
+        std::vector<unsigned long long> st(n_workers), en(n_workers), bu(n_workers);
+        CK(cudaMemcpy(executed_by, d_exec, 4ull * n_units, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(stolen, d_stolen, n_units, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(steals, d_steals, 4ull * n_workers, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(st.data(), d_start, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(en.data(), d_end, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(bu.data(), d_busy, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
+        const unsigned long long t0 = *std::min_element(st.begin(), st.end());
+        unsigned long long t1 = 0;
+        for (uint32_t w = 0; w < n_workers; w++) {
+            busy_ns[w] = bu[w];
+            end_ns[w] = en[w] - t0;
+            t1 = std::max(t1, en[w]);
+        }
+        *makespan_ns = t1 - t0;
+    }
+    cudaFree(d_seg); cudaFree(d_off); cudaFree(d_cost); cudaFree(d_exec); cudaFree(d_stolen); cudaFree(d_steals);
+    cudaFree(d_ht); cudaFree(d_busy); cudaFree(d_start); cudaFree(d_end);
+    gx_kernel_free(rt, k);
+    return rc;
+}
+
 void gx_kernel_free(gx_rt *rt, gx_kernel *k) {
     (void)rt;
     if (!k) return;
