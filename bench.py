@@ -318,6 +318,7 @@ def main():
             extra_lines(rt, args)
             f2_lines()
             f4_lines()
+            f3_lines()
     if world > 1:
         dist.destroy_process_group()
 
@@ -538,6 +539,31 @@ def f4_lines():
                       "added_ns_per_hook": (res[1] - res[0]) * 1e6 / hooks_per_launch,
                       "counter_total_ok": total == 13 * hooks_per_launch}), file=sys.stderr, flush=True)
     rt.close()
+
+
+def f3_lines():
+    """the work-stealing block scheduler on 148 persistent workers
+    (§6.2.1 / Fig 4 shape) -- makespan per policy and workload, next to the discrete-event
+    oracle's prediction for the same units (the oracle here is the model, not a baseline)."""
+    import paper_2512_12615_b200 as gx
+    from gxin import sched
+    from oracle.oracle import Oracle
+    W = 148
+    for kind in ("moderate", "heavy"):
+        cost, home = sched.workload(kind, W)
+        budget = int(cost.sum() / W * 0.2)
+        line = {"f3": kind, "workers": W, "units": len(cost), "work_us": int(cost.sum())}
+        for policy in ("fixed", "greedy", "latency_budget"):
+            rt = gx.Runtime(0)
+            prog, fds = sched.setup(rt, policy, W, budget_us=budget)
+            r = gx.gx_sched_run(rt.rt, prog, cost, home, W, 2)
+            env = Oracle()
+            oprog, _ = sched.setup(env, policy, W, budget_us=budget)
+            o = env.sched_run(oprog, cost, home, W, 2)
+            line[policy] = {"makespan_us": r["makespan_ns"] / 1e3, "steals": int(r["steals"].sum()),
+                            "oracle_makespan_us": o["makespan_us"]}
+            rt.close()
+        print(json.dumps(line), file=sys.stderr, flush=True)
 
 
 if __name__ == "__main__":

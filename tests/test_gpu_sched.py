@@ -21,7 +21,7 @@ def _gpu(policy, cost, home, budget=0, steal_cost=2):
     return r, rt, fds
 
 
-def test_fixedwork_matches_oracle():
+def test_fixedwork_matches_oracle(gpu):
     cost, home = sched.workload("moderate", W)
     r, rt, fds = _gpu("fixed", cost, home)
     env = Oracle()
@@ -38,7 +38,7 @@ def test_fixedwork_matches_oracle():
 
 @pytest.mark.parametrize("kind", ["moderate", "heavy"])
 @pytest.mark.parametrize("policy", ["greedy", "latency_budget"])
-def test_stealing_is_valid(kind, policy):
+def test_stealing_is_valid(gpu, kind, policy):
     cost, home = sched.workload(kind, W)
     budget = int(cost.sum() / W * 0.2)
     r, rt, fds = _gpu(policy, cost, home, budget=budget)
@@ -54,7 +54,7 @@ def test_stealing_is_valid(kind, policy):
         assert (rt.array_u64(fds["stolen_us"]) == stolen_work).all()
 
 
-def test_greedy_beats_fixedwork_under_moderate_imbalance():
+def test_greedy_beats_fixedwork_under_moderate_imbalance(gpu):
     """"both Greedy and LatencyBudget reduce latency" under moderate imbalance (the
     DES oracle predicts the same direction for this workload)."""
     cost, home = sched.workload("moderate", W)
