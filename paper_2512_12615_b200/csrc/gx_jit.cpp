@@ -744,10 +744,17 @@ struct Gen {
              * ahead onto a stale phase (measured: corrupted ring, launch failure at 2^24 events). */
             const int P = 1;
             two_level = true;
+            /* stage release: atom (default: a shared counter, the last reader refills the stage) or
+             * GX_JIT_RING_RELEASE=mbar (every warp arrives on the stage's "empty" mbarrier -- no
+             * returning atomic; the first claimant of chunk c waits for chunk c-1 to be read and
+             * issues chunk c+S-1).  Measured equal on C2/C3/C5/C6 (profiles/r1_jit_variants.md). */
+            const bool mbar_rel = getenv("GX_JIT_RING_RELEASE") && strcmp(getenv("GX_JIT_RING_RELEASE"), "mbar") == 0;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
                  "  __shared__ uint32_t gx_next;\n"
+                 "  __shared__ __align__(8) uint64_t gx_empty[" << S << "];\n"
+                 "  const uint32_t empty_s = (uint32_t)__cvta_generic_to_shared(gx_empty);\n"
                  "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(gx_ring);\n"
                  "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
                  "  const uint32_t wid = threadIdx.x >> 5;\n"
@@ -759,7 +766,7 @@ struct Gen {
                  "    bulk_load(ring_s + st * " << 1024 * W << "u, ev + r0_ * 64, bytes_, full_s + st * 8u, pol);\n"
                  "  };\n"
                  "  if (threadIdx.x == 0) {\n"
-                 "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); gx_used[k] = 0; }\n"
+                 "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); mbar_init(empty_s + k * 8u, " << W << "); gx_used[k] = 0; }\n"
                  "    gx_next = 0;\n"
                  "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
                  "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k * gstride + (uint64_t)blockIdx.x * " << W << ");\n"
@@ -780,17 +787,28 @@ struct Gen {
                  "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
                  "    if (rbase >= nrec) break;\n"
                  "    const uint32_t st = c_ % " << S << "u;\n"
+              << (mbar_rel ?
+                 "    if (w_ == 0 && c_ >= 1) {                /* first claimant of chunk c: issue chunk c+S-1 */\n"
+                 "      const uint32_t c2 = c_ + " + std::to_string(S - 1) + "u, st2 = c2 % " + std::to_string(S) + "u;\n"
+                 "      if (lane == 0) {\n"
+                 "        mbar_wait(empty_s + st2 * 8u, ((c2 / " + std::to_string(S) + "u) - 1u) & 1u);   /* chunk c-1 read */\n"
+                 "        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+                 "        stage_issue(st2, (uint64_t)c2 * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ");\n"
+                 "      }\n"
+                 "    }\n" : "") <<
                  "    mbar_wait(full_s + st * 8u, (c_ / " << S << "u) & 1u);\n"
                  "    const uint32_t ra_ = my_ring + st * " << 1024 * W << "u + w_ * 1024u;\n"
                  "    uint4 ea_[" << P << "], eb_[" << P << "];\n"
                  "    #pragma unroll\n"
                  "    for (int u = 0; u < " << P << "; u++) { ea_[u] = lds128(ra_ + u * 1024u); eb_[u] = lds128(ra_ + u * 1024u + 16u); }\n"
                  "    __syncwarp();\n"
-                 "    if (lane == 0 && atoms_add(used_s + st * 4u, " << P << "u) == " << W - P << "u) {\n"
+              << (mbar_rel ?
+                 "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(empty_s + st * 8u) : \"memory\");\n" :
+                 "    if (lane == 0 && atoms_add(used_s + st * 4u, 1u) == " + std::to_string(W - 1) + "u) {\n"
                  "      gx_used[st] = 0;\n"
                  "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-                 "      stage_issue(st, rbase + " << S << " * gstride);\n"
-                 "    }\n"
+                 "      stage_issue(st, rbase + " + std::to_string(S) + " * gstride);\n"
+                 "    }\n") <<
                  "    /* " << P << " records per claim: one claim and one release atomic per " << P << " */\n"
                  "    #pragma unroll\n"
                  "    for (int u = 0; u < " << P << "; u++) {\n"
