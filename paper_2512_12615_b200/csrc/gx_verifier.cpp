@@ -406,6 +406,10 @@ struct Slot {
     uint8_t init = 0;   /* bit k: byte k initialised */
     bool spill = false; /* a full 8-byte register spill */
     Reg reg;
+    /* 4-byte scalar stores (e.g. a map key written with stxw): bit h = half h holds a value known
+     * to be <= nmax[h].  Lets a lookup with a provably in-range key return a non-NULL pointer. */
+    uint8_t nok = 0;
+    uint64_t nmax[2] = {0, 0};
 };
 
 struct State {
@@ -457,6 +461,8 @@ bool state_in(const State &a, const State &b) {
         } else if (y.spill && y.reg.type != SCALAR) {
             return false; /* old read these bytes as plain bytes; a pointer there would leak */
         }
+        for (int h = 0; h < 2; h++) /* an old bound must still hold */
+            if (((x.nok >> h) & 1) && (!((y.nok >> h) & 1) || y.nmax[h] > x.nmax[h])) return false;
     }
     return true;
 }
@@ -465,8 +471,10 @@ bool state_eq(const State &a, const State &b) {
         if (!reg_eq(a.r[i], b.r[i])) return false;
     for (int k = 0; k < GX_STACK_SIZE / 8; k++) {
         const Slot &x = a.s[k], &y = b.s[k];
-        if (x.init != y.init || x.spill != y.spill) return false;
+        if (x.init != y.init || x.spill != y.spill || x.nok != y.nok) return false;
         if (x.spill && !reg_eq(x.reg, y.reg)) return false;
+        for (int h = 0; h < 2; h++)
+            if (((x.nok >> h) & 1) && x.nmax[h] != y.nmax[h]) return false;
     }
     return true;
 }
@@ -483,6 +491,7 @@ struct Fact {
     MemKind key_kind = MK_NONE, val_kind = MK_NONE;
     int32_t key_addr = 0, val_addr = 0;
     int64_t rb_size = -1, rb_flags = -1;
+    uint8_t br = 0;              /* conditional jumps: 1 = taken on some path, 2 = fell through on some path */
 };
 
 struct Checkpoint {
@@ -855,6 +864,21 @@ struct Verifier {
         return fail(pc, GX_BAD_HELPER, msg);
     }
 
+    /* upper bound of the u32 key at stack byte address ka (0..511), if one is known */
+    static bool key_bound(const State &st, int32_t ka, uint64_t &kmax) {
+        if (ka < 0 || ka + 4 > GX_STACK_SIZE || ka % 4) return false;
+        const Slot &s = st.s[ka / 8];
+        const int h = (ka % 8) / 4;
+        if (s.spill) {
+            if (is_ptr(s.reg) || s.reg.var.umax > 0xFFFFFFFFull) return false;
+            kmax = h == 0 ? s.reg.var.umax : 0;
+            return true;
+        }
+        if (!((s.nok >> h) & 1)) return false;
+        kmax = s.nmax[h];
+        return true;
+    }
+
     bool record_call(uint32_t pc, int map, MemKind kk, int32_t ka, MemKind vk, int32_t va, int64_t rbs, int64_t rbf) {
         Fact &f = facts[pc];
         if (!f.seen) {
@@ -881,12 +905,27 @@ struct Verifier {
             s.spill = true;
             s.reg = *val;
             s.init = 0xFF;
+            s.nok = 0;
             return;
         }
         uint8_t bits = (uint8_t)(((1u << size) - 1) << (x % 8));
         if (s.spill && is_ptr(s.reg)) s.init = 0;  /* the rest of a clobbered pointer is garbage */
+        if (s.spill && !is_ptr(s.reg) && s.reg.var.umax <= 0xFFFFFFFFull) {
+            /* the untouched half of a small spilled scalar keeps its bound */
+            s.nok = 3;
+            s.nmax[0] = s.reg.var.umax;
+            s.nmax[1] = 0;
+        } else if (s.spill) {
+            s.nok = 0;
+        }
         s.spill = false;
         s.init |= bits;
+        const int h0 = (int)(x % 8) / 4, h1 = (int)((x % 8) + size - 1) / 4;
+        for (int h = h0; h <= h1; h++) s.nok &= (uint8_t)~(1u << h);
+        if (size == 4 && x % 4 == 0 && val && val->type == SCALAR && val->var.umax <= 0xFFFFFFFFull) {
+            s.nok |= (uint8_t)(1u << h0);
+            s.nmax[h0] = val->var.umax;
+        }
     }
 
     Reg stack_read(State &st, int64_t a, uint32_t size, bool sx, uint32_t pc, bool &ok) {
@@ -914,6 +953,8 @@ struct Verifier {
                 return reg_scalar(sc_const(v));
             }
         }
+        if (!sx && size == 4 && x % 4 == 0 && !s.spill && ((s.nok >> ((x % 8) / 4)) & 1))
+            return reg_scalar(sc_urange(0, s.nmax[(x % 8) / 4]));
         if (sx) {
             Scalar r = sc_unknown();
             r.smin = -(int64_t)(1ull << (8 * size - 1));
@@ -1074,7 +1115,7 @@ struct Verifier {
             if (k == MK_STACK) {
                 Reg v = val;
                 if (size < 8 && v.type == SCALAR) v.var = sc_unknown();
-                stack_write(st, sa - GX_STACK_SIZE, size, size == 8 ? &v : nullptr);
+                stack_write(st, sa - GX_STACK_SIZE, size, size == 8 ? &v : &val); /* narrow: bound only */
             } else if (map >= 0) {
                 out.use[map].used = out.use[map].writes = out.use[map].non_add_write = true;
             }
@@ -1097,6 +1138,7 @@ struct Verifier {
                 if (s.spill) {
                     s.spill = false; /* value now unknown */
                 }
+                s.nok = 0;
             } else if (map >= 0) {
                 GxMapUse &u = out.use[map];
                 u.used = u.writes = true;
@@ -1132,7 +1174,20 @@ struct Verifier {
         }
         if (op == 0x80) return call(P) ? 0 : -1;
 
-        /* conditional */
+        /* conditional: every outcome seen on some path is recorded (facts[pc].br) so the pre-decoder
+         * can drop a branch the verifier proved one-sided on all paths (e.g. the NULL test after a
+         * lookup whose key is provably in range) */
+        int rc = cond_branch(P, pc, r, D, S, x, cls, pending);
+        if (rc == 0) {
+            const uint32_t tgt = pc + 1 + r.off;
+            if (P.pc == tgt) facts[pc].br |= 1;
+            if (P.pc == pc + 1) facts[pc].br |= 2;
+        }
+        return rc;
+    }
+
+    int cond_branch(Path &P, uint32_t pc, const Raw &r, Reg &D, Reg &S, bool x, uint32_t cls, std::vector<Path> &pending) {
+        const uint32_t op = r.code & 0xF0;
         bool is64 = cls == CL_JMP;
         if (D.type == NOT_INIT || (x && S.type == NOT_INIT)) return fail(pc, GX_UNINIT_READ, "comparison of an uninitialised register") ? 0 : -1;
         uint32_t tgt = pc + 1 + r.off;
@@ -1165,6 +1220,7 @@ struct Verifier {
                 mark(other.st, taken_is_null);
                 other.pc = tgt;
                 push_branch(other, pending);
+                facts[pc].br |= other.pc == tgt ? 1 : 2;
                 return 0;
             }
             /* non-null pointer vs 0: JEQ never taken, JNE always */
@@ -1185,6 +1241,7 @@ struct Verifier {
                 other.pc = tgt;
                 P.pc = pc + 1;
                 push_branch(other, pending);
+                facts[pc].br |= other.pc == tgt ? 1 : 2;
                 return 0;
             }
         }
@@ -1204,6 +1261,7 @@ struct Verifier {
         P.pc = pc + 1;
         if (okT && okF) {
             push_branch(other, pending);
+                facts[pc].br |= other.pc == tgt ? 1 : 2;
             return 0;
         }
         if (okT) {
@@ -1423,6 +1481,12 @@ struct Verifier {
             r0.id = next_id++;
             r0.off = 0;
             r0.var = sc_const(0);
+            /* an ARRAY lookup whose key is provably below max_entries cannot return NULL */
+            uint64_t kmax = 0;
+            if (mi.type == ARRAY && kk == MK_STACK && key_bound(st, ka, kmax) && kmax < mi.max_entries) {
+                r0.type = PTR_MAPV;
+                r0.id = 0;
+            }
         } else {
             Scalar s = sc_unknown();
             s.smin = -4095;
@@ -1752,6 +1816,9 @@ struct Verifier {
                     g.aux = (uint16_t)(i + 1 + r.off);
                     g.imm = is64 ? (uint64_t)(int64_t)r.imm : (uint64_t)(uint32_t)r.imm;
                     if (hint_uniform.size() == n && hint_uniform[i]) g.flags |= GXF_UNIFORM;
+                    /* one-sided on every explored path: an unconditional jump (no ballot, no split) */
+                    if (f.br == 1) g.op = GX_JA, g.flags = 0, g.imm = 0;
+                    else if (f.br == 2) g.op = GX_JA, g.aux = (uint16_t)(i + 1), g.flags = 0, g.imm = 0;
                 }
             } else if (cls == CL_LDX) {
                 uint32_t sz = size_of(r.code);

@@ -28,6 +28,10 @@ ACCEPT = {
     "const0": "mov64 r0, 0\nexit",
     "ctx_all_fields": "ldxdw r0, [r1+0]\nldxdw r2, [r1+8]\nldxw r3, [r1+16]\nldxh r4, [r1+24]\nldxb r5, [r1+27]\nexit",
     "lookup_nullcheck": LOOKUP + "jeq r0, 0, +1\nldxdw r0, [r0+0]\nexit",
+    # an ARRAY key provably below max_entries (constant, or masked) cannot miss: no NULL check needed
+    "lookup_key_in_range": LOOKUP + "ldxdw r0, [r0+0]\nexit",
+    "lookup_masked_key_in_range": LOOKUP.replace("stw [r10-4], 1", "ldxw r2, [r1+0]\nand64 r2, 15\nstxw [r10-4], r2")
+                                  + "ldxdw r0, [r0+0]\nexit",
     "bounded_loop_counter": "mov64 r0, 0\nmov64 r6, 8\nl: add64 r0, 1\nsub64 r6, 1\njne r6, 0, l\nexit",
     "stack_spill_fill_ptr": LOOKUP + "stxdw [r10-16], r0\nldxdw r1, [r10-16]\njeq r1, 0, +1\nldxdw r0, [r1+0]\nmov64 r0, 0\nexit",
     "var_offset_in_bounds": "ldxdw r2, [r1+0]\nand64 r2, 0xf8\nlddw r1, mapval:g+0\nadd64 r1, r2\nldxdw r0, [r1+0]\nexit",
@@ -58,7 +62,12 @@ REJECT = {
     "oob_stack": ("stdw [r10+0], 1\nmov64 r0, 0\nexit", False, "OOB_ACCESS"),
     "oob_stack_deep": ("stdw [r10-520], 1\nmov64 r0, 0\nexit", False, "OOB_ACCESS"),
     "oob_map_value": (LOOKUP + "jeq r0, 0, +1\nldxdw r0, [r0+8]\nmov64 r0, 0\nexit", False, "OOB_ACCESS"),
-    "null_deref": (LOOKUP + "ldxdw r0, [r0+0]\nexit", False, "NULL_DEREF"),
+    "null_deref": (LOOKUP.replace("stw [r10-4], 1", "ldxw r2, [r1+0]\nstxw [r10-4], r2") + "ldxdw r0, [r0+0]\nexit",
+                   False, "NULL_DEREF"),
+    "null_deref_key_out_of_range": (LOOKUP.replace("stw [r10-4], 1", "stw [r10-4], 16") + "ldxdw r0, [r0+0]\nexit",
+                                    False, "NULL_DEREF"),
+    "null_deref_key_range_too_wide": (LOOKUP.replace("stw [r10-4], 1", "ldxw r2, [r1+0]\nand64 r2, 31\nstxw [r10-4], r2")
+                                      + "ldxdw r0, [r0+0]\nexit", False, "NULL_DEREF"),
     "misaligned": ("ldxdw r0, [r1+4]\nexit", False, "MISALIGNED"),
     "var_offset_misaligned": ("ldxdw r2, [r1+0]\nand64 r2, 0xfc\nlddw r1, mapval:g+0\nadd64 r1, r2\nldxdw r0, [r1+0]\nexit", False, "MISALIGNED"),
     "var_offset_oob": ("ldxdw r2, [r1+0]\nand64 r2, 0xff8\nlddw r1, mapval:g+0\nadd64 r1, r2\nldxdw r0, [r1+0]\nexit", False, "OOB_ACCESS"),
