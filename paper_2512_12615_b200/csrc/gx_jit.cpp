@@ -749,6 +749,10 @@ struct Gen {
              * returning atomic; the first claimant of chunk c waits for chunk c-1 to be read and
              * issues chunk c+S-1).  Measured equal on C2/C3/C5/C6 (profiles/r1_jit_variants.md). */
             const bool mbar_rel = getenv("GX_JIT_RING_RELEASE") && strcmp(getenv("GX_JIT_RING_RELEASE"), "mbar") == 0;
+            /* record assignment: dynamic (default: claimed from a shared counter) or GX_JIT_RING_CLAIM=
+             * static (warp w runs record w of every chunk; no claim atomic, stage/phase advanced
+             * incrementally -- but the ring then waits on its slowest warp) */
+            const bool stat = getenv("GX_JIT_RING_CLAIM") && strcmp(getenv("GX_JIT_RING_CLAIM"), "static") == 0;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
@@ -776,17 +780,25 @@ struct Gen {
                  "  const uint32_t my_ring = ring_s + lane * 32u;\n"
                  "  const uint32_t used_s = (uint32_t)__cvta_generic_to_shared(gx_used);\n"
                  "  const uint32_t next_s = (uint32_t)__cvta_generic_to_shared(&gx_next);\n"
+                 "  uint32_t st_s = 0, ph_s = 0;\n  (void)st_s; (void)ph_s;\n"
                  "  #pragma unroll 1\n"
+              << (stat ?
+                 "  for (uint32_t c_ = 0;; c_++) {\n"
+                 "    const uint32_t w_ = wid;\n"
+                 "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ";\n"
+                 "    if (rbase >= nrec) break;\n"
+                 "    const uint32_t st = st_s, ph_c = ph_s;\n"
+                 "    if (++st_s == " + std::to_string(S) + "u) { st_s = 0; ph_s ^= 1u; }\n" :
                  "  for (;;) {\n"
                  "    /* claim the block's next record: warps are not tied to a slot, so a slow record\n"
                  "     * (a long program, a diverged warp) does not hold back the stage refills */\n"
                  "    uint32_t r_ = 0;\n"
-                 "    if (lane == 0) r_ = atoms_add(next_s, " << P << "u);\n"
+                 "    if (lane == 0) r_ = atoms_add(next_s, " + std::to_string(P) + "u);\n"
                  "    r_ = __shfl_sync(GX_ALL, r_, 0);\n"
-                 "    const uint32_t c_ = r_ / " << W << "u, w_ = r_ % " << W << "u;\n"
-                 "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " << W << ";\n"
+                 "    const uint32_t c_ = r_ / " + std::to_string(W) + "u, w_ = r_ % " + std::to_string(W) + "u;\n"
+                 "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ";\n"
                  "    if (rbase >= nrec) break;\n"
-                 "    const uint32_t st = c_ % " << S << "u;\n"
+                 "    const uint32_t st = c_ % " + std::to_string(S) + "u, ph_c = (c_ / " + std::to_string(S) + "u) & 1u;\n")
               << (mbar_rel ?
                  "    if (w_ == 0 && c_ >= 1) {                /* first claimant of chunk c: issue chunk c+S-1 */\n"
                  "      const uint32_t c2 = c_ + " + std::to_string(S - 1) + "u, st2 = c2 % " + std::to_string(S) + "u;\n"
@@ -796,7 +808,7 @@ struct Gen {
                  "        stage_issue(st2, (uint64_t)c2 * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ");\n"
                  "      }\n"
                  "    }\n" : "") <<
-                 "    mbar_wait(full_s + st * 8u, (c_ / " << S << "u) & 1u);\n"
+                 "    mbar_wait(full_s + st * 8u, ph_c);\n"
                  "    const uint32_t ra_ = my_ring + st * " << 1024 * W << "u + w_ * 1024u;\n"
                  "    uint4 ea_[" << P << "], eb_[" << P << "];\n"
                  "    #pragma unroll\n"

@@ -286,16 +286,19 @@ def test_overlapped_batches_parity(gpu, config, engine):
     assert rt.stats()["events_run"] + rt.stats()["events_skipped"] >= 0
 
 
-@pytest.mark.parametrize("mode,stages,release", [(0, 3, "atom"), (1, 2, "atom"), (2, 4, "atom"), (3, 4, "atom"),
-                                                (3, 3, "mbar")])
+@pytest.mark.parametrize("mode,stages,release,claim", [(0, 3, "atom", "dynamic"), (1, 2, "atom", "dynamic"),
+                                                      (2, 4, "atom", "dynamic"), (3, 4, "atom", "dynamic"),
+                                                      (3, 3, "mbar", "dynamic"), (3, 3, "atom", "static"),
+                                                      (3, 3, "mbar", "static")])
 @pytest.mark.parametrize("config", ["C2", "C3", "C5"])
-def test_ingest_variants_parity(gpu, config, mode, stages, release, monkeypatch):
+def test_ingest_variants_parity(gpu, config, mode, stages, release, claim, monkeypatch):
     """The alternative event-ingest variants kept for measurement (profiles/r1_jit_variants.md:
     per-lane / coalesced cp.async rings, per-warp TMA ring, deeper block ring) give the oracle's
     results too (ragged tail included)."""
     monkeypatch.setenv("GX_JIT_STAGE_MODE", str(mode))
     monkeypatch.setenv("GX_JIT_STAGES", str(stages))
     monkeypatch.setenv("GX_JIT_RING_RELEASE", release)
+    monkeypatch.setenv("GX_JIT_RING_CLAIM", claim)
     n = (1 << 17) + 21
     ev = configs.events(config, configs.SEEDS[config], n)
     rt, s, st = _compare(config, ev, threshold=2 if config == "C3" else None, engine="jit_ring")
