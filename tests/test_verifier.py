@@ -168,3 +168,24 @@ def test_jit_compiles_offline(name):
         pytest.skip(log)
     assert rc == 0, log
     assert "gx_jit_kernel" in src
+
+
+@pytest.mark.parametrize("knobs,progs", [
+    ({"GX_JIT_STAGE_MODE": "0", "GX_JIT_STAGES": "3"}, ("P2",)), ({"GX_JIT_STAGE_MODE": "1", "GX_JIT_STAGES": "2"}, ("P2",)),
+    ({"GX_JIT_STAGE_MODE": "2", "GX_JIT_STAGES": "4"}, ("P2",)), ({"GX_JIT_RING_RELEASE": "mbar"}, ("P2",)),
+    ({"GX_JIT_RING_CLAIM": "static", "GX_JIT_RING_RELEASE": "mbar"}, ("P2",)), ({"GX_JIT_PTCACHE": "1"}, ("P2",)),
+    ({"GX_JIT_IFCONV": "0"}, ("P4",)), ({"GX_JIT_HASH_L1PROBE": "0"}, ("P3",)), ({"GX_JIT_BLOCK": "256"}, ("P6",))])
+def test_jit_variants_compile_offline(knobs, progs, monkeypatch):
+    """Every JIT code-generation variant kept for measurement (profiles/r1_jit_variants.md) still
+    generates valid sm_100a code for a program that exercises it (P2 per-thread, P3 hash+ringbuf,
+    P4 loop, P6 prefetch)."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    for name in progs:
+        specs = programs.maps_of(name)
+        fds = {k: i for i, k in enumerate(specs)}
+        maps = {fds[k]: (s.type, s.key_size, s.value_size, s.max_entries) for k, s in specs.items()}
+        rc, src, log = gx.gx_jit_offline(programs.build(name, fds), maps)
+        if rc == -38:
+            pytest.skip(log)
+        assert rc == 0, (name, knobs, log[-2000:])
