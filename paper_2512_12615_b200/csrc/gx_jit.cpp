@@ -749,10 +749,12 @@ struct Gen {
              * returning atomic; the first claimant of chunk c waits for chunk c-1 to be read and
              * issues chunk c+S-1).  Measured equal on C2/C3/C5/C6 (profiles/r1_jit_variants.md). */
             const bool mbar_rel = getenv("GX_JIT_RING_RELEASE") && strcmp(getenv("GX_JIT_RING_RELEASE"), "mbar") == 0;
-            /* record assignment: dynamic (default: claimed from a shared counter) or GX_JIT_RING_CLAIM=
-             * static (warp w runs record w of every chunk; no claim atomic, stage/phase advanced
-             * incrementally -- but the ring then waits on its slowest warp) */
-            const bool stat = getenv("GX_JIT_RING_CLAIM") && strcmp(getenv("GX_JIT_RING_CLAIM"), "static") == 0;
+            /* record assignment: static (default: warp w runs record w of every chunk; no claim atomic,
+             * stage/phase advanced incrementally) or GX_JIT_RING_CLAIM=dynamic (claimed from a shared
+             * counter, so one slow warp does not hold back the refills).  Static measured faster on
+             * C2/C3/C5/C6 (profiles/r1_jit_variants.md §7); ALU-heavy loop programs take the
+             * register-ingest body anyway. */
+            const bool stat = !getenv("GX_JIT_RING_CLAIM") || strcmp(getenv("GX_JIT_RING_CLAIM"), "dynamic") != 0;
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
