@@ -35,7 +35,7 @@ EVENT_BYTES = 32
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C2")
     p.add_argument("--events", type=int, default=0, help="events per GPU (default: the config's size)")
@@ -77,27 +77,36 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                f = [x.strip() for x in out.stdout.strip().split(",")]
+        """one nvidia-smi in loop mode (-lms 20) for the whole region: a sample every ~20 ms"""
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "20"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            for line in self._p.stdout:
+                f = [x.strip() for x in line.strip().split(",")]
                 if len(f) >= 7:
                     self.samples.append(f)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+                if self._stop.is_set():
+                    break
+        except Exception:
+            pass
 
     def __enter__(self):
+        self._p = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.3)   # let the first sample land before the timed region starts
         return self
 
     def __exit__(self, *a):
+        time.sleep(0.05)
         self._stop.set()
+        if self._p is not None:
+            self._p.terminate()
         self._t.join(timeout=6)
 
     def summary(self):
