@@ -552,11 +552,10 @@ def f4_lines():
 
 def f3_lines():
     """the work-stealing block scheduler on 148 persistent workers
-    (§6.2.1 / Fig 4 shape) -- makespan per policy and workload, next to the discrete-event
-    oracle's prediction for the same units (the oracle here is the model, not a baseline)."""
+    (§6.2.1 / Fig 4 shape) -- makespan per policy and workload.  (The discrete-event
+    model's makespans for the same units are test-side: tests/test_oracle_sched.py.)"""
     import paper_2512_12615_b200 as gx
     from gxin import sched
-    from oracle.oracle import Oracle
     W = 148
     for kind in ("moderate", "heavy"):
         cost, home = sched.workload(kind, W)
@@ -566,11 +565,7 @@ def f3_lines():
             rt = gx.Runtime(0)
             prog, fds = sched.setup(rt, policy, W, budget_us=budget)
             r = gx.gx_sched_run(rt.rt, prog, cost, home, W, 2)
-            env = Oracle()
-            oprog, _ = sched.setup(env, policy, W, budget_us=budget)
-            o = env.sched_run(oprog, cost, home, W, 2)
-            line[policy] = {"makespan_us": r["makespan_ns"] / 1e3, "steals": int(r["steals"].sum()),
-                            "oracle_makespan_us": o["makespan_us"]}
+            line[policy] = {"makespan_us": r["makespan_ns"] / 1e3, "steals": int(r["steals"].sum())}
             rt.close()
         print(json.dumps(line), file=sys.stderr, flush=True)
 
