@@ -722,7 +722,7 @@ struct Gen {
              "  const uint32_t shard = blockIdx.x * " << B << " + threadIdx.x;\n"
              "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
              "  PtCache ptc;\n"
-             "  const uint64_t nrec = (n + 31) >> 5;\n"
+             "  const uint64_t nrec = (n + 31) >> 5, nfull = n >> 5; /* records, whole records */\n"
              "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
              "  const uint64_t pol = evict_first_policy();\n"
              "  /* PDL (gx_run_batch_ex GX_RUN_OVERLAP): let the next batch's grid be scheduled; no-ops\n"
@@ -742,7 +742,6 @@ struct Gen {
              * per claim the W warps can at most cover one whole unloaded chunk (and then all wait on
              * it); claiming 2 records let half the warps block a chunk while the rest ran two chunks
              * ahead onto a stale phase (measured: corrupted ring, launch failure at 2^24 events). */
-            const int P = 1;
             two_level = true;
             /* stage release: atom (default: a shared counter, the last reader refills the stage) or
              * GX_JIT_RING_RELEASE=mbar (every warp arrives on the stage's "empty" mbarrier -- no
@@ -755,6 +754,10 @@ struct Gen {
              * C2/C3/C5/C6 (profiles/r1_jit_variants.md §7); ALU-heavy loop programs take the
              * register-ingest body anyway. */
             const bool stat = !getenv("GX_JIT_RING_CLAIM") || strcmp(getenv("GX_JIT_RING_CLAIM"), "dynamic") != 0;
+            /* static assignment may give each warp P consecutive records of a (W x P)-record stage
+             * (GX_JIT_RING_RPW): bigger bulk copies, the same number of streams per SM */
+            const int P = stat ? gx_jit_ring_rpw() : 1;
+            const int CW = W * P; /* records per chunk (one stage) */
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
@@ -764,18 +767,18 @@ struct Gen {
                  "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(gx_ring);\n"
                  "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
                  "  const uint32_t wid = threadIdx.x >> 5;\n"
-                 "  const uint64_t gstride = (uint64_t)gridDim.x * " << W << ";\n"
+                 "  const uint64_t gstride = (uint64_t)gridDim.x * " << CW << ";\n"
                  "  auto stage_issue = [&](uint32_t st, uint64_t r0_) {\n"
                  "    if (r0_ >= nrec) return;\n"
                  "    const uint64_t left_ = n - r0_ * 32;\n"
-                 "    const uint32_t bytes_ = left_ >= " << 32 * W << "ull ? " << 1024 * W << "u : (uint32_t)left_ * 32u;\n"
-                 "    bulk_load(ring_s + st * " << 1024 * W << "u, ev + r0_ * 64, bytes_, full_s + st * 8u, pol);\n"
+                 "    const uint32_t bytes_ = left_ >= " << 32 * CW << "ull ? " << 1024 * CW << "u : (uint32_t)left_ * 32u;\n"
+                 "    bulk_load(ring_s + st * " << 1024 * CW << "u, ev + r0_ * 64, bytes_, full_s + st * 8u, pol);\n"
                  "  };\n"
                  "  if (threadIdx.x == 0) {\n"
                  "    for (int k = 0; k < " << S << "; k++) { mbar_init(full_s + k * 8u, 1); mbar_init(empty_s + k * 8u, " << W << "); gx_used[k] = 0; }\n"
                  "    gx_next = 0;\n"
                  "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
-                 "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k * gstride + (uint64_t)blockIdx.x * " << W << ");\n"
+                 "    for (int k = 0; k < " << S << "; k++) stage_issue(k, k * gstride + (uint64_t)blockIdx.x * " << CW << ");\n"
                  "  }\n"
                  "  __syncthreads();\n"
               << pdl_wait <<
@@ -783,11 +786,13 @@ struct Gen {
                  "  const uint32_t used_s = (uint32_t)__cvta_generic_to_shared(gx_used);\n"
                  "  const uint32_t next_s = (uint32_t)__cvta_generic_to_shared(&gx_next);\n"
                  "  uint32_t st_s = 0, ph_s = 0;\n  (void)st_s; (void)ph_s;\n"
+                 "  uint64_t rbase_s = (uint64_t)blockIdx.x * " << CW << ";\n  (void)rbase_s;\n"
                  "  #pragma unroll 1\n"
               << (stat ?
                  "  for (uint32_t c_ = 0;; c_++) {\n"
                  "    const uint32_t w_ = wid;\n"
-                 "    const uint64_t rbase = (uint64_t)c_ * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ";\n"
+                 "    const uint64_t rbase = rbase_s;\n"
+                 "    rbase_s += gstride;\n"
                  "    if (rbase >= nrec) break;\n"
                  "    const uint32_t st = st_s, ph_c = ph_s;\n"
                  "    if (++st_s == " + std::to_string(S) + "u) { st_s = 0; ph_s ^= 1u; }\n" :
@@ -807,11 +812,11 @@ struct Gen {
                  "      if (lane == 0) {\n"
                  "        mbar_wait(empty_s + st2 * 8u, ((c2 / " + std::to_string(S) + "u) - 1u) & 1u);   /* chunk c-1 read */\n"
                  "        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-                 "        stage_issue(st2, (uint64_t)c2 * gstride + (uint64_t)blockIdx.x * " + std::to_string(W) + ");\n"
+                 "        stage_issue(st2, (uint64_t)c2 * gstride + (uint64_t)blockIdx.x * " + std::to_string(CW) + ");\n"
                  "      }\n"
                  "    }\n" : "") <<
                  "    mbar_wait(full_s + st * 8u, ph_c);\n"
-                 "    const uint32_t ra_ = my_ring + st * " << 1024 * W << "u + w_ * 1024u;\n"
+                 "    const uint32_t ra_ = my_ring + st * " << 1024 * CW << "u + w_ * " << 1024 * P << "u;\n"
                  "    uint4 ea_[" << P << "], eb_[" << P << "];\n"
                  "    #pragma unroll\n"
                  "    for (int u = 0; u < " << P << "; u++) { ea_[u] = lds128(ra_ + u * 1024u); eb_[u] = lds128(ra_ + u * 1024u + 16u); }\n"
@@ -826,7 +831,7 @@ struct Gen {
                  "    /* " << P << " records per claim: one claim and one release atomic per " << P << " */\n"
                  "    #pragma unroll\n"
                  "    for (int u = 0; u < " << P << "; u++) {\n"
-                 "    const uint64_t rec = rbase + w_ + u;\n"
+                 "    const uint64_t rec = rbase + w_ * " << P << " + u;\n"
                  "    if (rec >= nrec) break;\n"
                  "    const uint4 a = ea_[u], b = eb_[u];\n";
         } else if (S >= 2) {
@@ -919,7 +924,7 @@ struct Gen {
             /* one program for every event.  A whole record (the warp-uniform test rec*32+32 <= n) runs
              * the whole-warp instance; a ragged tail record runs the masked one.  The run count (= n)
              * is added once at the end instead of per event. */
-            o << "    if (rec * 32 + 32 <= n) {\n"
+            o << "    if (rec < nfull) {\n"
                  "      prog0<true>(c, GX_ALL, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
                  "      if (WANT_RET) ret[i] = retv;\n"
                  "    } else {\n"
@@ -981,9 +986,19 @@ struct Gen {
 
 /* read at every compile (a compiled configuration keeps its shared-memory size in LaunchCfg) */
 int gx_jit_stages() {
-    int v = 3; /* profiles/r1_jit_variants.md: 3 stages of 32 KiB beat 4 and 6 (L1 carve-out) */
+    int v = 2; /* profiles/r1_jit_variants.md §9: 2 stages of 32 KiB beat 3 (-5 % on C2), 4 and 6 */
     if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
     return std::max(0, std::min(8, v));
+}
+
+int gx_jit_ring_rpw() {
+    int v = 1;
+    if (const char *e = getenv("GX_JIT_RING_RPW")) v = atoi(e);
+    if (getenv("GX_JIT_RING_CLAIM") && strcmp(getenv("GX_JIT_RING_CLAIM"), "dynamic") == 0) v = 1;
+    v = std::max(1, std::min(4, v));
+    const int st = gx_jit_stages() >= 2 ? gx_jit_stages() : 3;
+    while (v > 1 && st * v * (gx_jit_block() / 32) > 200) v--; /* the ring stays within 200 KiB of SMEM */
+    return v;
 }
 
 int gx_jit_stage_mode() {

@@ -16,14 +16,17 @@ int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string
 /* preferred threads per block of the generated kernel (1024; GX_JIT_BLOCK = 256 / 512 for experiments);
  * the runtime falls back to 256 only when a 1024-thread block cannot be resident */
 int gx_jit_block();
-/* depth of the shared-memory event ring (cp.async / TMA staging, a1): 3 by default
+/* depth of the shared-memory event ring (cp.async / TMA staging, a1): 2 by default
  * (GX_JIT_STAGES; < 2 = register loads, GX_JIT_UNROLL records per iteration).  Dynamic shared memory per block =
  * gx_jit_smem(block) bytes. */
 int gx_jit_stages();
 /* staging mode: 0 per-lane cp.async, 1 coalesced cp.async, 2 per-warp TMA bulk, 3 block-wide TMA bulk
  * (default: one 32-KiB cp.async.bulk per block stage) */
 int gx_jit_stage_mode();
+/* records per warp per ring stage with static record assignment (GX_JIT_RING_RPW, 1 by default; a
+ * stage then holds (block/32) x rpw records, brought in by one bulk copy) */
+int gx_jit_ring_rpw();
 inline unsigned gx_jit_smem(int block) {
     const int s = gx_jit_stages();
-    return (unsigned)(block / 32) * (unsigned)(s >= 2 ? s : 3) * 1024u; /* the ring instances' stages */
+    return (unsigned)(block / 32) * (unsigned)(s >= 2 ? s : 3) * (unsigned)gx_jit_ring_rpw() * 1024u; /* the ring stages */
 }

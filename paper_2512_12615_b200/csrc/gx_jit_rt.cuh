@@ -415,9 +415,16 @@ __device__ __forceinline__ uint64_t group_add_const(unsigned mask, uint64_t addr
 template <uint32_t K, uint32_t W>
 __device__ __forceinline__ uint8_t *pt_phys_c(uint64_t data, uint64_t logical, uint32_t shard) {
     const uint32_t lo = (uint32_t)(logical - data);
+    const uint32_t l = shard & 31, q = shard >> 5;
+    if constexpr (((K * W) & (K * W - 1)) == 0) {
+        /* K x W a power of two: ((k - r) mod K) * W + w == (wi - r W) mod K W, so the rotated word
+         * offset is one subtract and one mask of the byte offset (r W 8 and the base hoist out) */
+        const uint32_t t = (lo - (l & (K - 1)) * (W * 8)) & (K * W * 8 - 1);
+        const uint64_t base = data + ((uint64_t)q * (K * W * 32) + l) * 8;
+        return reinterpret_cast<uint8_t *>(base + (uint64_t)(((t & ~7u) << 5) | (t & 7u)));
+    }
     const uint32_t wi = lo >> 3;
     const uint32_t k = wi / W, w = wi % W;
-    const uint32_t l = shard & 31, q = shard >> 5;
     const uint32_t r = l % K;
     const uint32_t kk = (K & (K - 1)) == 0 ? ((k - r) & (K - 1)) : (k >= r ? k - r : k + K - r);
     const uint64_t base = data + ((uint64_t)q * (K * W * 32) + l) * 8;

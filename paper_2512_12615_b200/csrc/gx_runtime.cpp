@@ -379,6 +379,14 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         for (int k = 0; k < 2; k++)
             if (d.funcSetAttribute(fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
                 return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
+        /* shared-memory carve-out preference (GX_JIT_CARVEOUT percent; -1 = the driver's choice): a
+         * hint -- the driver still picks a configuration that fits the ring -- so 0 asks for the
+         * smallest carve-out, leaving the rest of the SM's 256 KiB to L1 */
+        if (const char *e = getenv("GX_JIT_CARVEOUT")) {
+            const int pct = atoi(e);
+            if (pct >= 0 && pct <= 100)
+                for (int k = 0; k < 4; k++) d.funcSetAttribute(fn[k], CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, pct);
+        }
         int bps = 2048 / B; /* per-thread shards: at most 2048 resident threads per SM */
         for (int k = 0; k < 4; k++) {
             int b = 0;

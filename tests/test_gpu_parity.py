@@ -286,12 +286,13 @@ def test_overlapped_batches_parity(gpu, config, engine):
     assert rt.stats()["events_run"] + rt.stats()["events_skipped"] >= 0
 
 
-@pytest.mark.parametrize("mode,stages,release,claim", [(0, 3, "atom", "dynamic"), (1, 2, "atom", "dynamic"),
-                                                      (2, 4, "atom", "dynamic"), (3, 4, "atom", "dynamic"),
-                                                      (3, 3, "mbar", "dynamic"), (3, 3, "atom", "static"),
-                                                      (3, 3, "mbar", "static")])
+@pytest.mark.parametrize("mode,stages,release,claim,rpw", [
+    (0, 3, "atom", "dynamic", 1), (1, 2, "atom", "dynamic", 1), (2, 4, "atom", "dynamic", 1),
+    (3, 4, "atom", "dynamic", 1), (3, 3, "mbar", "dynamic", 1), (3, 3, "atom", "static", 1),
+    (3, 3, "mbar", "static", 1), (3, 3, "atom", "static", 2), (3, 2, "atom", "static", 3),
+    (3, 2, "atom", "static", 1)])
 @pytest.mark.parametrize("config", ["C2", "C3", "C5"])
-def test_ingest_variants_parity(gpu, config, mode, stages, release, claim, monkeypatch):
+def test_ingest_variants_parity(gpu, config, mode, stages, release, claim, rpw, monkeypatch):
     """The alternative event-ingest variants kept for measurement (profiles/r1_jit_variants.md:
     per-lane / coalesced cp.async rings, per-warp TMA ring, deeper block ring) give the oracle's
     results too (ragged tail included)."""
@@ -299,6 +300,7 @@ def test_ingest_variants_parity(gpu, config, mode, stages, release, claim, monke
     monkeypatch.setenv("GX_JIT_STAGES", str(stages))
     monkeypatch.setenv("GX_JIT_RING_RELEASE", release)
     monkeypatch.setenv("GX_JIT_RING_CLAIM", claim)
+    monkeypatch.setenv("GX_JIT_RING_RPW", str(rpw))
     n = (1 << 17) + 21
     ev = configs.events(config, configs.SEEDS[config], n)
     rt, s, st = _compare(config, ev, threshold=2 if config == "C3" else None, engine="jit_ring")
