@@ -32,8 +32,10 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
     return r;
 }
+/* HASH probes through L1 (keys are immutable once published): 0 never, 1 the home slot, 2 the whole
+ * chain (default) */
 #ifndef GX_HASH_L1PROBE
-#define GX_HASH_L1PROBE 1
+#define GX_HASH_L1PROBE 2
 #endif
 __device__ __forceinline__ uint64_t ld_ca(const uint64_t *p) {
     uint64_t r;
@@ -74,21 +76,38 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
     /* one slot per probe step: a 4-wide step (keys of 4 slots per round trip) measured 1.7x slower
      * on C3 -- 4x the L2 requests, and the neighbours of hot slots are under atomic traffic */
     uint64_t h = mix64(key) & m.cap_mask;
-#if GX_HASH_L1PROBE
-    /* a slot's key word never changes once published (no deletes), so a key MATCH read through L1
-     * is always right; only a miss (EMPTY or another key, possibly stale) needs the coherent chain.
-     * Repeated keys -- the hot pages of C3's decode trace -- then probe in L1, not at their L2 slice. */
+#if GX_HASH_L1PROBE == 1
+    /* home slot only through L1 (a key match there is final), then the coherent chain */
     {
         uint64_t *s = slots + 2 * h;
         if (ld_ca(s) == key) return s + 1;
     }
-#endif
     for (uint64_t i = 0; i < cap; i++) {
         uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
         uint64_t k = ld_relaxed(s);
         if (k == key) return s + 1;
         if (k == GX_HASH_EMPTY) return nullptr;
     }
+#elif GX_HASH_L1PROBE
+    /* a slot's key word never changes once published (no deletes), so any NON-EMPTY key read through
+     * L1 is final -- a match is the entry, another key means probe on; only an EMPTY read may be
+     * stale and is re-read coherently at L2.  Chains over hot keys (C3's decode trace) then walk in
+     * L1 instead of at their L2 slices. */
+    for (uint64_t i = 0; i < cap; i++) {
+        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+        uint64_t k = ld_ca(s);
+        if (k == GX_HASH_EMPTY) k = ld_relaxed(s);
+        if (k == key) return s + 1;
+        if (k == GX_HASH_EMPTY) return nullptr;
+    }
+#else
+    for (uint64_t i = 0; i < cap; i++) {
+        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+        uint64_t k = ld_relaxed(s);
+        if (k == key) return s + 1;
+        if (k == GX_HASH_EMPTY) return nullptr;
+    }
+#endif
     return nullptr;
 }
 
