@@ -19,6 +19,39 @@ VARIANTS = {
     "red": HEAD + "    mov64 r1, 1\n    atomic_add64 [r0+0], r1\nout:\n    mov64 r0, 0\n    exit\n",
     "fetch": HEAD + "    mov64 r1, 1\n    atomic_fetch_add64 [r0+0], r1\n    mov64 r0, r1\n    exit\nout:\n    mov64 r0, 0\n    exit\n",
     "page_only": "ldxdw r0, [r1+0]\nrsh64 r0, 12\nexit",
+    # the same probe, the FETCH-ADD on a per-page counter in a separate ARRAY (another cache line than
+    # the key): what the key/value line sharing costs
+    "fetch_array": HEAD + """    mov64 r2, r6
+    and64 r2, 1048575
+    stxw [r10-12], r2
+    lddw r1, map:cnt
+    mov64 r2, r10
+    add64 r2, -12
+    call 1
+    jeq r0, 0, out
+    mov64 r1, 1
+    atomic_fetch_add64 [r0+0], r1
+    mov64 r0, r1
+    exit
+out:
+    mov64 r0, 0
+    exit
+""",
+    "array_only": """    ldxdw r6, [r1+0]
+    rsh64 r6, 12
+    and64 r6, 1048575
+    stxw [r10-12], r6
+    lddw r1, map:cnt
+    mov64 r2, r10
+    add64 r2, -12
+    call 1
+    jeq r0, 0, out
+    mov64 r1, 1
+    atomic_fetch_add64 [r0+0], r1
+    mov64 r0, r1
+out:
+    exit
+""",
 }
 n = 1 << int(sys.argv[1] if len(sys.argv) > 1 else 28)
 ONLY = sys.argv[2].split(",") if len(sys.argv) > 2 else None
@@ -28,6 +61,7 @@ for name, text in VARIANTS.items():
         continue
     rt = gx.Runtime(0, engine=gx.GX_ENGINE_JIT)
     fds = {k: rt.create_map(s.type, s.key_size, s.value_size, s.max_entries) for k, s in programs.P3_MAPS.items()}
+    fds["cnt"] = rt.create_map(programs.ARRAY, 4, 8, 1 << 20)
     fd = rt.load_prog(asm.assemble(text, fds))
     for _ in range(3):
         rt.run(ev, fd)
