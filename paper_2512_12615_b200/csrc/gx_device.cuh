@@ -37,6 +37,11 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
 #ifndef GX_HASH_L1PROBE
 #define GX_HASH_L1PROBE 2
 #endif
+__device__ __forceinline__ uint64_t ld_nc(const uint64_t *p) {
+    uint64_t r;
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint64_t ld_ca(const uint64_t *p) {
     uint64_t r;
     asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(r) : "l"(p));
@@ -95,7 +100,11 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
      * L1 instead of at their L2 slices. */
     for (uint64_t i = 0; i < cap; i++) {
         uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+#if GX_HASH_L1PROBE == 3
+        uint64_t k = ld_nc(s); /* read-only path: a stale EMPTY is re-read below like any other */
+#else
         uint64_t k = ld_ca(s);
+#endif
         if (k == GX_HASH_EMPTY) k = ld_relaxed(s);
         if (k == key) return s + 1;
         if (k == GX_HASH_EMPTY) return nullptr;

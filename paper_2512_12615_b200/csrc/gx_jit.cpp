@@ -220,6 +220,8 @@ struct Gen {
     std::ostringstream *out_ = nullptr;
     bool dmode_ = false; /* emitting the min-PC (diverged) copy of a block */
     bool ifconv_on_ = true; /* GX_JIT_IFCONV=0: off */
+    int hc_map_ = -1;    /* HASH map with the shared-memory key -> slot cache (GX_JIT_HASH_CACHE entries) */
+    uint32_t hc_n_ = 0;
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
     void me(const std::string &x) { (*out_) << "  { " << x << " }\n"; }
@@ -463,8 +465,12 @@ struct Gen {
                                       ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
                                       : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
-                st("{ const uint64_t k_ = " + key + "; r0 = (uint64_t)gxd::hash_lookup_coop(" + md(g.aux) + ", k_, true, " +
-                   M() + "); }");
+                if ((int)g.aux == hc_map_)
+                    st("{ const uint64_t k_ = " + key + "; r0 = (uint64_t)hash_lookup_cached<" + std::to_string(hc_n_) + "u>(" +
+                       md(g.aux) + ", k_, " + M() + ", gx_hc); }");
+                else
+                    st("{ const uint64_t k_ = " + key + "; r0 = (uint64_t)gxd::hash_lookup_coop(" + md(g.aux) + ", k_, true, " +
+                       M() + "); }");
             } else {
                 const std::string key = (g.flags & GXF_KEY_MAPV)
                                             ? "*(const uint32_t *)r2"
@@ -645,6 +651,22 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
+        /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot
+         * cache (GX_JIT_HASH_CACHE entries, a power of two; 0 = off) */
+        {
+            uint32_t ncache = 2048;
+            if (const char *e = getenv("GX_JIT_HASH_CACHE")) ncache = (uint32_t)atoi(e);
+            if (ncache & (ncache - 1)) ncache = 0;
+            hc_map_ = -1;
+            hc_n_ = std::min<uint32_t>(ncache, 2048); /* 32 KiB of static shared memory at most (48-KiB static limit) */
+            for (size_t q = 0; q < images.size() && hc_n_ && hc_map_ < 0; q++)
+                for (uint32_t i = 0; i < sizes[q]; i++)
+                    if (images[q][i].op == GX_CALL_LOOKUP_HASH && L.maps[images[q][i].aux].value_size == 8) {
+                        hc_map_ = images[q][i].aux;
+                        break;
+                    }
+            if (hc_map_ >= 0) o << "__shared__ __align__(16) unsigned long long gx_hc[" << 2 * hc_n_ << "];\n\n";
+        }
         for (size_t q = 0; q < images.size(); q++) program((int)q, images[q], sizes[q]);
         /* two launch bodies: event ingest through the block-wide TMA ring (large batches of light
          * programs) and through per-lane register loads (small batches, ALU-heavy programs) --
@@ -716,6 +738,8 @@ struct Gen {
         o << "  __shared__ uint32_t spriv[" << (priv_words ? priv_words : 1) << "];\n"
              "  __shared__ unsigned long long sstats[8];\n"
              "  for (uint32_t k = threadIdx.x; k < " << priv_words << "u; k += " << B << ") spriv[k] = 0;\n"
+          << (hc_map_ >= 0 ? "  for (uint32_t k = threadIdx.x; k < " + std::to_string(hc_n_) + "u; k += " + std::to_string(B) +
+                                 ") gx_hc[2 * k] = GX_HASH_EMPTY;\n" : std::string()) <<
              "  if (threadIdx.x < 8) sstats[threadIdx.x] = 0;\n"
              "  __syncthreads();\n"
              "  const uint32_t lane = threadIdx.x & 31;\n"

@@ -306,12 +306,15 @@ def test_ingest_variants_parity(gpu, config, mode, stages, release, claim, rpw, 
     rt, s, st = _compare(config, ev, threshold=2 if config == "C3" else None, engine="jit_ring")
 
 
-@pytest.mark.parametrize("probe", ["0", "1", "2"])
+@pytest.mark.parametrize("probe,cache", [("0", "0"), ("1", "0"), ("2", "0"), ("2", "2048"), ("2", "16"), ("1", "2048")])
 @pytest.mark.parametrize("config,engine", [("C3", "jit_ring"), ("C3", "jit"), ("C5", "jit_ring")])
-def test_hash_probe_variants_parity(gpu, config, engine, probe, monkeypatch):
+def test_hash_probe_variants_parity(gpu, config, engine, probe, cache, monkeypatch):
     """HASH probes through L1 (GX_JIT_HASH_L1PROBE: none / home slot / whole chain; keys never change
-    once published, so a non-EMPTY key read through L1 is final) give the oracle's results."""
+    once published, so a non-EMPTY key read through L1 is final) and the per-block shared-memory
+    key -> slot cache (GX_JIT_HASH_CACHE entries; 16 forces constant entry collisions) give the
+    oracle's results."""
     monkeypatch.setenv("GX_JIT_HASH_L1PROBE", probe)
+    monkeypatch.setenv("GX_JIT_HASH_CACHE", cache)
     n = (1 << 17) + 5
     ev = configs.events(config, configs.SEEDS[config], n)
     _compare(config, ev, threshold=2 if config == "C3" else None, engine=engine)
