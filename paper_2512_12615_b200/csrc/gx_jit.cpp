@@ -650,6 +650,7 @@ struct Gen {
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
+        if (const char *e = getenv("GX_JIT_PIN")) o << "#define GX_PIN " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot
          * cache (GX_JIT_HASH_CACHE entries, a power of two; 0 = off) */
@@ -787,9 +788,9 @@ struct Gen {
                  "  __shared__ uint32_t gx_used[" << S << "];\n"
                  "  __shared__ uint32_t gx_next;\n"
                  "  __shared__ __align__(8) uint64_t gx_empty[" << S << "];\n"
-                 "  const uint32_t empty_s = (uint32_t)__cvta_generic_to_shared(gx_empty);\n"
-                 "  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(gx_ring);\n"
-                 "  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(gx_full);\n"
+                 "  const uint32_t empty_s = pin32((uint32_t)__cvta_generic_to_shared(gx_empty));\n"
+                 "  const uint32_t ring_s = pin32((uint32_t)__cvta_generic_to_shared(gx_ring));\n"
+                 "  const uint32_t full_s = pin32((uint32_t)__cvta_generic_to_shared(gx_full));\n"
                  "  const uint32_t wid = threadIdx.x >> 5;\n"
                  "  const uint64_t gstride = (uint64_t)gridDim.x * " << CW << ";\n"
                  "  auto stage_issue = [&](uint32_t st, uint64_t r0_) {\n"
@@ -806,8 +807,8 @@ struct Gen {
                  "  }\n"
                  "  __syncthreads();\n"
               << pdl_wait <<
-                 "  const uint32_t my_ring = ring_s + lane * 32u;\n"
-                 "  const uint32_t used_s = (uint32_t)__cvta_generic_to_shared(gx_used);\n"
+                 "  const uint32_t my_ring = pin32(ring_s + lane * 32u);\n"
+                 "  const uint32_t used_s = pin32((uint32_t)__cvta_generic_to_shared(gx_used));\n"
                  "  const uint32_t next_s = (uint32_t)__cvta_generic_to_shared(&gx_next);\n"
                  "  uint32_t st_s = 0, ph_s = 0;\n  (void)st_s; (void)ph_s;\n"
                  "  uint64_t rbase_s = (uint64_t)blockIdx.x * " << CW << ";\n  (void)rbase_s;\n"

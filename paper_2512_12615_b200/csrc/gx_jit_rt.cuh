@@ -489,6 +489,18 @@ __device__ __forceinline__ int64_t group_ringbuf(unsigned mask, const GxMapDesc 
     return ok ? 0 : -(int64_t)gxd::E_AGAIN;
 }
 
+/* an opaque copy: keeps a loop-invariant shared-memory address in a register (NVRTC otherwise
+ * rematerialises __cvta_generic_to_shared -- an S2R of the CTA id -- in every ring iteration) */
+#ifndef GX_PIN
+#define GX_PIN 1
+#endif
+__device__ __forceinline__ uint32_t pin32(uint32_t v) {
+#if GX_PIN
+    asm volatile("mov.b32 %0, %1;" : "=r"(v) : "r"(v));
+#endif
+    return v;
+}
+
 /* ---- per-block key -> slot cache for one HASH map (8-B values) in shared memory.  A published key
  * never moves and never changes (no deletes), so a cached {key, slot index} stays right for the whole
  * launch.  Entries are write-once per launch: EMPTY -> RESV (a shared CAS) -> index stored -> key
