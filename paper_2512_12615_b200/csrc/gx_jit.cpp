@@ -435,7 +435,7 @@ struct Gen {
                 me("const uint64_t la_ = " + s + " + (int64_t)" + std::to_string(g.off) + "; " + d + " = " +
                    ld_fix("ptc_ld(ptc, la_, " + ptp((int)g.imm, "la_") + ", " + std::to_string(lg) + ")") + ";");
             else
-                me(d + " = " + ld_fix("gload<false>((uint64_t)" + ptp((int)g.imm, s + " + (int64_t)" + std::to_string(g.off)) + ", " +
+                me(d + " = " + ld_fix("ptload((uint64_t)" + ptp((int)g.imm, s + " + (int64_t)" + std::to_string(g.off)) + ", " +
                                       std::to_string(lg) + ")") + ";");
             break;
         case GX_ST_STACK: {
@@ -453,7 +453,7 @@ struct Gen {
             if (ptc_)
                 me("const uint64_t la_ = " + d + " + (int64_t)" + std::to_string(g.off) + "; ptc_st(ptc, la_, " + ptp(g.aux >> 4, "la_") + ", " + std::to_string(lg) + ", " + v + ");");
             else
-                me("gstore((uint64_t)" + ptp(g.aux >> 4, d + " + (int64_t)" + std::to_string(g.off)) + ", " + std::to_string(lg) +
+                me("ptstore((uint64_t)" + ptp(g.aux >> 4, d + " + (int64_t)" + std::to_string(g.off)) + ", " + std::to_string(lg) +
                    ", " + v + ");");
             break;
         }
@@ -651,6 +651,7 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PIN")) o << "#define GX_PIN " << atoi(e) << "\n";
+        if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot
          * cache (GX_JIT_HASH_CACHE entries, a power of two; 0 = off) */

@@ -145,6 +145,30 @@ __device__ __forceinline__ void gstore(uint64_t a, unsigned lg, uint64_t v) {
     }
 }
 
+/* per-thread word access (a5) with an optional L1 eviction-priority hint (GX_JIT_PT_HINT: 0 none,
+ * 1 ld/st L1::evict_last, 2 st L1::no_allocate) -- a measurement knob (profiles/r1_jit_variants.md) */
+#ifndef GX_PT_HINT
+#define GX_PT_HINT 0
+#endif
+__device__ __forceinline__ uint64_t ptload(uint64_t a, unsigned lg) {
+#if GX_PT_HINT == 1
+    if (lg == 3) {
+        uint64_t r;
+        asm volatile("ld.global.L1::evict_last.u64 %0, [%1];" : "=l"(r) : "l"(a) : "memory");
+        return r;
+    }
+#endif
+    return gload<false>(a, lg);
+}
+__device__ __forceinline__ void ptstore(uint64_t a, unsigned lg, uint64_t v) {
+#if GX_PT_HINT == 1
+    if (lg == 3) { asm volatile("st.global.L1::evict_last.u64 [%0], %1;" :: "l"(a), "l"(v) : "memory"); return; }
+#elif GX_PT_HINT == 2
+    if (lg == 3) { asm volatile("st.global.L1::no_allocate.u64 [%0], %1;" :: "l"(a), "l"(v) : "memory"); return; }
+#endif
+    gstore(a, lg, v);
+}
+
 /* plain RMW of a private word (stack slot or per-thread shard): returns old, stores new */
 __device__ __forceinline__ uint64_t rmw_word(uint64_t &w, unsigned byte, bool w32, uint32_t op, uint64_t s, uint64_t r0) {
     const uint64_t old = w32 ? (w >> (8 * byte)) & 0xFFFFFFFFull : w;

@@ -318,3 +318,13 @@ def test_hash_probe_variants_parity(gpu, config, engine, probe, cache, monkeypat
     n = (1 << 17) + 5
     ev = configs.events(config, configs.SEEDS[config], n)
     _compare(config, ev, threshold=2 if config == "C3" else None, engine=engine)
+
+
+@pytest.mark.parametrize("hint", ["0", "1", "2"])
+@pytest.mark.parametrize("config", ["C2", "C5"])
+def test_pt_hint_variants_parity(gpu, config, hint, monkeypatch):
+    """Per-thread word accesses with L1 eviction-priority hints (GX_JIT_PT_HINT) give the oracle's
+    results."""
+    monkeypatch.setenv("GX_JIT_PT_HINT", hint)
+    n = (1 << 17) + 9
+    _compare(config, configs.events(config, configs.SEEDS[config], n), engine="jit_ring")

@@ -175,7 +175,7 @@ def test_jit_compiles_offline(name):
     ({"GX_JIT_STAGE_MODE": "2", "GX_JIT_STAGES": "4"}, ("P2",)), ({"GX_JIT_RING_RELEASE": "mbar"}, ("P2",)),
     ({"GX_JIT_RING_CLAIM": "static", "GX_JIT_RING_RELEASE": "mbar"}, ("P2",)), ({"GX_JIT_PTCACHE": "1"}, ("P2",)),
     ({"GX_JIT_RING_RPW": "2"}, ("P2", "P3")),
-    ({"GX_JIT_IFCONV": "0"}, ("P4",)), ({"GX_JIT_HASH_L1PROBE": "0"}, ("P3",)), ({"GX_JIT_HASH_L1PROBE": "1"}, ("P3",)), ({"GX_JIT_HASH_CACHE": "0"}, ("P3",)), ({"GX_JIT_PIN": "0"}, ("P2",)), ({"GX_JIT_BLOCK": "256"}, ("P6",))])
+    ({"GX_JIT_IFCONV": "0"}, ("P4",)), ({"GX_JIT_HASH_L1PROBE": "0"}, ("P3",)), ({"GX_JIT_HASH_L1PROBE": "1"}, ("P3",)), ({"GX_JIT_HASH_CACHE": "0"}, ("P3",)), ({"GX_JIT_PIN": "0"}, ("P2",)), ({"GX_JIT_PT_HINT": "1"}, ("P2",)), ({"GX_JIT_PT_HINT": "2"}, ("P2",)), ({"GX_JIT_BLOCK": "256"}, ("P6",))])
 def test_jit_variants_compile_offline(knobs, progs, monkeypatch):
     """Every JIT code-generation variant kept for measurement (profiles/r1_jit_variants.md) still
     generates valid sm_100a code for a program that exercises it (P2 per-thread, P3 hash+ringbuf,
