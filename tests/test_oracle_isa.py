@@ -201,3 +201,21 @@ def test_oracle_faults_on_unsafe_programs(text, why):
     p = env.load_prog(asm.assemble(text))
     with pytest.raises(OracleFault, match=why):
         env.run(gen.records(1), p)
+
+
+def test_atomic_and_memsx_mnemonic_encodings():
+    """The assembler's atomic / MEMSX mnemonics emit the bpf.h encodings the hand-encoded pins use
+    (bpf.h:23 BPF_ATOMIC 0xc0, :49-51 BPF_FETCH 0x01 / BPF_XCHG 0xe1 / BPF_CMPXCHG 0xf1,
+    bpf_common.h:31-48 BPF_ADD 0x00 / BPF_OR 0x40 / BPF_AND 0x50 / BPF_XOR 0xa0; MEMSX 0x80)."""
+    cases = {
+        "atomic_add64 [r10-8], r4": "db 4a f8 ff 00 00 00 00",
+        "atomic_fetch_or64 [r10-8], r4": "db 4a f8 ff 41 00 00 00",
+        "atomic_and32 [r10-8], r4": "c3 4a f8 ff 50 00 00 00",
+        "atomic_fetch_xor32 [r10-8], r4": "c3 4a f8 ff a1 00 00 00",
+        "xchg32 [r10-8], r4": "c3 4a f8 ff e1 00 00 00",
+        "cmpxchg64 [r10-8], r4": "db 4a f8 ff f1 00 00 00",
+        "ldxsh r0, [r10-2]": "89 a0 fe ff 00 00 00 00",
+        "ldxsw r0, [r10-4]": "81 a0 fc ff 00 00 00 00",
+    }
+    for text, hexs in cases.items():
+        assert asm.assemble(text) == bytes.fromhex(hexs.replace(" ", "")), text
