@@ -316,6 +316,19 @@ ORA_EXPORT int ora_map_update(ora_env *e, int fd, const void *key, const void *v
     return r;
 }
 
+/* host control plane, n entries (keys / values packed back to back): ora_map_update per entry in
+ * order; stops at the first error and returns it */
+ORA_EXPORT int ora_map_update_n(ora_env *e, int fd, const void *keys, const void *vals, uint64_t n, uint64_t flags) {
+    if (fd < 0 || fd >= MAX_MAPS || !e->maps[fd].used) return -E_INVAL;
+    const uint8_t *kp = keys, *vp = vals;
+    const uint32_t ks = e->maps[fd].key_size, vs = e->maps[fd].value_size;
+    for (uint64_t i = 0; i < n; i++) {
+        int r = ora_map_update(e, fd, kp + i * ks, vp + i * vs, flags);
+        if (r) return r;
+    }
+    return 0;
+}
+
 /* bpf_ringbuf_output (helper 130), bpf.h:4407-4422, 6050-6051, 6064-6066; SURVEY.md O6:
  * flags in {0, NO_WAKEUP 1, FORCE_WAKEUP 2}; rec = roundup8(8 + size); if used + rec > capacity
  * the record is dropped (-EAGAIN) else appended with header {len, pg_off}. */

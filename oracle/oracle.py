@@ -44,6 +44,7 @@ def lib():
         L.ora_reset_stats.argtypes = [vp]
         L.ora_map_create.argtypes = [vp, u32, u32, u32, u32]
         L.ora_map_update.argtypes = [vp, i32, vp, vp, u64]
+        L.ora_map_update_n.argtypes = [vp, i32, vp, vp, u64, u64]
         L.ora_prog_load.argtypes = [vp, vp, u32]
         L.ora_attach.argtypes = [vp, i32, u32, u32]
         L.ora_set_pt_shards.argtypes = [vp, u32]
@@ -90,6 +91,9 @@ class Oracle:
 
     def update_map(self, fd, key: bytes, val: bytes, flags=0) -> int:
         return self.L.ora_map_update(self.h, fd, key, val, flags)
+
+    def update_many(self, fd, keys: bytes, vals: bytes, n: int, flags=0) -> int:
+        return self.L.ora_map_update_n(self.h, fd, keys, vals, n, flags)
 
     def load_prog(self, slots: bytes) -> int:
         p = self.L.ora_prog_load(self.h, slots, len(slots) // 8)

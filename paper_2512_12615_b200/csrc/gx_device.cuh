@@ -120,69 +120,128 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
     return nullptr;
 }
 
-/* bpf_map_update_elem on a HASH with 8-byte values (bpf.h:1762-1776).  Returns 0 or -errno;
- * *full set when refused for capacity (hash_full).
- * Capacity (max_entries): aux[1] counts committed entries.  An insert is refused when the committed
- * count has reached max_entries; inserts of DISTINCT keys racing at that boundary can each pass the
- * check, so up to (concurrent inserters - 1) entries beyond max_entries may be admitted (the slot
- * array holds 2 x max_entries, reading I-22).  Nothing ever spins on other lanes. */
-__device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
-                                               bool &full) {
+#ifndef GX_HASH_VALVE
+#define GX_HASH_VALVE (1u << 20)
+#endif
+/* bpf_map_update_elem on a HASH with 8-byte values (bpf.h:1762-1776): 0 or -errno; `full` set when
+ * refused for capacity (hash_full).
+ * Capacity (max_entries, exact): aux[1] counts committed entries, aux[2] reservations (committed +
+ * in-flight inserts).  An insert of an absent key first reserves (aux[2]++); a reservation below
+ * max_entries may publish its slot (16-B CAS) and then commits (aux[1]++); a lost CAS returns the
+ * reservation and probes again (the winner may hold our key).  With no reservation to be had: if the
+ * committed count has reached max_entries the map is full for good, and one more probe that still
+ * finds the key absent refuses the insert (-E2BIG, linearised at that probe); otherwise other inserts
+ * hold the excess reservations only transiently -- each publishes or returns its reservation without
+ * waiting on anything -- so the insert waits and probes again.  The map never holds more than
+ * max_entries entries and never refuses an insert while it has room (reading I-22).
+ *
+ * hash_step is ONE attempt; `st` carries state between attempts (0 initially, kHashFullSeen after
+ * the count reached max_entries).  Returns kHashDone (rc / full set), kHashAgain (probe again now)
+ * or kHashWait (reservations in flight: back off, then probe again). */
+enum { kHashDone = 0, kHashAgain = 1, kHashWait = 2, kHashFullSeen = 1 };
+__device__ __forceinline__ int hash_step(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags, uint32_t &st,
+                                         int64_t &rc, bool &full) {
     full = false;
-    if (flags > 2) return -E_INVAL;
+    rc = 0;
+    if (flags > 2) {
+        rc = -E_INVAL;
+        return kHashDone;
+    }
     uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(m.aux);
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    for (;;) {
-        uint64_t *s = nullptr;
-        bool present = false;
-        if (key == GX_HASH_EMPTY) {
-            s = slots + 2 * cap;
-            present = ld_acquire(s) == 1;
-        } else {
-            const uint64_t h = mix64(key) & m.cap_mask;
-            uint64_t i = 0;
-            for (; i < cap; i++) {
-                s = slots + 2 * ((h + i) & m.cap_mask);
-                const uint64_t k = ld_acquire(s);
-                if (k == key) {
-                    present = true;
-                    break;
-                }
-                if (k == GX_HASH_EMPTY) break;
+    uint64_t *s = nullptr;
+    bool present = false;
+    if (key == GX_HASH_EMPTY) {
+        s = slots + 2 * cap;
+        present = ld_acquire(s) == 1;
+    } else {
+        const uint64_t h = mix64(key) & m.cap_mask;
+        uint64_t i = 0;
+        for (; i < cap; i++) {
+            s = slots + 2 * ((h + i) & m.cap_mask);
+            const uint64_t k = ld_acquire(s);
+            if (k == key) {
+                present = true;
+                break;
             }
-            if (i == cap) {
+            if (k == GX_HASH_EMPTY) break;
+        }
+        if (i == cap) {
+            full = true;
+            rc = -E_2BIG;
+            return kHashDone;
+        }
+    }
+    if (present) {
+        if (flags == 1) rc = -E_EXIST;
+        else st_relaxed(s + 1, val);
+        return kHashDone;
+    }
+    if (flags == 2) {
+        rc = -E_NOENT;
+        return kHashDone;
+    }
+    if (st == kHashFullSeen) { /* absent at a probe after the committed count reached max_entries */
+        full = true;
+        rc = -E_2BIG;
+        return kHashDone;
+    }
+    /* a reservation: the counter is watched with a plain load first (no RMW storm on its line while
+     * the map sits at its capacity) */
+    bool got = false;
+    if (ld_relaxed(reinterpret_cast<const uint64_t *>(&ctr[2])) < m.max_entries) {
+        got = atomicAdd(&ctr[2], 1ull) < m.max_entries;
+        if (!got) atomicAdd(&ctr[2], ~0ull); /* return it */
+    }
+    if (!got) {
+        if (ld_relaxed(reinterpret_cast<const uint64_t *>(&ctr[1])) >= m.max_entries) {
+            st = kHashFullSeen; /* full for good; our key may have arrived since the probe */
+            return kHashAgain;
+        }
+        return kHashWait;
+    }
+    const uint64_t empty = key == GX_HASH_EMPTY ? 0 : GX_HASH_EMPTY;
+    const uint64_t tag = key == GX_HASH_EMPTY ? 1 : key;
+    uint64_t ol, oh;
+    cas128(s, empty, 0, tag, val, ol, oh);
+    if (ol == empty && oh == 0) {
+        atomicAdd(&ctr[1], 1ull);
+        return kHashDone;
+    }
+    atomicAdd(&ctr[2], ~0ull); /* lost the slot: return the reservation, probe again */
+    return kHashAgain;
+}
+/* one thread on its own (host control-plane kernels, gx_maps.cu) */
+__device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
+                                               bool &full) {
+    uint32_t st = 0, waits = 0;
+    int64_t rc;
+    for (;;) {
+        const int r = hash_step(m, key, val, flags, st, rc, full);
+        if (r == kHashDone) return rc;
+        if (r == kHashWait) {
+            if (++waits > GX_HASH_VALVE) { /* safety valve, far beyond any in-flight insert */
                 full = true;
                 return -E_2BIG;
             }
+            __nanosleep(waits < 7 ? 32u << waits : 2048u);
         }
-        if (present) {
-            if (flags == 1) return -E_EXIST;
-            st_relaxed(s + 1, val);
-            return 0;
-        }
-        if (flags == 2) return -E_NOENT;
-        if (ld_relaxed(reinterpret_cast<const uint64_t *>(&ctr[1])) >= m.max_entries) {
-            full = true;
-            return -E_2BIG;
-        }
-        const uint64_t empty = key == GX_HASH_EMPTY ? 0 : GX_HASH_EMPTY;
-        const uint64_t tag = key == GX_HASH_EMPTY ? 1 : key;
-        uint64_t ol, oh;
-        cas128(s, empty, 0, tag, val, ol, oh);
-        if (ol == empty && oh == 0) {
-            atomicAdd(&ctr[1], 1ull);
-            return 0;
-        }
-        /* lost the slot: probe again (the winner may hold our key) */
     }
 }
 
+/* JIT builds move the cold, code-heavy group paths out of line (one copy per module instead of one
+ * per call site and per uniform / min-PC block copy); the interpreter keeps them inline. */
+#ifdef GX_JIT
+#define GXD_COLD __noinline__
+#else
+#define GXD_COLD __forceinline__
+#endif
+
 /* Warp-cooperative HASH helpers: the lanes of `mask` call together; `me` marks the lanes whose
  * event is executing the helper.  When every executing lane asks for the same key (a warp-uniform
- * key -- a page swept by a whole warp record in C3's prefill), one lane probes / inserts and the
- * others reuse its result instead of 31 probes and 31 contending CASes on one slot.  Sequential
- * equivalent: the leader's event goes first. */
+ * key -- a page swept by a whole warp record in C3's prefill), one lane probes and the others reuse
+ * its result instead of 31 probes on one chain.  Sequential equivalent: the leader's event goes first. */
 __device__ __forceinline__ uint64_t *hash_lookup_coop(const GxMapDesc &m, uint64_t key, bool me, unsigned mask) {
     const unsigned part = __ballot_sync(mask, me);
     if (!part) return nullptr;
@@ -196,26 +255,51 @@ __device__ __forceinline__ uint64_t *hash_lookup_coop(const GxMapDesc &m, uint64
     }
     return me ? hash_find(m, key) : nullptr;
 }
-__device__ __forceinline__ int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
-                                                    bool &full, bool me, unsigned mask) {
+/* update(map, key, val, flags): lanes asking for the same key with the same flags form a group
+ * (__match_any_sync) and take the group's SEQUENTIAL result in lane order with one map update (S1;
+ * the lanes of a record are consecutive events):
+ *   NOEXIST -- the group's first lane inserts (0 / -EEXIST / -E2BIG); the later lanes then find the
+ *              key present (-EEXIST), or the map still full (-E2BIG);
+ *   ANY / EXIST -- every lane meets the same state (present: all overwrite, the last value stays;
+ *              absent: all insert-or-overwrite, resp. all -ENOENT; full: all -E2BIG), so the group's
+ *              LAST lane performs the update with its value and every lane takes its result.
+ * The doing lanes of the warp run their attempts in lock-step rounds (hash_step), so a lane waiting
+ * for reservations never spins past a lane of its own warp that holds one. */
+__device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
+                                             bool &full, bool me, unsigned mask) {
     full = false;
     const unsigned part = __ballot_sync(mask, me);
-    if (!part) return 0;
+    if (!me) return 0;
     const unsigned lane = threadIdx.x & 31;
-    const int leader = __ffs(part) - 1;
-    const uint64_t k0 = __shfl_sync(mask, key, leader);
-    const uint64_t f0 = __shfl_sync(mask, flags, leader);
-    if (__all_sync(mask, !me || (key == k0 && flags == f0))) {
-        int64_t rc = 0;
-        if ((int)lane == leader) rc = hash_update(m, key, val, flags, full);
-        const int64_t rc0 = (int64_t)__shfl_sync(mask, (unsigned long long)rc, leader);
-        __syncwarp(mask);
-        if (!me || (int)lane == leader) return rc;
-        /* NOEXIST after the leader inserted (or found) the key: it is present for everyone else */
-        if (flags == 1 && (rc0 == 0 || rc0 == -E_EXIST)) return -E_EXIST;
-        return hash_update(m, key, val, flags, full);
+    const unsigned grp = __match_any_sync(part, key) & __match_any_sync(part, flags);
+    const int doer = flags == 1 ? __ffs(grp) - 1 : 31 - __clz(grp);
+    const bool is_doer = (int)lane == doer;
+    const unsigned doers = __ballot_sync(part, is_doer);
+    int64_t rc = 0;
+    bool f = false;
+    if (is_doer) {
+        uint32_t st = 0, waits = 0;
+        unsigned pend = doers;
+        for (;;) {
+            const int r = hash_step(m, key, val, flags, st, rc, f);
+            const unsigned still = __ballot_sync(pend, r != kHashDone);
+            if (r == kHashDone) break;
+            if (__any_sync(still, r == kHashWait)) {
+                if (++waits > GX_HASH_VALVE) { /* safety valve, far beyond any in-flight insert */
+                    rc = -E_2BIG;
+                    f = true;
+                    break;
+                }
+                __nanosleep(waits < 7 ? 32u << waits : 2048u);
+            }
+            pend = still;
+        }
     }
-    return me ? hash_update(m, key, val, flags, full) : 0;
+    rc = (int64_t)__shfl_sync(grp, (unsigned long long)rc, doer);
+    f = __shfl_sync(grp, (int)f, doer) != 0;
+    if (!is_doer && flags == 1 && rc == 0) rc = -E_EXIST;
+    full = f;
+    return rc;
 }
 
 /* ---- PREFETCH QUEUE: gdev_mem_prefetch(queue, addr, len) (F-1..F-3).

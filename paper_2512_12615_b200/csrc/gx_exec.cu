@@ -174,6 +174,64 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
     }
 }
 
+/* XCHG on a shared map value, called by the lanes of `mask`: lanes on one address take the group's
+ * sequential result in lane order (the first gets the old value, each later lane the value of the
+ * lane before it; the word keeps the last lane's value) with one atomicExch per address. */
+__device__ __forceinline__ uint64_t group_xchg(unsigned mask, uint64_t addr, uint64_t v, bool w32) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(mask, addr);
+    const int last = 31 - __clz(peers);
+    const unsigned below = peers & ((1u << lane) - 1);
+    const int prev = below ? 31 - __clz(below) : (int)lane;
+    uint64_t old = 0;
+    if ((int)lane == last)
+        old = w32 ? (uint64_t)atomicExch(reinterpret_cast<unsigned *>(addr), (uint32_t)v)
+                  : (uint64_t)atomicExch(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)v);
+    old = __shfl_sync(peers, old, last);
+    const uint64_t pv = __shfl_sync(peers, v, prev);
+    const uint64_t r = below ? pv : old;
+    return w32 ? (uint32_t)r : r;
+}
+/* CMPXCHG (cmp = r0): the group's sequential outcome in lane order from one read of the word,
+ * committed with one CAS old -> final (recomputed from the returned value if another warp changed
+ * the word).  W: 32-bit compare and result, zero-extended. */
+__device__ __forceinline__ uint64_t group_cmpxchg(unsigned mask, uint64_t addr, uint64_t cmp, uint64_t v, bool w32) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(mask, addr);
+    const int gl = __ffs(peers) - 1;
+    const uint64_t M = w32 ? 0xFFFFFFFFull : ~0ull;
+    cmp &= M;
+    v &= M;
+    uint64_t cur = 0;
+    if ((int)lane == gl) {
+        if (w32) {
+            uint32_t t;
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(addr) : "memory");
+            cur = t;
+        } else {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(addr) : "memory");
+        }
+    }
+    cur = __shfl_sync(peers, cur, gl);
+    for (;;) {
+        uint64_t c = cur, mine = 0;
+        for (unsigned m = peers; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const uint64_t cj = __shfl_sync(peers, cmp, j), vj = __shfl_sync(peers, v, j);
+            if (j == (int)lane) mine = c;
+            if (c == cj) c = vj;
+        }
+        uint64_t got = 0;
+        if ((int)lane == gl)
+            got = w32 ? (uint64_t)atomicCAS(reinterpret_cast<unsigned *>(addr), (uint32_t)cur, (uint32_t)c)
+                      : (uint64_t)atomicCAS(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)cur,
+                                            (unsigned long long)c);
+        got = __shfl_sync(peers, got, gl);
+        if (got == cur) return mine;
+        cur = got;
+    }
+}
+
 struct Smem {
     GxInsn *prog;
     GxMapDesc *maps;
@@ -440,15 +498,10 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     const uint64_t addr = me ? R[in.dst * 32 + lane] + in.off : 0;
                     const uint64_t sv = !me ? 0 : (in.flags & GXF_PRIV) ? (uint64_t)(int64_t)(int32_t)(in.imm >> 32)
                                                                        : R[in.src * 32 + lane];
-                    if (op == 0xE1 || op == 0xF1) { /* XCHG / CMPXCHG: per lane */
+                    if (op == 0xE1 || op == 0xF1) { /* XCHG / CMPXCHG: the sequential result in lane order */
                         if (me) {
-                            if (op == 0xE1) {
-                                R[in.src * 32 + lane] = w32 ? atomicExch(reinterpret_cast<unsigned *>(addr), (uint32_t)sv)
-                                                            : atomicExch(reinterpret_cast<unsigned long long *>(addr), sv);
-                            } else {
-                                R[lane] = w32 ? atomicCAS(reinterpret_cast<unsigned *>(addr), (uint32_t)R[lane], (uint32_t)sv)
-                                              : atomicCAS(reinterpret_cast<unsigned long long *>(addr), R[lane], sv);
-                            }
+                            if (op == 0xE1) R[in.src * 32 + lane] = group_xchg(exec, addr, sv, w32);
+                            else R[lane] = group_cmpxchg(exec, addr, R[lane], sv, w32);
                         }
                         break;
                     }
@@ -563,11 +616,16 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         const uint32_t k = (in.flags & GXF_KEY_MAPV) ? *reinterpret_cast<const uint32_t *>(R[2 * 32 + lane])
                                                                       : (uint32_t)(K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7)));
                         const uint64_t flags = R[4 * 32 + lane];
+                        /* ARRAY: lanes copying into one key (flags ANY / EXIST) keep the sequential
+                         * result, the last such lane's value */
+                        const bool copies = flags == 0 || flags == 2;
+                        const unsigned kg = in.op == GX_CALL_UPDATE_ARRAY
+                                                ? __match_any_sync(exec, k) & __ballot_sync(exec, copies) : (1u << lane);
                         int64_t rc = 0;
                         if (flags > 2) rc = -E_INVAL;
                         else if (k >= md.max_entries) rc = -E_2BIG;
                         else if (flags == 1) rc = -E_EXIST;
-                        else {
+                        else if ((int)lane == 31 - __clz(kg)) {
                             const uint32_t nw = md.value_size / 8;
                             for (uint32_t w = 0; w < nw; w++) {
                                 const uint64_t v = (in.flags & GXF_VAL_MAPV)

@@ -488,8 +488,13 @@ struct Gen {
                                         ? "*(const uint32_t *)r2"
                                         : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             std::ostringstream b;
-            b << "const uint32_t k = " << key << "; int64_t rc = 0;"
-              << " if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17; else {";
+            /* ARRAY: lanes writing the same key keep the sequential result -- the group's last lane's
+             * value (one copy per key); the return code depends on the key and flags only */
+            b << "const uint32_t k = " << key << "; int64_t rc = 0;";
+            if (g.op == GX_CALL_UPDATE_ARRAY)
+                b << " const unsigned kg_ = __match_any_sync(" << M() << ", k) & __ballot_sync(" << M() << ", r4 == 0 || r4 == 2);";
+            b << " if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17; else";
+            b << (g.op == GX_CALL_UPDATE_ARRAY ? " if ((int)lane == 31 - __clz(kg_)) {" : " {");
             for (uint32_t w = 0; w < m.value_size / 8; w++) {
                 const std::string v = (g.flags & GXF_VAL_MAPV) ? "((const uint64_t *)r3)[" + std::to_string(w) + "]"
                                                                : "s" + std::to_string((uint32_t)g.imm / 8 + w);
@@ -608,14 +613,16 @@ struct Gen {
             me(fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";");
             return;
         }
+        /* XCHG / CMPXCHG on shared map values: lanes grouped by address, the group's sequential
+         * result in lane order (gx_jit_rt.cuh group_xchg / group_cmpxchg) */
         if (op == 0xE1) {
-            me(R(g.src) + " = " + (w32 ? "atomicExch((unsigned *)(" + addr + "), (uint32_t)" + v + ")"
-                                       : "atomicExch((unsigned long long *)(" + addr + "), " + v + ")") + ";");
+            st("{ const uint64_t res_ = group_xchg<" + std::string(w32 ? "true" : "false") + ">(" + M() + ", " + addr + ", " + v +
+               "); " + R(g.src) + " = res_; }");
             return;
         }
         if (op == 0xF1) {
-            me("r0 = " + (w32 ? "atomicCAS((unsigned *)(" + addr + "), (uint32_t)r0, (uint32_t)" + v + ")"
-                               : "atomicCAS((unsigned long long *)(" + addr + "), r0, " + v + ")") + ";");
+            st("{ const uint64_t res_ = group_cmpxchg<" + std::string(w32 ? "true" : "false") + ">(" + M() + ", " + addr +
+               ", r0, " + v + "); r0 = res_; }");
             return;
         }
         const GxMapDesc &m = L.maps[fd];
@@ -638,7 +645,7 @@ struct Gen {
         else st("(void)" + e + ";");
     }
 
-    void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes, int B) {
+    void kernel(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes, int B, unsigned vmask) {
         int U = 2;
         if (const char *e = getenv("GX_JIT_UNROLL")) U = std::max(1, std::min(8, atoi(e)));
         /* GX_JIT_MINB: min resident blocks per SM in __launch_bounds__ (default 1: up to 64 registers
@@ -673,15 +680,17 @@ struct Gen {
         /* two launch bodies: event ingest through the block-wide TMA ring (large batches of light
          * programs) and through per-lane register loads (small batches, ALU-heavy programs) --
          * the runtime picks per launch (gx_runtime.cpp launch_cfg) */
+        /* only the instances `vmask` asks for (GX_JIT_V_*): a module per launch variant keeps NVRTC
+         * time proportional to what runs -- each instance inlines every program U times */
         const int S = gx_jit_stages();
-        body("gx_body_ring", S >= 2 ? S : 3, B, U, punroll, images);
-        body("gx_body_reg", 0, B, U, punroll, images);
+        if (vmask & (GX_JIT_V_RING | GX_JIT_V_RING_R)) body("gx_body_ring", S >= 2 ? S : 3, B, U, punroll, images);
+        if (vmask & (GX_JIT_V_REG | GX_JIT_V_REG_R)) body("gx_body_reg", 0, B, U, punroll, images);
         const std::string lb = "__launch_bounds__(" + std::to_string(B) + (minb > 0 ? ", " + std::to_string(minb) : std::string()) + ")";
         const char *args = "(const uint4 *__restrict__ ev, uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats)";
-        o << "extern \"C\" __global__ void " << lb << " gx_jit_kernel" << args << " {\n  gx_body_ring<false>(ev, n, ret, gstats);\n}\n"
-          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_r" << args << " {\n  gx_body_ring<true>(ev, n, ret, gstats);\n}\n"
-          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_g" << args << " {\n  gx_body_reg<false>(ev, n, ret, gstats);\n}\n"
-          << "extern \"C\" __global__ void " << lb << " gx_jit_kernel_gr" << args << " {\n  gx_body_reg<true>(ev, n, ret, gstats);\n}\n";
+        for (int k = 0; k < 4; k++)
+            if (vmask & (1u << k))
+                o << "extern \"C\" __global__ void " << lb << " " << gx_jit_kernel_name(k) << args << " {\n  "
+                  << (k < 2 ? "gx_body_ring" : "gx_body_reg") << (k & 1 ? "<true>" : "<false>") << "(ev, n, ret, gstats);\n}\n";
     }
 
     /* f4: the program as __device__ hooks a user kernel calls inline -- the paper's
@@ -1042,10 +1051,15 @@ int gx_jit_block() {
     return b;
 }
 
+const char *gx_jit_kernel_name(int variant) {
+    static const char *names[4] = {"gx_jit_kernel", "gx_jit_kernel_r", "gx_jit_kernel_g", "gx_jit_kernel_gr"};
+    return names[variant & 3];
+}
+
 std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes,
-                          int block) {
+                          int block, unsigned vmask) {
     Gen g(L);
-    g.kernel(images, sizes, block);
+    g.kernel(images, sizes, block, vmask);
     return g.o.str();
 }
 

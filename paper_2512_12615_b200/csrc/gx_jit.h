@@ -5,9 +5,14 @@
 
 #include "gx_internal.h"
 
-/* CUDA C++ source of one launch configuration (programs in launch-slot order). */
+/* launch variants of a configuration: event ingest (block-wide TMA ring / per-lane register loads)
+ * x per-event R0 (off / on); bit k of a variant mask = variant k, kernel gx_jit_kernel_name(k) */
+enum { GX_JIT_V_RING = 1, GX_JIT_V_RING_R = 2, GX_JIT_V_REG = 4, GX_JIT_V_REG_R = 8, GX_JIT_V_ALL = 15 };
+const char *gx_jit_kernel_name(int variant);
+/* CUDA C++ source of one launch configuration (programs in launch-slot order), the kernels of
+ * the variants in `vmask` only. */
 std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images,
-                          const std::vector<uint32_t> &sizes, int block);
+                          const std::vector<uint32_t> &sizes, int block, unsigned vmask = GX_JIT_V_ALL);
 /* f4: CUDA C++ of the program as inline __device__ hooks (gx_hook_access / gx_hook_block_enter)
  * followed by the user's kernels; no privatised maps (L must have none). */
 std::string gx_jit_instrument_source(const GxLaunch &L, const GxInsn *image, uint32_t n, const std::string &user);

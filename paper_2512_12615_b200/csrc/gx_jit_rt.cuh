@@ -330,36 +330,44 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
  * scale; the group is known by construction here.)
  *
  * Map atomic (ADD/OR/AND/XOR, +-FETCH).  All lanes on one address (record-uniform keys): one
- * REDUX + one L2 atomic for the group.  Mixed addresses: plain per-lane atomics for non-FETCH
- * ops (the L2 serialises per address; a match_any costs more than it saves on random keys), and
- * __match_any_sync groups for FETCH ops, whose lanes get old + their exclusive prefix in lane
- * order (a valid linearisation of the group's sequential order). */
+ * REDUX + one L2 atomic for the group, inline.  Mixed addresses (and partial FETCH groups), out of
+ * line: __match_any_sync groups, one L2 atomic per distinct address; FETCH lanes get old + their
+ * exclusive prefix in lane order -- the group's sequential result (the lanes of a record are
+ * consecutive events). */
+template <uint32_t OP, bool W32, bool FETCH>
+__device__ __noinline__ uint64_t group_atomic_slow(unsigned mask, uint64_t addr, uint64_t v) {
+    /* lanes grouped by address: one L2 atomic per distinct address carrying the group's reduced
+     * value; FETCH lanes get old + their exclusive prefix in lane order */
+    const unsigned lane = threadIdx.x & 31;
+    constexpr uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
+    const unsigned peers = __match_any_sync(mask, addr);
+    const unsigned gl = __ffs(peers) - 1;
+    uint64_t pre = ident, tot = ident;
+    for (unsigned m = peers; m; m &= m - 1) {
+        const int jl = __ffs(m) - 1;
+        const uint64_t vj = __shfl_sync(peers, v, jl);
+        if (jl < (int)lane) pre = apply_op(OP, pre, vj);
+        tot = apply_op(OP, tot, vj);
+    }
+    uint64_t old = 0;
+    if (lane == gl) old = global_atomic(OP, addr, tot, W32, FETCH);
+    if (!FETCH) return 0;
+    old = __shfl_sync(peers, old, gl);
+    const uint64_t r = apply_op(OP, old, pre);
+    return W32 ? (uint32_t)r : r;
+}
 template <uint32_t OP, bool W32, bool FETCH>
 __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, uint64_t v) {
     const unsigned lane = threadIdx.x & 31;
     const unsigned leader = __ffs(mask) - 1;
     const uint64_t a0 = __shfl_sync(mask, addr, leader);
     constexpr uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
-    if (__all_sync(mask, addr == a0)) {
+    /* the inline fast paths: one address for the whole group (record-uniform keys) */
+    if (__all_sync(mask, addr == a0) && (!FETCH || mask == 0xFFFFFFFFu)) {
         if (!FETCH) {
             const uint64_t agg = group_reduce(mask, OP, v, W32);
             if (lane == leader) global_atomic(OP, a0, agg, W32, false);
             return 0;
-        }
-        /* partial group: explicit walk over its lanes (shfl_up chains need all 32) */
-        if (mask != 0xFFFFFFFFu) {
-            uint64_t pre = ident, tot = ident;
-            for (unsigned m = mask; m; m &= m - 1) {
-                const int jl = __ffs(m) - 1;
-                const uint64_t vj = __shfl_sync(mask, v, jl);
-                if (jl < (int)lane) pre = apply_op(OP, pre, vj);
-                tot = apply_op(OP, tot, vj);
-            }
-            uint64_t old = 0;
-            if (lane == leader) old = global_atomic(OP, a0, tot, W32, true);
-            old = __shfl_sync(mask, old, leader);
-            const uint64_t r = apply_op(OP, old, pre);
-            return W32 ? (uint32_t)r : r;
         }
         /* full warp: inclusive scan in lane order */
         uint64_t inc = W32 ? (uint32_t)v : v;
@@ -377,27 +385,72 @@ __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, u
         const uint64_t r = apply_op(OP, old, exc);
         return W32 ? (uint32_t)r : r;
     }
+    /* mixed addresses or a partial FETCH group: out of line */
+    return group_atomic_slow<OP, W32, FETCH>(mask, addr, v);
+}
+
+/* XCHG on a shared map value.  Lanes on one address take the sequential result in lane order (the
+ * lanes of a record are consecutive events, S1): the first gets the old value, each later lane the
+ * value of the lane before it, and the word ends with the last lane's value -- one atomicExch per
+ * address. */
+template <bool W32>
+__device__ __noinline__ uint64_t group_xchg(unsigned mask, uint64_t addr, uint64_t v) {
+    const unsigned lane = threadIdx.x & 31;
     const unsigned peers = __match_any_sync(mask, addr);
-    const unsigned gl = __ffs(peers) - 1;
-    if (!FETCH) {
-        /* one L2 atomic per distinct address (the group's values reduced by a walk over its lanes) */
-        uint64_t tot = ident;
-        for (unsigned m = peers; m; m &= m - 1) tot = apply_op(OP, tot, __shfl_sync(peers, v, __ffs(m) - 1));
-        if (lane == gl) global_atomic(OP, addr, tot, W32, false);
-        return 0;
-    }
-    uint64_t pre = ident, tot = ident;
-    for (unsigned m = peers; m; m &= m - 1) {
-        const int jl = __ffs(m) - 1;
-        const uint64_t vj = __shfl_sync(peers, v, jl);
-        if (jl < (int)lane) pre = apply_op(OP, pre, vj);
-        tot = apply_op(OP, tot, vj);
-    }
+    const int last = 31 - __clz(peers);
+    const unsigned below = peers & ((1u << lane) - 1);
+    const int prev = below ? 31 - __clz(below) : (int)lane;
     uint64_t old = 0;
-    if (lane == gl) old = global_atomic(OP, addr, tot, W32, true);
-    old = __shfl_sync(peers, old, gl);
-    const uint64_t r = apply_op(OP, old, pre);
+    if ((int)lane == last)
+        old = W32 ? (uint64_t)atomicExch(reinterpret_cast<unsigned *>(addr), (uint32_t)v)
+                  : (uint64_t)atomicExch(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)v);
+    old = __shfl_sync(peers, old, last);
+    const uint64_t pv = __shfl_sync(peers, v, prev);
+    const uint64_t r = below ? pv : old;
     return W32 ? (uint32_t)r : r;
+}
+
+/* CMPXCHG on a shared map value (r0 = compare value).  Lanes on one address: the group's sequential
+ * outcome in lane order (each lane sees the value the lanes before it left and swaps if it equals its
+ * r0) is computed from one read of the word and committed with one CAS of old -> final; a failed CAS
+ * (another warp changed the word) recomputes from the value it returned.  W: 32-bit compare and
+ * result, zero-extended. */
+template <bool W32>
+__device__ __noinline__ uint64_t group_cmpxchg(unsigned mask, uint64_t addr, uint64_t cmp, uint64_t v) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(mask, addr);
+    const int gl = __ffs(peers) - 1;
+    const uint64_t M = W32 ? 0xFFFFFFFFull : ~0ull;
+    cmp &= M;
+    v &= M;
+    uint64_t cur = 0;
+    if ((int)lane == gl) {
+        if (W32) {
+            uint32_t t;
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(addr) : "memory");
+            cur = t;
+        } else {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(addr) : "memory");
+        }
+    }
+    cur = __shfl_sync(peers, cur, gl);
+    for (;;) {
+        uint64_t c = cur, mine = 0;
+        for (unsigned m = peers; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const uint64_t cj = __shfl_sync(peers, cmp, j), vj = __shfl_sync(peers, v, j);
+            if (j == (int)lane) mine = c;
+            if (c == cj) c = vj;
+        }
+        uint64_t got = 0;
+        if ((int)lane == gl)
+            got = W32 ? (uint64_t)atomicCAS(reinterpret_cast<unsigned *>(addr), (uint32_t)cur, (uint32_t)c)
+                      : (uint64_t)atomicCAS(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)cur,
+                                            (unsigned long long)c);
+        got = __shfl_sync(peers, got, gl);
+        if (got == cur) return mine;
+        cur = got;
+    }
 }
 
 /* ADD of a compile-time constant K (the verifier folded the source register: `mov r1, 1;

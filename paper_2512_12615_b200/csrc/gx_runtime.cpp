@@ -97,15 +97,16 @@ struct LaunchCfg {
     std::vector<int> progs;  /* launch slot -> prog fd */
     uint32_t smem = 0;
     uint32_t grid = 0;
-    /* JIT engine */
-    bool jit_tried = false;
-    CUmodule jmod = nullptr;
-    CUfunction jfunc = nullptr;   /* gx_jit_kernel: no per-event R0 */
-    CUfunction jfunc_r = nullptr; /* gx_jit_kernel_r: writes d_ret */
-    CUfunction jfunc_g = nullptr, jfunc_gr = nullptr; /* register-ingest instances */
-    unsigned jsmem = 0;           /* dynamic shared bytes of the ring instances (fixed at compile) */
+    /* JIT engine: one module per launch variant (GX_JIT_V_*: ring / register ingest x R0 off / on),
+     * compiled on the variant's first launch */
+    struct JitVar {
+        bool tried = false;
+        CUmodule mod = nullptr;
+        CUfunction fn = nullptr;
+        unsigned smem = 0;        /* dynamic shared bytes (the ring stages; fixed at compile) */
+        uint32_t grid = 0, block = 256;
+    } jv[4];
     bool ring_ok = true;
-    uint32_t jgrid = 0, jblock = 256;
     std::string jit_log;
     double jit_ms = 0;
 };
@@ -337,11 +338,12 @@ int get_launch(gx_rt *rt, int prog_fd, LaunchCfg *&out) {
     return 0;
 }
 
-/* compiles (once) the JIT kernel of a launch configuration */
-int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
-    if (cfg.jfunc) return 0;
-    if (cfg.jit_tried) return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
-    cfg.jit_tried = true;
+/* compiles (once) the JIT kernel of launch variant `k` of a configuration */
+int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
+    LaunchCfg::JitVar &V = cfg.jv[k];
+    if (V.fn) return 0;
+    if (V.tried) return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
+    V.tried = true;
     Drv &d = drv();
     if (!d.ok) {
         cfg.jit_log = "driver entry points unavailable";
@@ -354,11 +356,12 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         images.push_back(rt->progs[q].vr.image.data());
         sizes.push_back((uint32_t)rt->progs[q].vr.image.size());
     }
+    const bool ring = k < 2;
     /* fewer, larger blocks keep the per-block privatised-shard flush small; one 1024-thread block
      * per SM measured fastest on every config (profiles/r1_jit_variants.md); 256-thread blocks only
      * if the 1024-thread kernel cannot be resident at all */
     for (int B : {gx_jit_block(), 256}) {
-        std::string src = gx_jit_source(cfg.h, images, sizes, B);
+        std::string src = gx_jit_source(cfg.h, images, sizes, B, 1u << k);
         if (const char *dump = getenv("GX_JIT_DUMP")) {
             if (FILE *f = fopen(dump, "w")) {
                 fputs(src.c_str(), f);
@@ -369,51 +372,53 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg) {
         if (gx_jit_compile(src, cubin, cfg.jit_log)) return set_err(rt, -ENOSYS, "JIT compile failed: %s", cfg.jit_log.c_str());
         CUmodule mod = nullptr;
         if (d.moduleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return set_err(rt, -EFAULT, "cuModuleLoadData failed");
-        /* ring ingest (no R0 / R0), register ingest (no R0 / R0) */
-        static const char *names[4] = {"gx_jit_kernel", "gx_jit_kernel_r", "gx_jit_kernel_g", "gx_jit_kernel_gr"};
-        CUfunction fn[4] = {};
-        for (int k = 0; k < 4; k++)
-            if (d.moduleGetFunction(&fn[k], mod, names[k]) != CUDA_SUCCESS)
-                return set_err(rt, -EFAULT, "cuModuleGetFunction(%s) failed", names[k]);
-        const unsigned smem = gx_jit_smem(B);
-        for (int k = 0; k < 2; k++)
-            if (d.funcSetAttribute(fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
-                return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
+        CUfunction fn = nullptr;
+        if (d.moduleGetFunction(&fn, mod, gx_jit_kernel_name(k)) != CUDA_SUCCESS)
+            return set_err(rt, -EFAULT, "cuModuleGetFunction(%s) failed", gx_jit_kernel_name(k));
+        const unsigned smem = ring ? gx_jit_smem(B) : 0u;
+        if (ring && d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+            return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
         /* shared-memory carve-out preference (GX_JIT_CARVEOUT percent; -1 = the driver's choice): a
          * hint -- the driver still picks a configuration that fits the ring -- so 0 asks for the
          * smallest carve-out, leaving the rest of the SM's 256 KiB to L1 */
         if (const char *e = getenv("GX_JIT_CARVEOUT")) {
             const int pct = atoi(e);
-            if (pct >= 0 && pct <= 100)
-                for (int k = 0; k < 4; k++) d.funcSetAttribute(fn[k], CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, pct);
+            if (pct >= 0 && pct <= 100) d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, pct);
         }
         int bps = 2048 / B; /* per-thread shards: at most 2048 resident threads per SM */
-        for (int k = 0; k < 4; k++) {
+        {
             int b = 0;
-            if (!d.occupancy || d.occupancy(&b, fn[k], B, k < 2 ? smem : 0) != CUDA_SUCCESS || b < 1) b = 1;
+            if (!d.occupancy || d.occupancy(&b, fn, B, smem) != CUDA_SUCCESS || b < 1) b = 1;
             bps = std::min(bps, b);
         }
         if (bps * B < 1024 && B != 256) {
             if (d.moduleUnload) d.moduleUnload(mod);
             continue;
         }
-        cfg.jmod = mod;
-        cfg.jsmem = smem;
-        cfg.jfunc = fn[0];
-        cfg.jfunc_r = fn[1];
-        cfg.jfunc_g = fn[2];
-        cfg.jfunc_gr = fn[3];
-        /* ALU-heavy single programs (a bounded loop: > 64 instructions on the worst path) keep
-         * per-lane register ingest -- the ring's per-record bookkeeping costs more than it hides */
-        uint64_t worst = 0;
-        for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
-        cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
-        cfg.jblock = (uint32_t)B;
-        cfg.jgrid = (uint32_t)rt->nsm * (uint32_t)bps;
+        V.mod = mod;
+        V.fn = fn;
+        V.smem = smem;
+        V.block = (uint32_t)B;
+        V.grid = (uint32_t)rt->nsm * (uint32_t)bps;
         break;
     }
-    cfg.jit_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    /* ALU-heavy single programs (a bounded loop: > 64 instructions on the worst path) keep
+     * per-lane register ingest -- the ring's per-record bookkeeping costs more than it hides */
+    uint64_t worst = 0;
+    for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
+    cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
+    cfg.jit_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return 0;
+}
+
+/* the launch variant a batch takes: the TMA ring for large batches (>= 2^22 events) of light
+ * programs, per-lane register loads otherwise (GX_JIT_INGEST=ring|reg forces one;
+ * profiles/r1_jit_variants.md) */
+int jit_variant(const LaunchCfg &cfg, uint64_t n, bool want_ret) {
+    const char *fe = getenv("GX_JIT_INGEST");
+    const int force = !fe ? 0 : strcmp(fe, "ring") == 0 ? 1 : strcmp(fe, "reg") == 0 ? 2 : 0;
+    const bool ring = force == 1 || (force == 0 && cfg.ring_ok && n >= (1ull << 22));
+    return (ring ? 0 : 2) + (want_ret ? 1 : 0);
 }
 
 /* a publish point on `stream` after the batch's kernel: take a free slot (wait for the daemon if
@@ -522,8 +527,15 @@ void daemon_main(gx_rt *rt) {
 int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream,
                uint32_t flags = 0) {
     if (rt->engine == GX_ENGINE_JIT) {
-        int rc = jit_prepare(rt, cfg);
+        if (!cfg.jv[0].tried && !cfg.jv[1].tried && !cfg.jv[2].tried && !cfg.jv[3].tried) {
+            uint64_t worst = 0; /* ring_ok before the first compile (jit_prepare sets it too) */
+            for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
+            cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
+        }
+        const int vk = jit_variant(cfg, n, d_ret != nullptr);
+        int rc = jit_prepare(rt, cfg, vk);
         if (rc) return rc;
+        const LaunchCfg::JitVar &V = cfg.jv[vk];
         const void *ev = d_events;
         uint64_t nn = n;
         uint64_t *rp = d_ret;
@@ -533,18 +545,13 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
          * privatised-shard flush do not dominate; large batches: the resident grid */
         static const uint64_t per_thread = getenv("GX_JIT_EPT") ? strtoull(getenv("GX_JIT_EPT"), nullptr, 10) : 8;
         static const uint64_t cap = getenv("GX_JIT_GRID") ? strtoull(getenv("GX_JIT_GRID"), nullptr, 10) : ~0ull;
-        const uint64_t B = cfg.jblock;
+        const uint64_t B = V.block;
         uint64_t want = (n + B * per_thread - 1) / (B * per_thread);
-        if (want * 2 >= cfg.jgrid) want = cfg.jgrid; /* past half the resident grid: every SM streams */
+        if (want * 2 >= V.grid) want = V.grid; /* past half the resident grid: every SM streams */
         want = std::min<uint64_t>(cap, want);
-        uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cfg.jgrid, want));
-        /* ingest: the TMA ring for large batches (>= 2^22 events) of light programs, per-lane register
-         * loads otherwise (GX_JIT_INGEST=ring|reg forces one; profiles/r1_jit_variants.md) */
-        const char *fe = getenv("GX_JIT_INGEST");
-        const int force = !fe ? 0 : strcmp(fe, "ring") == 0 ? 1 : strcmp(fe, "reg") == 0 ? 2 : 0;
-        const bool ring = force == 1 || (force == 0 && cfg.ring_ok && n >= (1ull << 22));
-        CUfunction fnl = ring ? (d_ret ? cfg.jfunc_r : cfg.jfunc) : (d_ret ? cfg.jfunc_gr : cfg.jfunc_g);
-        const unsigned smem = ring ? cfg.jsmem : 0u;
+        uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(V.grid, want));
+        CUfunction fnl = V.fn;
+        const unsigned smem = V.smem;
         if ((flags & GX_RUN_OVERLAP) && drv().launchKernelEx) {
             /* programmatic dependent launch: the grid may start while the previous kernel on the
              * stream drains; it stages its first records, then griddepcontrol.wait holds every map
@@ -630,7 +637,8 @@ void gx_close(gx_rt *rt) {
     for (auto &p : rt->progs) cudaFree(p.d_image);
     for (auto &kv : rt->launches) {
         cudaFree(kv.second.d);
-        if (kv.second.jmod && drv().moduleUnload) drv().moduleUnload(kv.second.jmod);
+        for (auto &v : kv.second.jv)
+            if (v.mod && drv().moduleUnload) drv().moduleUnload(v.mod);
     }
     cudaFree(rt->d_stats);
     if (rt->pipe_init) {
@@ -994,7 +1002,9 @@ int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *
     h.single = 0;
     std::vector<const GxInsn *> images{vr.image.data()};
     std::vector<uint32_t> sizes{(uint32_t)vr.image.size()};
-    std::string s = gx_jit_source(h, images, sizes, gx_jit_block());
+    unsigned vmask = GX_JIT_V_ALL; /* GX_JIT_VMASK: the launch variants to generate (GX_JIT_V_* bits) */
+    if (const char *e = getenv("GX_JIT_VMASK")) vmask = (unsigned)strtoul(e, nullptr, 0) & GX_JIT_V_ALL;
+    std::string s = gx_jit_source(h, images, sizes, gx_jit_block(), vmask ? vmask : GX_JIT_V_ALL);
     if (src && src_len) {
         size_t k = std::min<size_t>(src_len - 1, s.size());
         memcpy(src, s.data(), k);

@@ -1437,10 +1437,10 @@ struct Verifier {
             if (mi.type == RINGBUF || mi.type == PFQ)
                 return fail(pc, GX_BAD_HELPER, "map lookup/update on a ring buffer / prefetch queue");
             if (!check_arg_mem(pc, st, st.r[2], mi.key_size, mi.key_size, "key", kk, ka)) return false;
-            if (kk == MK_MAPV) out.use[st.r[2].map].reads = true;
+            if (kk == MK_MAPV) out.use[st.r[2].map].reads = out.use[st.r[2].map].used = true;
             if (id == 2) {
                 if (!check_arg_mem(pc, st, st.r[3], mi.value_size, 8, "value", vk, va)) return false;
-                if (vk == MK_MAPV) out.use[st.r[3].map].reads = true;
+                if (vk == MK_MAPV) out.use[st.r[3].map].reads = out.use[st.r[3].map].used = true;
                 Reg &R4 = st.r[4];
                 if (R4.type != SCALAR) return fail(pc, R4.type == NOT_INIT ? GX_UNINIT_READ : GX_BAD_HELPER, "flags must be a scalar");
                 u.writes = u.non_add_write = u.update_call = true;
@@ -1468,7 +1468,7 @@ struct Verifier {
             rbs = (int64_t)R3.var.t.v;
             rbf = (int64_t)R4.var.t.v;
             if (!check_arg_mem(pc, st, st.r[2], (uint32_t)rbs, 8, "ringbuf data", vk, va)) return false;
-            if (vk == MK_MAPV) out.use[st.r[2].map].reads = true;
+            if (vk == MK_MAPV) out.use[st.r[2].map].reads = out.use[st.r[2].map].used = true;
             u.writes = true;
             P.ch += 1;
         }

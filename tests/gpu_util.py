@@ -35,12 +35,12 @@ def oracle_run(config, ev, threshold=None):
 ENGINES = ("interp", "jit", "jit_ring")
 
 
-def make_runtime(engine="jit"):
+def make_runtime(engine="jit", set_env=True):
     import os
     import paper_2512_12615_b200 as gx
-    if engine == "jit_ring":
+    if set_env and engine == "jit_ring":
         os.environ["GX_JIT_INGEST"] = "ring"
-    else:
+    elif set_env:
         os.environ.pop("GX_JIT_INGEST", None)
     return gx.Runtime(0, engine=gx.GX_ENGINE_INTERP if engine == "interp" else gx.GX_ENGINE_JIT)
 
