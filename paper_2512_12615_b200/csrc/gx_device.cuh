@@ -327,11 +327,12 @@ __device__ __forceinline__ int64_t pfq_request_coop(const GxMapDesc &md, uint64_
      * whose filter word already holds it was queued earlier in this drain epoch -- set semantics
      * let it go; a plain load first keeps hot requests off the atomic unit */
     bool dup = false;
+    unsigned long long *fw = nullptr;
+    const unsigned long long tag = key + 1;
     if (head) {
         unsigned long long *filt =
             reinterpret_cast<unsigned long long *>(md.data + 16ull * ((uint64_t)md.cap_mask + 1));
-        unsigned long long *fw = filt + (mix64(key) & (md.nshards - 1));
-        const unsigned long long tag = key + 1;
+        fw = filt + (mix64(key) & (md.nshards - 1));
         dup = ld_relaxed(reinterpret_cast<const uint64_t *>(fw)) == tag || atomicExch(fw, tag) == tag;
         head = !dup;
     }
@@ -350,6 +351,9 @@ __device__ __forceinline__ int64_t pfq_request_coop(const GxMapDesc &md, uint64_
         d[0] = first;
         d[1] = np;
     }
+    /* a dropped request was not queued: take it back out of the filter so a repeat is refused
+     * (-EAGAIN, counted) like the oracle's, not passed as a duplicate */
+    if (head && !ok) atomicCAS(fw, tag, 0ull);
     if (!me) return 0;
     if (!valid) return -(int64_t)E_INVAL;
     if (dup_g) return 0;

@@ -667,7 +667,13 @@ struct Gen {
             if (const char *e = getenv("GX_JIT_HASH_CACHE")) ncache = (uint32_t)atoi(e);
             if (ncache & (ncache - 1)) ncache = 0;
             hc_map_ = -1;
-            hc_n_ = std::min<uint32_t>(ncache, 2048); /* 32 KiB of static shared memory at most (48-KiB static limit) */
+            /* static shared memory stays under the 48-KiB static limit: the privatised accumulators
+             * (spriv), the stats, the ring barriers and the key cache (16 B per entry) share it */
+            const uint32_t fixed = 4u * ((L.priv_bytes + 3) / 4) + 1024u;
+            const uint32_t room = fixed < 48u * 1024u ? (48u * 1024u - fixed) / 16u : 0u;
+            hc_n_ = std::min<uint32_t>(ncache, 2048);
+            while (hc_n_ && hc_n_ > room) hc_n_ >>= 1;
+            if (hc_n_ < 64) hc_n_ = 0; /* too small to pay for itself */
             for (size_t q = 0; q < images.size() && hc_n_ && hc_map_ < 0; q++)
                 for (uint32_t i = 0; i < sizes[q]; i++)
                     if (images[q][i].op == GX_CALL_LOOKUP_HASH && L.maps[images[q][i].aux].value_size == 8) {
@@ -699,6 +705,12 @@ struct Gen {
      * is converged): the helpers' warp collectives need the exact set of lanes that reach them.
      * The ctx is built in registers from the call site; per-thread shards are keyed by the
      * hardware slot (SM, warp slot, lane), unique among resident threads. */
+    uint32_t pt_shards_min() const {
+        uint32_t v = ~0u;
+        for (int m = 0; m < GX_MAX_MAPS; m++)
+            if (L.maps[m].type == 6 /* PERTHREAD_ARRAY */ && L.maps[m].nshards) v = std::min(v, L.maps[m].nshards);
+        return v == ~0u ? 1u << 30 : v;
+    }
     void instrument(const GxInsn *image, uint32_t n, const std::string &user) {
         ptc_ = false;
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
@@ -715,7 +727,9 @@ struct Gen {
              "  Ctx c;\n"
              "  c.w[0] = (uint32_t)addr; c.w[1] = (uint32_t)(addr >> 32); c.w[2] = (uint32_t)ts; c.w[3] = (uint32_t)(ts >> 32);\n"
              "  c.w[4] = hook; c.w[5] = blk; c.w[6] = (smid & 0xFFFF) | ((wslot & 63) << 16) | (lane << 24); c.w[7] = size;\n"
-             "  const uint32_t shard = (smid * 64 + (wslot & 63)) * 32 + lane;\n"
+             "  /* unique among resident threads; the shards are sized from %nsmid (gx_open), the modulo\n"
+             "   * only keeps a device that reports more SM ids than that inside the map */\n"
+             "  const uint32_t shard = ((smid * 64 + (wslot & 63)) * 32 + lane) % " << pt_shards_min() << "u;\n"
              "  uint64_t retv = 0;\n"
              "  unsigned long long herr = 0, drop = 0, rbb = 0, hfull = 0;\n"
              "  PtCache ptc;\n"

@@ -255,3 +255,20 @@ int gx_k_hash_accumulate(const GxMapDesc *m, const uint64_t *keys, const uint64_
 }
 
 }  // extern "C"
+
+/* %nsmid: one more than the largest %smid the device can report (PTX: SM ids need not be
+ * contiguous) -- sizes the per-thread shards the f4 hooks key by (SM, warp slot, lane) */
+__global__ void nsmid_kernel(uint32_t *out) {
+    uint32_t v;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+    *out = v;
+}
+int gx_k_nsmid(uint32_t *out_host) {
+    uint32_t *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4);
+    if (e) return (int)e;
+    nsmid_kernel<<<1, 1>>>(d);
+    e = cudaMemcpy(out_host, d, 4, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return (int)e;
+}

@@ -36,6 +36,7 @@ int gx_launch_exec(const GxLaunch *d_launch, const void *d_events, uint64_t n, u
 int gx_exec_occupancy(uint32_t smem, int *blocks_per_sm);
 uint32_t gx_exec_block_threads();
 int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint64_t *out, cudaStream_t s);
+int gx_k_nsmid(uint32_t *out_host);
 int gx_k_pt_set(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint32_t k, const uint64_t *vals,
                 cudaStream_t s);
 int gx_k_pt_store_canonical(uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, const uint64_t *vals,
@@ -610,7 +611,13 @@ int gx_open(int cuda_device, gx_rt **out) {
     gx_rt *rt = new gx_rt();
     rt->dev = cuda_device;
     rt->nsm = prop.multiProcessorCount;
-    rt->max_shards = (uint32_t)rt->nsm * 2048; /* one shard per resident thread slot (2048 / SM) */
+    /* one shard per resident thread slot (2048 / SM); f4 hooks key shards by (%smid, %warpid, lane),
+     * and %smid ranges over [0, %nsmid), which may exceed the SM count */
+    {
+        uint32_t nsmid = 0;
+        if (gx_k_nsmid(&nsmid) != 0) nsmid = 0;
+        rt->max_shards = (uint32_t)std::max<int>(rt->nsm, (int)nsmid) * 2048;
+    }
     if (const char *e = getenv("GX_ENGINE")) rt->engine = strcmp(e, "interp") == 0 ? GX_ENGINE_INTERP : GX_ENGINE_JIT;
     for (auto &row : rt->attach)
         for (int &x : row) x = -1;
