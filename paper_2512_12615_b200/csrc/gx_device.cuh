@@ -51,70 +51,68 @@ __device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-/* 128-bit compare-and-swap of a {key, value} hash slot (PTX atom.cas.b128, sm_90+): publishes
- * key and value in one indivisible step so a reader that sees the key sees its value. */
-__device__ __forceinline__ void cas128(uint64_t *a, uint64_t cmp_lo, uint64_t cmp_hi, uint64_t new_lo,
-                                       uint64_t new_hi, uint64_t &old_lo, uint64_t &old_hi) {
-    asm volatile(
-        "{\n\t.reg .b128 d, b, c;\n\t"
-        "mov.b128 b, {%2, %3};\n\t"
-        "mov.b128 c, {%4, %5};\n\t"
-        "atom.global.cas.b128 d, [%6], b, c;\n\t"
-        "mov.b128 {%0, %1}, d;\n\t}"
-        : "=l"(old_lo), "=l"(old_hi)
-        : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(a)
-        : "memory");
+/* ---- HASH: open addressing, linear probing, keys and values in SEPARATE arrays of cap + 2 words
+ * (cap = cap_mask + 1, a power of two >= 2 x max_entries):
+ *     data[0 .. cap+1]            key words K: EMPTY (all-ones), BUSY (all-ones - 1: an insert in
+ *                                 flight) or a published key; K[cap] / K[cap+1] are the presence
+ *                                 states (0 absent, 2 inserting, 1 present) of the two keys that
+ *                                 equal the sentinels, whose entries live in these side slots;
+ *     data[cap+2 .. 2 cap+3]      value words V, V[i] belonging to K[i].
+ * Values sit on lines of their own: the map's atomics (a hot LFU page takes millions of FETCH-ADDs
+ * per batch) never contend with the probes that read keys (C3: 17 -> ~8 ms at 2^28 events,
+ * profiles/r2_c3.md).  An insert claims a slot EMPTY -> BUSY (CAS), writes the value, and publishes
+ * the key with a release store; a published key never changes (no deletes). */
+constexpr uint64_t GX_HASH_BUSY = 0xFFFFFFFFFFFFFFFEull;
+__device__ __forceinline__ uint64_t *hash_keys(const GxMapDesc &m) { return reinterpret_cast<uint64_t *>(m.data); }
+__device__ __forceinline__ uint64_t *hash_vals(const GxMapDesc &m) {
+    return reinterpret_cast<uint64_t *>(m.data) + (uint64_t)m.cap_mask + 3;
+}
+__device__ __forceinline__ void st_release(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-/* ---- HASH (open addressing, linear probing; slot = {u64 key, u64 value}; EMPTY key = all-ones;
- * the all-ones key itself lives in a side slot at index cap whose key word is a present flag) */
+/* lookup: the value word of `key`, or nullptr.  An insert still in flight (BUSY) is not yet in the
+ * map: a slot that was EMPTY when a probe for `key` passed it cannot be followed by `key`, so BUSY
+ * ends the chain like EMPTY. */
 __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key) {
-    uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
+    uint64_t *K = hash_keys(m), *V = hash_vals(m);
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    if (key == GX_HASH_EMPTY) {
-        uint64_t *side = slots + 2 * cap;
-        return ld_acquire(side) == 1 ? side + 1 : nullptr;
+    if (key == GX_HASH_EMPTY || key == GX_HASH_BUSY) {
+        const uint64_t side = cap + (key == GX_HASH_BUSY ? 1 : 0);
+        return ld_acquire(K + side) == 1 ? V + side : nullptr;
     }
-    /* relaxed gpu-scope probes: coherent at L2 without the L1 invalidation an acquire costs; the
-     * slot was published by one 16-B atomic, and the value is only read after the key compare
-     * resolved (no load speculation on the GPU) */
-    /* one slot per probe step: a 4-wide step (keys of 4 slots per round trip) measured 1.7x slower
-     * on C3 -- 4x the L2 requests, and the neighbours of hot slots are under atomic traffic */
+    /* one slot per probe step: a 4-wide step measured 1.7x slower on C3 (round 1) */
     uint64_t h = mix64(key) & m.cap_mask;
 #if GX_HASH_L1PROBE == 1
     /* home slot only through L1 (a key match there is final), then the coherent chain */
-    {
-        uint64_t *s = slots + 2 * h;
-        if (ld_ca(s) == key) return s + 1;
-    }
+    if (ld_ca(K + h) == key) return V + h;
     for (uint64_t i = 0; i < cap; i++) {
-        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
-        uint64_t k = ld_relaxed(s);
-        if (k == key) return s + 1;
-        if (k == GX_HASH_EMPTY) return nullptr;
+        const uint64_t s = (h + i) & m.cap_mask;
+        const uint64_t k = ld_acquire(K + s);
+        if (k == key) return V + s;
+        if (k >= GX_HASH_BUSY) return nullptr;
     }
 #elif GX_HASH_L1PROBE
-    /* a slot's key word never changes once published (no deletes), so any NON-EMPTY key read through
-     * L1 is final -- a match is the entry, another key means probe on; only an EMPTY read may be
-     * stale and is re-read coherently at L2.  Chains over hot keys (C3's decode trace) then walk in
-     * L1 instead of at their L2 slices. */
+    /* a published key never changes, so any key read through L1 is final -- a match is the entry,
+     * another key means probe on; only EMPTY / BUSY may be stale and are re-read at L2 (acquire:
+     * the value written before the key's release is then visible) */
     for (uint64_t i = 0; i < cap; i++) {
-        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
+        const uint64_t s = (h + i) & m.cap_mask;
 #if GX_HASH_L1PROBE == 3
-        uint64_t k = ld_nc(s); /* read-only path: a stale EMPTY is re-read below like any other */
+        uint64_t k = ld_nc(K + s);
 #else
-        uint64_t k = ld_ca(s);
+        uint64_t k = ld_ca(K + s);
 #endif
-        if (k == GX_HASH_EMPTY) k = ld_relaxed(s);
-        if (k == key) return s + 1;
-        if (k == GX_HASH_EMPTY) return nullptr;
+        if (k >= GX_HASH_BUSY) k = ld_acquire(K + s);
+        if (k == key) return V + s;
+        if (k >= GX_HASH_BUSY) return nullptr;
     }
 #else
     for (uint64_t i = 0; i < cap; i++) {
-        uint64_t *s = slots + 2 * ((h + i) & m.cap_mask);
-        uint64_t k = ld_relaxed(s);
-        if (k == key) return s + 1;
-        if (k == GX_HASH_EMPTY) return nullptr;
+        const uint64_t s = (h + i) & m.cap_mask;
+        const uint64_t k = ld_acquire(K + s);
+        if (k == key) return V + s;
+        if (k >= GX_HASH_BUSY) return nullptr;
     }
 #endif
     return nullptr;
@@ -127,7 +125,8 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
  * refused for capacity (hash_full).
  * Capacity (max_entries, exact): aux[1] counts committed entries, aux[2] reservations (committed +
  * in-flight inserts).  An insert of an absent key first reserves (aux[2]++); a reservation below
- * max_entries may publish its slot (16-B CAS) and then commits (aux[1]++); a lost CAS returns the
+ * max_entries may claim its slot (EMPTY -> BUSY), write the value, publish the key and then commit
+ * (aux[1]++); a lost claim returns the
  * reservation and probes again (the winner may hold our key).  With no reservation to be had: if the
  * committed count has reached max_entries the map is full for good, and one more probe that still
  * finds the key absent refuses the insert (-E2BIG, linearised at that probe); otherwise other inserts
@@ -147,24 +146,28 @@ __device__ __forceinline__ int hash_step(const GxMapDesc &m, uint64_t key, uint6
         rc = -E_INVAL;
         return kHashDone;
     }
-    uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
+    uint64_t *K = hash_keys(m), *V = hash_vals(m);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(m.aux);
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    uint64_t *s = nullptr;
+    const bool side = key == GX_HASH_EMPTY || key == GX_HASH_BUSY;
+    uint64_t s = 0;
     bool present = false;
-    if (key == GX_HASH_EMPTY) {
-        s = slots + 2 * cap;
-        present = ld_acquire(s) == 1;
+    if (side) {
+        s = cap + (key == GX_HASH_BUSY ? 1 : 0);
+        const uint64_t st8 = ld_acquire(K + s);
+        if (st8 == 2) return kHashWait; /* its insert is in flight */
+        present = st8 == 1;
     } else {
         const uint64_t h = mix64(key) & m.cap_mask;
         uint64_t i = 0;
         for (; i < cap; i++) {
-            s = slots + 2 * ((h + i) & m.cap_mask);
-            const uint64_t k = ld_acquire(s);
+            s = (h + i) & m.cap_mask;
+            const uint64_t k = ld_acquire(K + s);
             if (k == key) {
                 present = true;
                 break;
             }
+            if (k == GX_HASH_BUSY) return kHashWait; /* an insert in flight: it may be this key */
             if (k == GX_HASH_EMPTY) break;
         }
         if (i == cap) {
@@ -175,7 +178,7 @@ __device__ __forceinline__ int hash_step(const GxMapDesc &m, uint64_t key, uint6
     }
     if (present) {
         if (flags == 1) rc = -E_EXIST;
-        else st_relaxed(s + 1, val);
+        else st_relaxed(V + s, val);
         return kHashDone;
     }
     if (flags == 2) {
@@ -201,11 +204,10 @@ __device__ __forceinline__ int hash_step(const GxMapDesc &m, uint64_t key, uint6
         }
         return kHashWait;
     }
-    const uint64_t empty = key == GX_HASH_EMPTY ? 0 : GX_HASH_EMPTY;
-    const uint64_t tag = key == GX_HASH_EMPTY ? 1 : key;
-    uint64_t ol, oh;
-    cas128(s, empty, 0, tag, val, ol, oh);
-    if (ol == empty && oh == 0) {
+    const unsigned long long from = side ? 0ull : GX_HASH_EMPTY, busy = side ? 2ull : GX_HASH_BUSY;
+    if (atomicCAS(reinterpret_cast<unsigned long long *>(K + s), from, busy) == from) {
+        st_relaxed(V + s, val);
+        st_release(K + s, side ? 1ull : key);
         atomicAdd(&ctr[1], 1ull);
         return kHashDone;
     }

@@ -658,6 +658,7 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PIN")) o << "#define GX_PIN " << atoi(e) << "\n";
+        if (const char *e = getenv("GX_JIT_ATOM_MIXED")) o << "#define GX_ATOM_MIXED " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot

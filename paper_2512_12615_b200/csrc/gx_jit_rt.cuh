@@ -334,13 +334,15 @@ __device__ __forceinline__ uint64_t global_atomic(uint32_t op, uint64_t addr, ui
  * line: __match_any_sync groups, one L2 atomic per distinct address; FETCH lanes get old + their
  * exclusive prefix in lane order -- the group's sequential result (the lanes of a record are
  * consecutive events). */
+#ifndef GX_ATOM_MIXED
+#define GX_ATOM_MIXED 0
+#endif
 template <uint32_t OP, bool W32, bool FETCH>
-__device__ __noinline__ uint64_t group_atomic_slow(unsigned mask, uint64_t addr, uint64_t v) {
-    /* lanes grouped by address: one L2 atomic per distinct address carrying the group's reduced
-     * value; FETCH lanes get old + their exclusive prefix in lane order */
+__device__ __noinline__ uint64_t group_atomic_walk(unsigned peers, uint64_t addr, uint64_t v) {
+    /* the lanes of `peers` share `addr` (a __match_any_sync group of two or more): one L2 atomic
+     * carrying the group's reduced value; FETCH lanes get old + their exclusive prefix in lane order */
     const unsigned lane = threadIdx.x & 31;
     constexpr uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
-    const unsigned peers = __match_any_sync(mask, addr);
     const unsigned gl = __ffs(peers) - 1;
     uint64_t pre = ident, tot = ident;
     for (unsigned m = peers; m; m &= m - 1) {
@@ -362,7 +364,7 @@ __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, u
     const unsigned leader = __ffs(mask) - 1;
     const uint64_t a0 = __shfl_sync(mask, addr, leader);
     constexpr uint64_t ident = (OP & 0xF0) == 0x50 ? ~0ull : 0;
-    /* the inline fast paths: one address for the whole group (record-uniform keys) */
+    /* one address for the whole group (record-uniform keys) */
     if (__all_sync(mask, addr == a0) && (!FETCH || mask == 0xFFFFFFFFu)) {
         if (!FETCH) {
             const uint64_t agg = group_reduce(mask, OP, v, W32);
@@ -385,8 +387,42 @@ __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, u
         const uint64_t r = apply_op(OP, old, exc);
         return W32 ? (uint32_t)r : r;
     }
-    /* mixed addresses or a partial FETCH group: out of line */
-    return group_atomic_slow<OP, W32, FETCH>(mask, addr, v);
+    /* mixed addresses: lanes grouped by address.  A lane alone on its address (most lanes of a
+     * random-key record) issues its own atomic -- no shuffles; groups of two or more take the
+     * out-of-line walk */
+#if GX_ATOM_MIXED == 1
+    /* per-lane atomics: the L1/TEX unit merges same-address lanes of one instruction itself */
+    {
+        const uint64_t r = global_atomic(OP, addr, v, W32, FETCH);
+        return W32 ? (uint32_t)r : r;
+    }
+#elif GX_ATOM_MIXED == 2
+    /* the whole warp walks its address groups (no divergence) */
+    {
+        const unsigned peers = __match_any_sync(mask, addr);
+        const unsigned gl = __ffs(peers) - 1;
+        uint64_t pre = ident, tot = ident;
+        for (unsigned m = peers; m; m &= m - 1) {
+            const int jl = __ffs(m) - 1;
+            const uint64_t vj = __shfl_sync(peers, v, jl);
+            if (jl < (int)lane) pre = apply_op(OP, pre, vj);
+            tot = apply_op(OP, tot, vj);
+        }
+        uint64_t old = 0;
+        if (lane == gl) old = global_atomic(OP, addr, tot, W32, FETCH);
+        if (!FETCH) return 0;
+        old = __shfl_sync(peers, old, gl);
+        const uint64_t r = apply_op(OP, old, pre);
+        return W32 ? (uint32_t)r : r;
+    }
+#else
+    const unsigned peers = __match_any_sync(mask, addr);
+    if (peers == (1u << lane)) {
+        const uint64_t r = global_atomic(OP, addr, v, W32, FETCH);
+        return W32 ? (uint32_t)r : r;
+    }
+    return group_atomic_walk<OP, W32, FETCH>(peers, addr, v);
+#endif
 }
 
 /* XCHG on a shared map value.  Lanes on one address take the sequential result in lane order (the
@@ -598,11 +634,11 @@ __device__ __forceinline__ uint64_t *hc_find(const GxMapDesc &m, uint64_t key, u
     if (key == GX_HASH_EMPTY || key == HC_RESV) return gxd::hash_find(m, key);
     unsigned long long *e = hc + 2 * ((uint32_t)(gxd::mix64(key) >> 40) & (NC - 1));
     const uint64_t ek = hc_ld_acq(e);
-    uint64_t *slots = reinterpret_cast<uint64_t *>(m.data);
-    if (ek == key) return slots + 2 * e[1] + 1;
+    uint64_t *vals = gxd::hash_vals(m);
+    if (ek == key) return vals + e[1];
     uint64_t *v = gxd::hash_find(m, key);
     if (v && ek == GX_HASH_EMPTY && atomicCAS(e, GX_HASH_EMPTY, HC_RESV) == GX_HASH_EMPTY) {
-        e[1] = (unsigned long long)((v - 1 - slots) >> 1);
+        e[1] = (unsigned long long)(v - vals);
         hc_st_rel(e, key);
     }
     return v;

@@ -98,11 +98,12 @@ __global__ void publish_reset_kernel(const GxPublishItem *__restrict__ items) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<unsigned long long *>(it.aux) = 0;
 }
 
-__global__ void hash_init_kernel(uint64_t *slots, uint64_t cap) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
+__global__ void hash_init_kernel(uint64_t *data, uint64_t cap) {
+    /* key words EMPTY, the two side-slot presence states 0, value words 0 (gx_device.cuh layout) */
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 2;
          i += gridDim.x * (uint64_t)blockDim.x) {
-        slots[2 * i] = i < cap ? GX_HASH_EMPTY : 0; /* side slot: present flag 0 */
-        slots[2 * i + 1] = 0;
+        data[i] = i < cap ? GX_HASH_EMPTY : 0;
+        data[cap + 2 + i] = 0;
     }
 }
 
@@ -130,15 +131,14 @@ __global__ void add_kernel(const uint64_t *a, const uint64_t *b, uint64_t *out, 
  * owner = mix64(key) mod nranks.  Pass 0 counts per owner, pass 1 scatters at per-owner offsets. */
 __device__ __forceinline__ bool export_entry(const GxMapDesc &m, const GxMapDesc &base, uint64_t i, uint64_t &k,
                                              uint64_t &d) {
-    const uint64_t *slots = reinterpret_cast<const uint64_t *>(m.data);
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    k = slots[2 * i];
-    const uint64_t v = slots[2 * i + 1];
+    k = gxd::hash_keys(m)[i];
+    const uint64_t v = gxd::hash_vals(m)[i];
     if (i < cap) {
-        if (k == GX_HASH_EMPTY) return false;
+        if (k >= gxd::GX_HASH_BUSY) return false;
     } else {
         if (k != 1) return false;
-        k = GX_HASH_EMPTY;
+        k = i == cap ? GX_HASH_EMPTY : gxd::GX_HASH_BUSY; /* side slots */
     }
     const uint64_t *bv = gxd::hash_find(base, k);
     d = v - (bv ? *bv : 0);
@@ -148,7 +148,7 @@ __global__ void hash_export_kernel(GxMapDesc m, GxMapDesc base, uint32_t nranks,
                                    unsigned long long *counts, unsigned long long *offsets, uint64_t *keys,
                                    uint64_t *deltas, uint64_t cap_out) {
     const uint64_t cap = (uint64_t)m.cap_mask + 1;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap + 2;
          i += gridDim.x * (uint64_t)blockDim.x) {
         uint64_t k, d;
         if (!export_entry(m, base, i, k, d)) continue;
@@ -192,6 +192,14 @@ inline uint32_t grid_for(uint64_t n, uint32_t block) {
 
 }  // namespace
 
+/* %nsmid: one more than the largest %smid the device can report (PTX: SM ids need not be
+ * contiguous) -- sizes the per-thread shards the f4 hooks key by (SM, warp slot, lane) */
+__global__ void nsmid_kernel(uint32_t *out) {
+    uint32_t v;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+    *out = v;
+}
+
 extern "C" {
 
 int gx_k_pt_fold(const uint64_t *data, uint32_t nshards, uint32_t K, uint32_t W, uint64_t *out, cudaStream_t s) {
@@ -225,7 +233,7 @@ int gx_k_publish(const GxPublishItem *items, uint32_t n_items, uint8_t *host_slo
 }
 
 int gx_k_hash_init(uint64_t *slots, uint64_t cap, cudaStream_t s) {
-    hash_init_kernel<<<grid_for(cap + 1, 256), 256, 0, s>>>(slots, cap);
+    hash_init_kernel<<<grid_for(cap + 2, 256), 256, 0, s>>>(slots, cap);
     return (int)cudaGetLastError();
 }
 int gx_k_hash_host_update(const GxMapDesc *m, const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t flags,
@@ -244,7 +252,7 @@ int gx_k_add(const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, cu
 int gx_k_hash_export(const GxMapDesc *m, const GxMapDesc *base, uint32_t nranks, int32_t owner, int pass,
                      unsigned long long *counts, unsigned long long *offsets, uint64_t *keys, uint64_t *deltas,
                      uint64_t cap_out, cudaStream_t s) {
-    hash_export_kernel<<<grid_for((uint64_t)m->cap_mask + 2, 256), 256, 0, s>>>(*m, *base, nranks, owner, pass, counts,
+    hash_export_kernel<<<grid_for((uint64_t)m->cap_mask + 3, 256), 256, 0, s>>>(*m, *base, nranks, owner, pass, counts,
                                                                                offsets, keys, deltas, cap_out);
     return (int)cudaGetLastError();
 }
@@ -254,15 +262,6 @@ int gx_k_hash_accumulate(const GxMapDesc *m, const uint64_t *keys, const uint64_
     return (int)cudaGetLastError();
 }
 
-}  // extern "C"
-
-/* %nsmid: one more than the largest %smid the device can report (PTX: SM ids need not be
- * contiguous) -- sizes the per-thread shards the f4 hooks key by (SM, warp slot, lane) */
-__global__ void nsmid_kernel(uint32_t *out) {
-    uint32_t v;
-    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
-    *out = v;
-}
 int gx_k_nsmid(uint32_t *out_host) {
     uint32_t *d = nullptr;
     cudaError_t e = cudaMalloc(&d, 4);
@@ -272,3 +271,5 @@ int gx_k_nsmid(uint32_t *out_host) {
     cudaFree(d);
     return (int)e;
 }
+
+}  // extern "C"

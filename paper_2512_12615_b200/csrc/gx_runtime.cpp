@@ -696,7 +696,7 @@ int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
         uint64_t cap = 16;
         while (cap < 2ull * s.max_entries) cap <<= 1;
         m.cap = cap;
-        m.data_bytes = (cap + 1) * 16;
+        m.data_bytes = (cap + 2) * 16; /* key words, then value words (gx_device.cuh) */
         break;
     }
     case GX_MAP_RINGBUF:
@@ -838,12 +838,16 @@ int gx_read_map(gx_rt *rt, int fd, void *keys, void *vals, uint64_t cap, uint64_
         return 0;
     }
     if (s.type == GX_MAP_HASH) {
-        std::vector<uint64_t> slots(2 * (m.cap + 1));
-        CK(cudaMemcpy(slots.data(), m.data, m.data_bytes, cudaMemcpyDeviceToHost), "read hash");
+        /* key words K[0 .. cap+1], then value words V (gx_device.cuh); K[cap] / K[cap+1] are the
+         * presence states of the all-ones and the all-ones - 1 key */
+        std::vector<uint64_t> w(2 * (m.cap + 2));
+        CK(cudaMemcpy(w.data(), m.data, m.data_bytes, cudaMemcpyDeviceToHost), "read hash");
+        const uint64_t *K = w.data(), *V = w.data() + m.cap + 2;
         std::vector<std::pair<uint64_t, uint64_t>> ent;
         for (uint64_t i = 0; i < m.cap; i++)
-            if (slots[2 * i] != GX_HASH_EMPTY) ent.push_back({slots[2 * i], slots[2 * i + 1]});
-        if (slots[2 * m.cap] == 1) ent.push_back({GX_HASH_EMPTY, slots[2 * m.cap + 1]});
+            if (K[i] < GX_HASH_EMPTY - 1) ent.push_back({K[i], V[i]});
+        if (K[m.cap] == 1) ent.push_back({GX_HASH_EMPTY, V[m.cap]});
+        if (K[m.cap + 1] == 1) ent.push_back({GX_HASH_EMPTY - 1, V[m.cap + 1]});
         std::sort(ent.begin(), ent.end());
         if (ent.size() > cap) return -E2BIG;
         for (size_t i = 0; i < ent.size(); i++) {

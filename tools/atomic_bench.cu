@@ -38,6 +38,15 @@ __global__ void kern(unsigned long long *buf, uint64_t mask, int iters, unsigned
         if (MODE == 5) acc += atomicAdd(&buf[0], 1ull);                         // one address
         if (MODE == 6 && (threadIdx.x & 31) == 0) acc += atomicAdd(&buf[0], 32ull); // one address, one returning op per warp
         if (MODE == 7 && (threadIdx.x & 31) == 0) atomicAdd(&buf[0], 32ull);        // one address, one RED per warp
+        if (MODE == 8) {                                                        // dependent chain: one returning
+            uint64_t d = mix64(t * 0x9E3779B97F4A7C15ull + i + (acc >> 62));    // atomic in flight per thread
+            acc += atomicAdd(&buf[d & mask], 1ull);                             // (C3's per-record pattern)
+        }
+        if (MODE == 9) {                                                        // two dependent chains per thread
+            uint64_t d = mix64(t * 0x9E3779B97F4A7C15ull + i + (acc >> 62));
+            uint64_t e = mix64(d);
+            acc += atomicAdd(&buf[d & mask], 1ull) + atomicAdd(&buf[e & mask], 1ull);
+        }
     }
     if (acc == 0x123456789ull) sink[0] = acc;
 }
@@ -78,6 +87,10 @@ int main() {
     double r5 = run<5>(buf, words - 1, sink, sms, 16);
     double r6 = run<6>(buf, words - 1, sink, sms * 8, 16) / 32;   /* warp-level ops */
     double r7 = run<7>(buf, words - 1, sink, sms * 8, 16) / 32;
+    double r8a = run<8>(buf, words - 1, sink, sms * 4, 64), r8b = run<8>(buf, words - 1, sink, sms * 8, 64);
+    double r9a = run<9>(buf, words - 1, sink, sms * 4, 32) * 2, r9b = run<9>(buf, words - 1, sink, sms * 8, 32) * 2;
+    fprintf(stderr, "{\"dependent_chain_1024thr_per_s\": %.4g, \"dependent_chain_2048thr_per_s\": %.4g, "
+            "\"two_chains_1024thr_per_s\": %.4g, \"two_chains_2048thr_per_s\": %.4g}\n", r8a, r8b, r9a, r9b);
     printf("{\"device\": \"B200\", \"buffer_bytes\": %llu, \"atom_add_u64_random_per_s\": %.4g, "
            "\"red_add_u64_random_per_s\": %.4g, \"atom_cas_b64_random_per_s\": %.4g, "
            "\"atom_cas_b128_random_per_s\": %.4g, \"red_add_u64_warp_uniform_per_s\": %.4g, "
