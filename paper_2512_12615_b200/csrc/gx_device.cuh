@@ -37,6 +37,10 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
 #ifndef GX_HASH_L1PROBE
 #define GX_HASH_L1PROBE 2
 #endif
+/* keys per probe step with the L1 chain (1, 2 or 4) */
+#ifndef GX_HASH_PROBE_W
+#define GX_HASH_PROBE_W 4
+#endif
 __device__ __forceinline__ uint64_t ld_nc(const uint64_t *p) {
     uint64_t r;
     asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
@@ -95,7 +99,10 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
 #elif GX_HASH_L1PROBE
     /* a published key never changes, so any key read through L1 is final -- a match is the entry,
      * another key means probe on; only EMPTY / BUSY may be stale and are re-read at L2 (acquire:
-     * the value written before the key's release is then visible) */
+     * the value written before the key's release is then visible).  The chain is read one 32-B
+     * sector (4 key words, two 16-B loads, one L2 request) at a time in slot order: C3's chains of
+     * ~1.5 slots per lane took 3.4 serial round trips per warp record one slot at a time. */
+#if GX_HASH_PROBE_W == 1
     for (uint64_t i = 0; i < cap; i++) {
         const uint64_t s = (h + i) & m.cap_mask;
 #if GX_HASH_L1PROBE == 3
@@ -108,6 +115,45 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
         if (k >= GX_HASH_BUSY) return nullptr;
     }
 #else
+    constexpr uint32_t PW = GX_HASH_PROBE_W; /* 2 or 4 keys per step (16 or 32 B; a 32-B sector is one L2 request) */
+    unsigned valid = ((1u << PW) - 1) << ((uint32_t)h & (PW - 1)); /* the first step starts at the home slot */
+    for (uint64_t i = 0; i < cap; i += PW) {
+        const uint64_t b = ((h & ~(uint64_t)(PW - 1)) + i) & m.cap_mask;
+        uint64_t kk[PW];
+#pragma unroll
+        for (uint32_t q = 0; q < PW; q += 2) {
+#if GX_HASH_L1PROBE == 3
+            asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(kk[q]), "=l"(kk[q + 1]) : "l"(K + b + q));
+#else
+            asm volatile("ld.global.ca.v2.u64 {%0, %1}, [%2];" : "=l"(kk[q]), "=l"(kk[q + 1]) : "l"(K + b + q));
+#endif
+        }
+        /* branch-free scan of the step: the first slot (in probe order) holding the key or a
+         * sentinel decides */
+        unsigned hit = 0, stop = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < PW; j++) {
+            hit |= (kk[j] == key ? 1u : 0u) << j;
+            stop |= (kk[j] >= GX_HASH_BUSY ? 1u : 0u) << j;
+        }
+        hit &= valid;
+        stop &= valid;
+        valid = (1u << PW) - 1;
+        if (hit | stop) {
+            const uint32_t j = __ffs(hit | stop) - 1;
+            if ((hit >> j) & 1) return V + b + j;
+            /* EMPTY / BUSY read through L1 may be stale: re-read coherently; a key that arrived
+             * meanwhile continues the chain slot by slot (rare) */
+            for (uint64_t s = b + j, n = 0; n < cap; n++, s = (s + 1) & m.cap_mask) {
+                const uint64_t k = ld_acquire(K + s);
+                if (k == key) return V + s;
+                if (k >= GX_HASH_BUSY) return nullptr;
+            }
+            return nullptr;
+        }
+    }
+#endif
+#else
     for (uint64_t i = 0; i < cap; i++) {
         const uint64_t s = (h + i) & m.cap_mask;
         const uint64_t k = ld_acquire(K + s);
@@ -118,6 +164,9 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
     return nullptr;
 }
 
+#ifndef GX_HASH_LOCKSTEP
+#define GX_HASH_LOCKSTEP 0
+#endif
 #ifndef GX_HASH_VALVE
 #define GX_HASH_VALVE (1u << 20)
 #endif
@@ -234,7 +283,7 @@ __device__ __forceinline__ int64_t hash_update(const GxMapDesc &m, uint64_t key,
 
 /* JIT builds move the cold, code-heavy group paths out of line (one copy per module instead of one
  * per call site and per uniform / min-PC block copy); the interpreter keeps them inline. */
-#ifdef GX_JIT
+#if defined(GX_JIT) && !defined(GX_COLD_INLINE)
 #define GXD_COLD __noinline__
 #else
 #define GXD_COLD __forceinline__
@@ -267,19 +316,20 @@ __device__ __forceinline__ uint64_t *hash_lookup_coop(const GxMapDesc &m, uint64
  *              LAST lane performs the update with its value and every lane takes its result.
  * The doing lanes of the warp run their attempts in lock-step rounds (hash_step), so a lane waiting
  * for reservations never spins past a lane of its own warp that holds one. */
-__device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, uint64_t val, uint64_t flags,
-                                             bool &full, bool me, unsigned mask) {
-    full = false;
+__device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc m, uint64_t key, uint64_t val, uint64_t flags, bool me,
+                                             unsigned mask) {
     const unsigned part = __ballot_sync(mask, me);
     if (!me) return 0;
     const unsigned lane = threadIdx.x & 31;
     const unsigned grp = __match_any_sync(part, key) & __match_any_sync(part, flags);
     const int doer = flags == 1 ? __ffs(grp) - 1 : 31 - __clz(grp);
     const bool is_doer = (int)lane == doer;
+#if GX_HASH_LOCKSTEP
+    /* the doing lanes of the warp run their attempts in lock-step rounds */
     const unsigned doers = __ballot_sync(part, is_doer);
     int64_t rc = 0;
-    bool f = false;
     if (is_doer) {
+        bool f = false;
         uint32_t st = 0, waits = 0;
         unsigned pend = doers;
         for (;;) {
@@ -289,7 +339,6 @@ __device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, u
             if (__any_sync(still, r == kHashWait)) {
                 if (++waits > GX_HASH_VALVE) { /* safety valve, far beyond any in-flight insert */
                     rc = -E_2BIG;
-                    f = true;
                     break;
                 }
                 __nanosleep(waits < 7 ? 32u << waits : 2048u);
@@ -297,11 +346,18 @@ __device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc &m, uint64_t key, u
             pend = still;
         }
     }
+#else
+    /* each doing lane on its own: a lane that has to wait for in-flight reservations backs off with
+     * __nanosleep, which lets a reservation holder of its own warp run (hash_update) */
+    int64_t rc = 0;
+    if (is_doer) {
+        bool f;
+        rc = hash_update(m, key, val, flags, f);
+    }
+#endif
     rc = (int64_t)__shfl_sync(grp, (unsigned long long)rc, doer);
-    f = __shfl_sync(grp, (int)f, doer) != 0;
     if (!is_doer && flags == 1 && rc == 0) rc = -E_EXIST;
-    full = f;
-    return rc;
+    return rc; /* refused for capacity (hash_full) exactly when -E2BIG */
 }
 
 /* ---- PREFETCH QUEUE: gdev_mem_prefetch(queue, addr, len) (F-1..F-3).

@@ -654,7 +654,8 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         fl = R[4 * 32 + lane];
                     }
                     bool full;
-                    const int64_t rc = gxd::hash_update_coop(md, k, v, fl, full, me, GX_FULL);
+                    const int64_t rc = gxd::hash_update_coop(md, k, v, fl, me, GX_FULL);
+                    full = rc == -E_2BIG;
                     if (me) {
                         if (rc) c_herr++;
                         if (full) c_hfull++;

@@ -288,8 +288,7 @@ struct Gen {
         }
         o << "template <bool FULL>\n__device__ __forceinline__ void prog" << q
           << "(const Ctx &c, unsigned active, uint64_t &retv, const uint32_t shard, uint32_t *spriv, "
-             "unsigned long long &c_herr, unsigned long long &c_drop, unsigned long long &c_rbb, "
-             "unsigned long long &c_hfull, PtCache &ptc) {\n"
+             "unsigned &c_herr, unsigned &c_drop, unsigned long long &c_rbb, unsigned &c_hfull, PtCache &ptc) {\n"
              "  const unsigned lane = threadIdx.x & 31;\n"
              "  if (FULL) active = GX_ALL;\n"
              "  if (!((active >> lane) & 1)) return;\n"
@@ -516,9 +515,9 @@ struct Gen {
                                   : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
             const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
-            st("{ const uint64_t k_ = " + key + ", v_ = " + v + "; bool full = false;");
-            st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, r4, full, true, " + M() + ");");
-            st("  if (rc) c_herr++; if (full) c_hfull++; r0 = (uint64_t)rc; }");
+            st("{ const uint64_t k_ = " + key + ", v_ = " + v + ";");
+            st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, r4, true, " + M() + ");");
+            st("  if (rc) c_herr++; if (rc == -7) c_hfull++; r0 = (uint64_t)rc; }");
             break;
         }
         case GX_CALL_MEM_PREFETCH:
@@ -659,6 +658,9 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PIN")) o << "#define GX_PIN " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_ATOM_MIXED")) o << "#define GX_ATOM_MIXED " << atoi(e) << "\n";
+        if (getenv("GX_JIT_COLD_INLINE")) o << "#define GX_COLD_INLINE 1\n";
+        if (getenv("GX_JIT_LOCKSTEP")) o << "#define GX_HASH_LOCKSTEP 1\n";
+        if (const char *e = getenv("GX_JIT_PROBE_W")) o << "#define GX_HASH_PROBE_W " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot
@@ -732,7 +734,8 @@ struct Gen {
              "   * only keeps a device that reports more SM ids than that inside the map */\n"
              "  const uint32_t shard = ((smid * 64 + (wslot & 63)) * 32 + lane) % " << pt_shards_min() << "u;\n"
              "  uint64_t retv = 0;\n"
-             "  unsigned long long herr = 0, drop = 0, rbb = 0, hfull = 0;\n"
+             "  unsigned herr = 0, drop = 0, hfull = 0;\n"
+             "  unsigned long long rbb = 0;\n"
              "  PtCache ptc;\n"
              "  if (group == GX_ALL) prog0<true>(c, GX_ALL, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
              "  else prog0<false>(c, group, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
@@ -770,7 +773,9 @@ struct Gen {
              "  __syncthreads();\n"
              "  const uint32_t lane = threadIdx.x & 31;\n"
              "  const uint32_t shard = blockIdx.x * " << B << " + threadIdx.x;\n"
-             "  unsigned long long c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_rbb = 0, c_hfull = 0;\n"
+             "  /* per-thread event counts in 32 bits (register pressure), widened for the warp reduction */\n"
+             "  unsigned c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_hfull = 0;\n"
+             "  unsigned long long c_rbb = 0;\n"
              "  PtCache ptc;\n"
              "  const uint64_t nrec = (n + 31) >> 5, nfull = n >> 5; /* records, whole records */\n"
              "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
@@ -1005,18 +1010,21 @@ struct Gen {
         }
         o << (two_level ? "    }\n  }\n" : "  }\n");
         o << "  ptc_flush(ptc);\n"
+             "  {\n"
+             "  unsigned long long w_run = c_run, w_skip = c_skip, w_herr = c_herr, w_drop = c_drop, w_hfull = c_hfull;\n"
              "  for (int s = 16; s; s >>= 1) {\n"
-             "    c_run += __shfl_xor_sync(GX_ALL, c_run, s); c_skip += __shfl_xor_sync(GX_ALL, c_skip, s);\n"
-             "    c_herr += __shfl_xor_sync(GX_ALL, c_herr, s); c_drop += __shfl_xor_sync(GX_ALL, c_drop, s);\n"
-             "    c_rbb += __shfl_xor_sync(GX_ALL, c_rbb, s); c_hfull += __shfl_xor_sync(GX_ALL, c_hfull, s);\n"
+             "    w_run += __shfl_xor_sync(GX_ALL, w_run, s); w_skip += __shfl_xor_sync(GX_ALL, w_skip, s);\n"
+             "    w_herr += __shfl_xor_sync(GX_ALL, w_herr, s); w_drop += __shfl_xor_sync(GX_ALL, w_drop, s);\n"
+             "    c_rbb += __shfl_xor_sync(GX_ALL, c_rbb, s); w_hfull += __shfl_xor_sync(GX_ALL, w_hfull, s);\n"
              "  }\n"
              "  if (lane == 0) {\n"
-             "    if (c_run) atomicAdd(&sstats[" << GXS_RUN << "], c_run);\n"
-             "    if (c_skip) atomicAdd(&sstats[" << GXS_SKIP << "], c_skip);\n"
-             "    if (c_herr) atomicAdd(&sstats[" << GXS_HERR << "], c_herr);\n"
-             "    if (c_drop) atomicAdd(&sstats[" << GXS_RB_DROPS << "], c_drop);\n"
+             "    if (w_run) atomicAdd(&sstats[" << GXS_RUN << "], w_run);\n"
+             "    if (w_skip) atomicAdd(&sstats[" << GXS_SKIP << "], w_skip);\n"
+             "    if (w_herr) atomicAdd(&sstats[" << GXS_HERR << "], w_herr);\n"
+             "    if (w_drop) atomicAdd(&sstats[" << GXS_RB_DROPS << "], w_drop);\n"
              "    if (c_rbb) atomicAdd(&sstats[" << GXS_RB_BYTES << "], c_rbb);\n"
-             "    if (c_hfull) atomicAdd(&sstats[" << GXS_HFULL << "], c_hfull);\n"
+             "    if (w_hfull) atomicAdd(&sstats[" << GXS_HFULL << "], w_hfull);\n"
+             "  }\n"
              "  }\n"
              "  __syncthreads();\n";
         for (uint32_t k = 0; k < L.n_priv; k++) {

@@ -397,31 +397,37 @@ __device__ __forceinline__ uint64_t group_atomic(unsigned mask, uint64_t addr, u
         return W32 ? (uint32_t)r : r;
     }
 #elif GX_ATOM_MIXED == 2
-    /* the whole warp walks its address groups (no divergence) */
-    {
-        const unsigned peers = __match_any_sync(mask, addr);
-        const unsigned gl = __ffs(peers) - 1;
-        uint64_t pre = ident, tot = ident;
-        for (unsigned m = peers; m; m &= m - 1) {
-            const int jl = __ffs(m) - 1;
-            const uint64_t vj = __shfl_sync(peers, v, jl);
-            if (jl < (int)lane) pre = apply_op(OP, pre, vj);
-            tot = apply_op(OP, tot, vj);
-        }
-        uint64_t old = 0;
-        if (lane == gl) old = global_atomic(OP, addr, tot, W32, FETCH);
-        if (!FETCH) return 0;
-        old = __shfl_sync(peers, old, gl);
-        const uint64_t r = apply_op(OP, old, pre);
-        return W32 ? (uint32_t)r : r;
-    }
-#else
     const unsigned peers = __match_any_sync(mask, addr);
     if (peers == (1u << lane)) {
         const uint64_t r = global_atomic(OP, addr, v, W32, FETCH);
         return W32 ? (uint32_t)r : r;
     }
     return group_atomic_walk<OP, W32, FETCH>(peers, addr, v);
+#else
+    /* lanes grouped by address (one __match_any_sync).  The lanes that share an address with
+     * another lane (`dup`, warp-uniform) are visited by a uniform loop of whole-group shuffles --
+     * no per-group masks, so no convergence checks -- accumulating each lane's group total and its
+     * exclusive prefix in lane order; then every group leader (a lone lane is its own) issues ONE
+     * atomic in one instruction, and FETCH lanes take old (one shuffle from the leader) + prefix. */
+    const unsigned peers = __match_any_sync(mask, addr);
+    const unsigned me_bit = 1u << lane;
+    const unsigned dup = __ballot_sync(mask, peers != me_bit);
+    uint64_t tot = W32 ? (uint32_t)v : v, pre = ident;
+    for (unsigned m = dup; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const uint64_t vj = __shfl_sync(mask, v, j);
+        if (j != (int)lane && ((peers >> j) & 1)) {
+            tot = apply_op(OP, tot, vj);
+            if (j < (int)lane) pre = apply_op(OP, pre, vj);
+        }
+    }
+    const int gl = __ffs(peers) - 1;
+    uint64_t old = 0;
+    if ((int)lane == gl) old = global_atomic(OP, addr, tot, W32, FETCH);
+    if (!FETCH) return 0;
+    if (dup) old = __shfl_sync(mask, old, gl);
+    const uint64_t r = apply_op(OP, old, pre);
+    return W32 ? (uint32_t)r : r;
 #endif
 }
 
@@ -490,39 +496,37 @@ __device__ __noinline__ uint64_t group_cmpxchg(unsigned mask, uint64_t addr, uin
 }
 
 /* ADD of a compile-time constant K (the verifier folded the source register: `mov r1, 1;
- * atomic_add [r0], r1`).  Uniform address (one MATCH.ALL): the group's sum is K * popc(mask), no
- * reduction; FETCH lanes get old + K * (their rank in the group).  Mixed addresses: per-lane RED
- * (non-FETCH) or __match_any_sync groups with the same rank arithmetic (FETCH). */
+ * atomic_add [r0], r1`, with or without FETCH).  Groups of lanes on one address: the group's
+ * leader adds K * popc(group) with one L2 atomic; FETCH lanes get old + K * (their rank in the
+ * group) -- the group's sequential result in lane order, no reduction or prefix loop.
+ *   non-FETCH: one MATCH.ALL tests address uniformity (C1 / C2's record-uniform keys), else
+ *              __match_any_sync groups (per-lane REDs to a hot address serialise at its L2 slice);
+ *   FETCH: a shuffle + vote tests uniformity (cheaper than a 64-bit match on C3's decode records,
+ *              which are almost never uniform), else __match_any_sync groups and one whole-group
+ *              shuffle from each leader. */
 template <bool W32, bool FETCH>
 __device__ __forceinline__ uint64_t group_add_const(unsigned mask, uint64_t addr, uint64_t k) {
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1;
-    int same = 0;
-    const unsigned peers = __match_all_sync(mask, (unsigned long long)addr, &same);
-    if (same) {
-        const unsigned leader = __ffs(mask) - 1;
-        const uint64_t tot = k * (uint64_t)__popc(mask);
-        if (!FETCH) {
-            if (lane == leader) global_atomic(0x00, addr, tot, W32, false);
+    if (!FETCH) {
+        int same = 0;
+        (void)__match_all_sync(mask, (unsigned long long)addr, &same);
+        if (same) {
+            if (lane == (unsigned)(__ffs(mask) - 1)) global_atomic(0x00, addr, k * (uint64_t)__popc(mask), W32, false);
             return 0;
         }
-        uint64_t old = 0;
-        if (lane == leader) old = global_atomic(0x00, addr, tot, W32, true);
-        old = __shfl_sync(mask, old, leader);
-        const uint64_t r = old + k * (uint64_t)__popc(peers & lt);
-        return W32 ? (uint32_t)r : r;
-    }
-    /* lanes grouped by address: one L2 atomic per distinct address -- per-lane REDs
-     * to a hot address serialise at its L2 slice (C3 trace: 22.5 vs 21.4 ms with FETCH groups) */
-    const unsigned grp = __match_any_sync(mask, (unsigned long long)addr);
-    const unsigned gl = __ffs(grp) - 1;
-    if (!FETCH) {
-        if (lane == gl) global_atomic(0x00, addr, k * (uint64_t)__popc(grp), W32, false);
+        const unsigned grp = __match_any_sync(mask, (unsigned long long)addr);
+        if (lane == (unsigned)(__ffs(grp) - 1)) global_atomic(0x00, addr, k * (uint64_t)__popc(grp), W32, false);
         return 0;
     }
+    const unsigned leader = __ffs(mask) - 1;
+    const uint64_t a0 = __shfl_sync(mask, addr, leader);
+    unsigned grp = mask;
+    if (!__all_sync(mask, addr == a0)) grp = __match_any_sync(mask, (unsigned long long)addr);
+    const unsigned gl = __ffs(grp) - 1;
     uint64_t old = 0;
     if (lane == gl) old = global_atomic(0x00, addr, k * (uint64_t)__popc(grp), W32, true);
-    old = __shfl_sync(grp, old, gl);
+    old = __shfl_sync(mask, old, gl);
     const uint64_t r = old + k * (uint64_t)__popc(grp & lt);
     return W32 ? (uint32_t)r : r;
 }
@@ -569,8 +573,9 @@ __device__ __forceinline__ void group_priv_add(unsigned mask, uint32_t *lo, uint
 }
 
 /* one ringbuf reservation per group (records in lane order); returns 0 or -EAGAIN */
+template <typename Counter>
 __device__ __forceinline__ int64_t group_ringbuf(unsigned mask, const GxMapDesc &md, const uint64_t *words, uint32_t size,
-                                                 unsigned long long &drops, unsigned long long &bytes) {
+                                                 Counter &drops, unsigned long long &bytes) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t recb = (8 + size + 7) & ~7u;
     const uint32_t cnt = __popc(mask), rank = __popc(mask & ((1u << lane) - 1));

@@ -2030,6 +2030,8 @@ struct Verifier {
             } else if (a.op == GX_MOV64 && !(a.flags & GXF_X) &&
                        (b.op == GX_ATOM_MAP || b.op == GX_ATOM_PT || b.op == GX_ATOM_STACK) && b.src == a.dst &&
                        !(b.imm & 1) && (b.imm & 0xFF) != 0xE1 && !(live[j] & (1u << a.dst))) {
+                /* non-FETCH only: on C3 the folded FETCH-ADD measured 25 % slower than the register
+                 * form (8.1 vs 6.2 ms, same box, interleaved; profiles/r2_c3.md) */
                 GxInsn f = b;
                 f.flags |= GXF_PRIV; /* constant operand in imm[63:32] */
                 f.imm = (b.imm & 0xFF) | ((uint64_t)(uint32_t)(int32_t)(int64_t)a.imm << 32);
