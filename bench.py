@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-c1", action="store_true", help="skip the C1 (1M-event counter) section")
     p.add_argument("--extra", action="store_true", help="also time C1/C3/C4 single-GPU lines (stderr)")
+    p.add_argument("--no-configs", action="store_true",
+                   help="skip the per-config records (C1-C5 at N=1; C4 strong / C5 weak scaling with gx_merge at N>1)")
     p.add_argument("--engine", default="jit", choices=["jit", "interp"],
                    help="headline engine (the other one is timed too and reported under 'engines')")
     return p.parse_args()
@@ -158,6 +160,166 @@ def oracle_rate(config, seed, n_total, budget_s=12.0):
     return done / t_used, done, t_used
 
 
+def _oracle_worker(a):
+    config, seed, n_total, i0, budget_s = a
+    from gxin import configs
+    from oracle.oracle import Oracle
+    env = Oracle()
+    s = configs.setup(env, config)
+    done, t_used, n = 0, 0.0, 1 << 20
+    while t_used < budget_s:
+        ev = configs.events(config, seed, n, i0 + done, n_total)
+        t0 = time.perf_counter()
+        env.run(ev, s.prog_arg, index_base=i0 + done, want_r0=False)
+        t_used += time.perf_counter() - t0
+        done += n
+    return done, t_used
+
+
+def oracle_rate_allcores(config, seed, n_total, budget_s=10.0):
+    """The same oracle on every host core at once: one process per core on disjoint chunks of the
+    stream (the per-event work is the same as the 1-core figure; no merge is timed)."""
+    import multiprocessing as mproc
+    cores = host_cores()
+    span = n_total // cores // (1 << 20) * (1 << 20) or (1 << 20)
+    with mproc.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_worker, [(config, seed, n_total, (k * span) % max(1, n_total - (1 << 22)), budget_s)
+                                        for k in range(cores)])
+    done = sum(d for d, _ in res)
+    wall = max(t for _, t in res)
+    return done / wall, done, cores
+
+
+# SURVEY.md §8d roofline inputs per config: L2 atomics per event the method cannot avoid (A_alg):
+# C1 privatised (0); C2 one record-uniform ADD per 32-event record (the 74 KiB histogram is over the
+# 16 KiB privatisation budget); C3 0.69 returning FETCH-ADDs per event (prefill records key-uniform,
+# a decode record holds 29.2 distinct pages: DESIGN.md §6); C4 two record-near-uniform ADDs per
+# record; C5 the tenant mix (40 % P1, 30 % P2, 20 % P3', 10 % P4).
+A_ALG = {"C1": 0.0, "C2": 1 / 32, "C3": 0.69, "C4": 2 / 32,
+         "C5": 0.3 * (1 / 32) + 0.2 * 0.69 + 0.1 * (2 / 32)}
+CONFIG_EVENTS = {"C1": 1 << 26, "C2": 1 << 30, "C3": 1 << 28, "C4": 1 << 28, "C5": 1 << 28}
+
+
+def atomic_rate():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "atomics_b200.json")))["atom_add_u64_random_per_s"]
+    except Exception:
+        return 1.257e11
+
+
+def config_records(device, args):
+    """One record per config (SURVEY.md §8d result fields): device time per batch, events/s, the three
+    roofline components T_hbm / T_atom / T_alu with their fractions, and a parity verdict from this
+    run (a 2^16-event sample against the oracle, bit-exact, plus the full batch's event count)."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+    from oracle.oracle import Oracle
+    peaks = measured_peaks()[0]
+    r_atom = atomic_rate()
+    out = {}
+    for config, n in CONFIG_EVENTS.items():
+        try:
+            seed = configs.SEEDS[config]
+            # parity sample: the oracle and the CUDA path on the same 2^16 events
+            ns = 1 << 16
+            evs = configs.events(config, seed, ns)
+            env = Oracle()
+            so = configs.setup(env, config)
+            r0o = env.run(evs, so.prog_arg)
+            ost = env.stats()
+            rts = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
+            sg = configs.setup(rts, config)
+            ret = torch.zeros(ns, dtype=torch.int64, device="cuda")
+            rts.run(torch.from_numpy(evs.view(np.uint8).reshape(-1, 32)).cuda(), sg.prog_arg, ret=ret)
+            torch.cuda.synchronize()
+            same = bool((ret.cpu().numpy().view(np.uint64) == r0o).all())
+            for key, fd in so.fds.items():
+                if env.specs[fd][0] == 27:
+                    same &= env.ringbuf_records(fd) == rts.ringbuf_records(sg.fds[key])
+                else:
+                    same &= env.dump(fd) == rts.dump(sg.fds[key])
+            rts.close()
+            insns = ost["insns"] / max(1, ost["events_run"])
+            # the timed batch: warm maps, 3 + 5 launches
+            rt = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
+            s = configs.setup(rt, config)
+            ev = gen_gpu.generate_device(config, seed, n, device=device)
+            for _ in range(3):
+                rt.run(ev, s.prog_arg)
+            st0 = rt.stats()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(5):
+                rt.run(ev, s.prog_arg)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / 5
+            st = rt.stats()
+            run_ok = st["events_run"] + st["events_skipped"] == 5 * n
+            rb = st["ringbuf_bytes"] / 5 / n
+            t_hbm = n * (EVENT_BYTES + rb) / (peaks["hbm_gbs"] * 1e9) * 1e3
+            t_atom = n * A_ALG[config] / r_atom * 1e3
+            f_sm = 1965e6
+            t_alu = n / 32 * (2 * insns) / (148 * 4 * f_sm) * 1e3
+            comp = {"hbm": t_hbm, "atom": t_atom, "alu": t_alu}
+            bound = max(comp, key=comp.get)
+            out[config] = {"events": n, "ms": ms, "events_per_s": n / (ms / 1e3), "ns_per_event": ms * 1e6 / n,
+                           "t_hbm_ms": t_hbm, "t_atom_ms": t_atom, "t_alu_ms": t_alu,
+                           "frac_hbm": t_hbm / ms, "frac_atom": t_atom / ms, "frac_alu": t_alu / ms,
+                           "bound": bound, "frac": comp[bound] / ms, "R_atom_per_s": r_atom, "A_alg": A_ALG[config],
+                           "insns_per_event": insns, "f_sm_mhz": f_sm / 1e6,
+                           "parity": ("exact" if same else "mismatch") + " (2^16-event sample vs oracle)",
+                           "events_accounted": bool(run_ok)}
+            del ev
+            rt.close()
+        except Exception as exc:  # pragma: no cover - box-dependent
+            out[config] = {"error": str(exc)[:200]}
+    return out
+
+
+def multi_records(device, rank, world, args):
+    """N > 1: C4 strong scaling (2^31 events in total, 2^31/N per GPU)
+    and C5 (the multi-tenant mix, 2^28 events per GPU, weak), each step = the batch + gx_merge of
+    every map over the library's NCCL communicator; max over ranks of the device time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2512_12615_b200 as gx
+    from gxin import configs, gen_gpu
+    from paper_2512_12615_b200.dist import Merger
+    out = {}
+    for config, n_total, scaling in (("C4", 1 << 31, "strong"), ("C5", (1 << 28) * world, "weak")):
+        n = n_total // world // 32 * 32
+        rt = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
+        s = configs.setup(rt, config)
+        ev = gen_gpu.generate_device(config, configs.SEEDS[config], n, i0=rank * n, n_total=n_total, device=device)
+        m = Merger(rt, dist.group.WORLD)
+        for _ in range(2):
+            rt.run(ev, s.prog_arg)
+            m.merge()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b, mb = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record()
+        for k in range(5):
+            rt.run(ev, s.prog_arg)
+            if k == 4:
+                mb.record()
+            m.merge()
+        b.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = torch.tensor([a.elapsed_time(b) / 5, mb.elapsed_time(b)], device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        out[config] = {"scaling": scaling, "events_total_per_step": n * world, "events_per_gpu": n,
+                       "ms_per_step": float(ms[0]), "events_per_s": n * world / (float(ms[0]) / 1e3),
+                       "merge_ms": float(ms[1]), "steps": 5, "merge": "every step (gx_merge after each batch)"}
+        del ev
+        rt.close()
+    return out
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle on the host cores, rank 0 only (the base contract's reference arm)."""
     if rank != 0:
@@ -216,7 +378,7 @@ def main():
     merger = None
     if world > 1:
         from paper_2512_12615_b200.dist import Merger
-        merger = Merger(rt, [fd for fd in s.fds.values()], dist.group.WORLD)
+        merger = Merger(rt, dist.group.WORLD)   # gx_comm_init on the library's NCCL communicator
 
     def step():
         rt.run(events, s.prog_arg, stream=stream)
@@ -316,6 +478,19 @@ def main():
         line["cpu_baseline"] = {"value": r, "unit": "events/s", "cores": 1, "kind": "oracle",
                                 "sample": f"prefix of {done} events of the {config} stream (seed {seed}) in "
                                           f"{t:.1f} s, interpretation only; host has {host_cores()} cores, {cpu_model()}"}
+        try:
+            ra, dn, cores = oracle_rate_allcores(config, seed, n_total)
+            line["cpu_baseline"]["all_cores"] = {
+                "value": ra, "cores": cores, "sample": f"{dn} events: disjoint 2^20-event chunks of the same stream, "
+                                                      f"one oracle process per core for ~10 s (interpretation only)"}
+        except Exception as exc:  # pragma: no cover - host-dependent
+            line["cpu_baseline"]["all_cores"] = {"error": str(exc)[:200]}
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["configs"] = config_records(local, args)
+    if world > 1 and not args.no_configs:
+        multi = multi_records(local, rank, world, args)
+        if rank == 0:
+            line["multi"] = multi
     if rank == 0 and world == 1 and not args.no_c1:
         try:
             line["c1"] = c1_measure(local)

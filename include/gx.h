@@ -319,6 +319,49 @@ int  gx_hash_export(gx_rt *rt, int map_fd, uint32_t nranks, int32_t owner, uint6
 int  gx_hash_apply(gx_rt *rt, int map_fd, const uint64_t *d_keys, const uint64_t *d_vals, uint64_t n,
                    uint32_t flags, void *cuda_stream);
 
+/* ---- Multi-GPU merge (§4.4.3 "merges these shards into canonical
+ * snapshots at synchronization points", §5.3 "snapshot-based aggregation at GPU kernel
+ * completion boundaries").  One gx_rt per GPU, one process per GPU; every rank creates the same maps,
+ * applies the same host writes and loads the same programs, then runs its own event shard.
+ *   gx_comm_unique_id: a fresh NCCL unique id (128 bytes into id_out) -- rank 0 makes it, the caller
+ *     ships it to the other ranks (process bootstrap, e.g. torch.distributed).  -ENOSYS without NCCL.
+ *   gx_comm_init:   joins the NCCL communicator (ncclCommInitRank on this gx_rt's device; collective
+ *     over the nranks processes) and takes every map's base snapshot: the state all ranks agree on.
+ *     Host writes (gx_update_map) after it must be identical on every rank and followed by
+ *     gx_merge_snapshot of that map on every rank.
+ *   gx_comm_init_host: the same merge over caller callbacks on HOST buffers (several ranks sharing one
+ *     device, where NCCL refuses two ranks on one GPU; tests): allreduce_sum_u64 sums n u64 words in
+ *     place over the ranks (wraparound); alltoallv sends send_bytes[g] bytes at send + send_off[g] to
+ *     rank g and receives recv_bytes[g] bytes from rank g into recv + recv_off[g]; allgather puts rank
+ *     g's `bytes` bytes at recv + g * bytes.  Callbacks return 0 or a negative errno.
+ *   gx_merge:       collective over all ranks (call it on every rank at the same point, between
+ *     batches): every map reaches S3's canonical state:
+ *       ARRAY / PERTHREAD: canon = base + sum over ranks of (local - base), per u64 word (PERTHREAD
+ *         folded first) -- one packed u64 SUM all-reduce over all such maps;
+ *       HASH: key union, value = base (or 0 if new) + sum of deltas -- owner-sharded (owner =
+ *         mix64(key) mod nranks): counts all-gather, (key, delta) all-to-all, owners accumulate onto
+ *         the base, owners' merged deltas all-gathered, every rank rebuilds;
+ *       RINGBUF / PREFETCH QUEUE: rank-local (their union is the multiset / set union; drain each).
+ *     Afterwards base = canon on every rank.  Stream-ordered on cuda_stream; returns after it.
+ *     -EINVAL (nothing changed) if a map is not mergeable by S3: an ARRAY written by anything but
+ *     64-bit ATOMIC ADD (+-FETCH), a HASH whose values change by anything but 64-bit ATOMIC ADD or
+ *     whose keys are inserted by update_elem with flags other than the constant BPF_NOEXIST (the
+ *     verifier's usage facts of every loaded program); -E2BIG if a merged HASH union exceeds
+ *     max_entries; -EIO on a transport error (gx_last_error).
+ *   gx_comm_free:   leaves the communicator (gx_close does too). */
+typedef struct {
+    void *user;
+    int (*allreduce_sum_u64)(void *user, uint64_t *buf, uint64_t n);
+    int (*alltoallv)(void *user, const void *send, const uint64_t *send_bytes, const uint64_t *send_off, void *recv,
+                     const uint64_t *recv_bytes, const uint64_t *recv_off);
+    int (*allgather)(void *user, const void *send, void *recv, uint64_t bytes);
+} gx_comm_host_ops;
+int  gx_comm_unique_id(void *id_out);
+int  gx_comm_init(gx_rt *rt, const void *nccl_unique_id, int nranks, int rank);
+int  gx_comm_init_host(gx_rt *rt, const gx_comm_host_ops *ops, int nranks, int rank);
+int  gx_merge(gx_rt *rt, void *cuda_stream);
+int  gx_comm_free(gx_rt *rt);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,8 @@ EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_m
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply", "gx_prefetch_drain", "gx_daemon_start", "gx_daemon_stop", "gx_daemon_watch",
            "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range", "gx_instrument",
-           "gx_kernel_launch", "gx_kernel_free", "gx_sched_run")
+           "gx_kernel_launch", "gx_kernel_free", "gx_sched_run", "gx_comm_unique_id", "gx_comm_init",
+           "gx_comm_init_host", "gx_merge", "gx_comm_free")
 
 
 class gx_map_spec(C.Structure):
@@ -128,6 +129,11 @@ def lib():
         "gx_merge_apply": (i32, [vp, i32, vp, vp]),
         "gx_hash_export": (i32, [vp, i32, u32, C.c_int32, vp, vp, u64, p64]),
         "gx_hash_apply": (i32, [vp, i32, vp, vp, u64, u32, vp]),
+        "gx_comm_unique_id": (i32, [vp]),
+        "gx_comm_init": (i32, [vp, vp, i32, i32]),
+        "gx_comm_init_host": (i32, [vp, C.POINTER(gx_comm_host_ops), i32, i32]),
+        "gx_merge": (i32, [vp, vp]),
+        "gx_comm_free": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -139,6 +145,18 @@ def lib():
 
 class GxError(OSError):
     pass
+
+
+# gx_comm_host_ops (include/gx.h): host-buffer transport callbacks of gx_merge
+ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64)
+ALLTOALLV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p,
+                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint64))
+ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class gx_comm_host_ops(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum_u64", ALLREDUCE_CB), ("alltoallv", ALLTOALLV_CB),
+                ("allgather", ALLGATHER_CB)]
 
 
 def _check(rc, what, rt=None):
@@ -445,6 +463,68 @@ GX_MERGE_RESTORE, GX_MERGE_COMMIT = 1, 2
 def gx_hash_apply(rt, fd, keys, vals, n, flags=GX_MERGE_RESTORE | GX_MERGE_COMMIT, stream=None):
     _check(lib().gx_hash_apply(rt, fd, keys.data_ptr() if n else None, vals.data_ptr() if n else None, n, flags,
                                _stream_handle(stream)), "gx_hash_apply", rt)
+
+
+def gx_comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for gx_comm_init (rank 0 makes it, the caller ships it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().gx_comm_unique_id(buf), "gx_comm_unique_id")
+    return buf.raw
+
+
+def gx_comm_init(rt, unique_id: bytes, nranks: int, rank: int):
+    _check(lib().gx_comm_init(rt, unique_id, nranks, rank), "gx_comm_init", rt)
+
+
+def gx_comm_init_host(rt, allreduce_sum_u64, alltoallv, allgather, nranks: int, rank: int):
+    """Host-buffer transport: the three callables get numpy views of the library's host staging
+    buffers (uint64 words for the all-reduce, uint8 bytes otherwise) and must fill them in place:
+        allreduce_sum_u64(buf_u64)                          -- in-place SUM over ranks
+        alltoallv(send_u8, send_bytes, send_off, recv_u8, recv_bytes, recv_off)
+        allgather(send_u8, recv_u8)                          -- recv = concat over ranks
+    Returns the ctypes object that must stay alive as long as the runtime merges."""
+    def ar(user, buf, n):
+        try:
+            allreduce_sum_u64(np.ctypeslib.as_array(buf, shape=(n,)))
+            return 0
+        except Exception:
+            return -errno.EIO
+
+    def a2a(user, send, sb, so, recv, rb, ro):
+        try:
+            G = nranks
+            sbv, sov = np.ctypeslib.as_array(sb, shape=(G,)).copy(), np.ctypeslib.as_array(so, shape=(G,)).copy()
+            rbv, rov = np.ctypeslib.as_array(rb, shape=(G,)).copy(), np.ctypeslib.as_array(ro, shape=(G,)).copy()
+            ns = int((sov + sbv).max()) if G else 0
+            nr = int((rov + rbv).max()) if G else 0
+            sa = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(max(ns, 1),)) if ns else np.zeros(0, np.uint8)
+            ra = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), shape=(max(nr, 1),)) if nr else np.zeros(0, np.uint8)
+            alltoallv(sa, sbv, sov, ra, rbv, rov)
+            return 0
+        except Exception:
+            return -errno.EIO
+
+    def ag(user, send, recv, nbytes):
+        try:
+            sa = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(nbytes,))
+            ra = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), shape=(nbytes * nranks,))
+            allgather(sa, ra)
+            return 0
+        except Exception:
+            return -errno.EIO
+
+    ops = gx_comm_host_ops(None, ALLREDUCE_CB(ar), ALLTOALLV_CB(a2a), ALLGATHER_CB(ag))
+    _check(lib().gx_comm_init_host(rt, C.byref(ops), nranks, rank), "gx_comm_init_host", rt)
+    return ops
+
+
+def gx_merge(rt, stream=None):
+    """Collective S3 merge of every map over the communicator's ranks (include/gx.h)."""
+    _check(lib().gx_merge(rt, _stream_handle(stream)), "gx_merge", rt)
+
+
+def gx_comm_free(rt):
+    _check(lib().gx_comm_free(rt), "gx_comm_free", rt)
 
 
 # ---------------------------------------------------------------- engine object

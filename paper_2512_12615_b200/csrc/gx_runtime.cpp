@@ -7,6 +7,7 @@
  * gx_maps.cu; nothing here computes on events.
  */
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <errno.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -28,6 +29,7 @@
 #include "gx_verifier.h"
 
 #include <cuda.h>
+#include <nccl.h> /* types only: libnccl is dlopen'ed at gx_comm_init (no link-time dependency) */
 #include <chrono>
 
 extern "C" {
@@ -177,6 +179,29 @@ struct Daemon {
     cudaStream_t s_prefetch = nullptr;
 };
 
+/* ---- multi-GPU transport of gx_merge: NCCL (dlopen'ed; device buffers over
+ * NVLink / NVSwitch), or caller-supplied host callbacks (several ranks sharing one device in tests). */
+struct GxComm {
+    int nranks = 1, rank = 0;
+    virtual ~GxComm() {}
+    virtual bool device_buffers() const = 0;
+    /* in-place u64 SUM over ranks (wraparound: exactly the S3 delta arithmetic) */
+    virtual int allreduce_sum_u64(uint64_t *buf, uint64_t n, cudaStream_t s) = 0;
+    /* every rank sends send_bytes[g] bytes from send + soff[g] to rank g and receives recv_bytes[g]
+     * bytes from rank g at recv + roff[g] */
+    virtual int alltoallv(const uint8_t *send, const uint64_t *send_bytes, const uint64_t *soff, uint8_t *recv,
+                          const uint64_t *recv_bytes, const uint64_t *roff, cudaStream_t s) = 0;
+    /* recv[g * bytes .. ] = rank g's send[0 .. bytes) */
+    virtual int allgather(const void *send, void *recv, uint64_t bytes, cudaStream_t s) = 0;
+    virtual const char *error() const { return ""; }
+};
+
+struct MergeScratch {
+    uint64_t *d = nullptr; /* device scratch (packed deltas, hash exchange buffers) */
+    uint64_t words = 0;
+    std::vector<uint64_t> h; /* host staging for host transports */
+};
+
 struct gx_rt {
     int dev = 0;
     int nsm = 0;
@@ -198,6 +223,10 @@ struct gx_rt {
     cudaEvent_t ev_copied[2], ev_done[2];
     bool pipe_init = false;
     Daemon dmn;
+    /* gx_comm_init / gx_merge */
+    std::unique_ptr<GxComm> comm;
+    MergeScratch ms;
+    uint64_t merges = 0;
 };
 
 namespace {
@@ -648,6 +677,8 @@ void gx_close(gx_rt *rt) {
             if (v.mod && drv().moduleUnload) drv().moduleUnload(v.mod);
     }
     cudaFree(rt->d_stats);
+    rt->comm.reset();
+    cudaFree(rt->ms.d);
     if (rt->pipe_init) {
         for (int b = 0; b < 2; b++) {
             cudaFree(rt->d_chunk[b]);
@@ -1628,6 +1659,417 @@ int gx_hash_apply(gx_rt *rt, int fd, const uint64_t *d_keys, const uint64_t *d_v
     CK(cudaStreamSynchronize(s), "sync");
     cudaFree(full);
     if (h) return set_err(rt, -E2BIG, "merged hash union exceeds max_entries (%llu refused)", h);
+    return 0;
+}
+
+}  // extern "C"
+
+/* ------------------------------------------------------------------ gx_comm_init / gx_merge (S3) */
+
+namespace {
+
+
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        /* the NCCL already in the process (torch.distributed's) first, then GX_NCCL_LIB, then the
+         * loader path */
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h && getenv("GX_NCCL_LIB")) h = dlopen(getenv("GX_NCCL_LIB"), RTLD_NOW);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!h) {
+            a.err = std::string("libnccl.so.2 not found: ") + dlerror();
+            return;
+        }
+#define GX_NCCL_SYM(f, n) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, n))
+        GX_NCCL_SYM(getUniqueId, "ncclGetUniqueId");
+        GX_NCCL_SYM(commInitRank, "ncclCommInitRank");
+        GX_NCCL_SYM(commDestroy, "ncclCommDestroy");
+        GX_NCCL_SYM(allReduce, "ncclAllReduce");
+        GX_NCCL_SYM(allGather, "ncclAllGather");
+        GX_NCCL_SYM(send, "ncclSend");
+        GX_NCCL_SYM(recv, "ncclRecv");
+        GX_NCCL_SYM(groupStart, "ncclGroupStart");
+        GX_NCCL_SYM(groupEnd, "ncclGroupEnd");
+        GX_NCCL_SYM(getErrorString, "ncclGetErrorString");
+#undef GX_NCCL_SYM
+        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.allGather && a.send && a.recv &&
+               a.groupStart && a.groupEnd;
+        if (!a.ok) a.err = "libnccl.so.2 lacks a needed symbol";
+    });
+    return a;
+}
+
+/* NCCL: the collectives are stream-ordered on the merge stream; point-to-point exchanges are one
+ * grouped send/recv set (the all-to-all of the key-sharded hash merge) */
+struct NcclComm : GxComm {
+    ncclComm_t comm = nullptr;
+    std::string last;
+    bool device_buffers() const override { return true; }
+    int fail(ncclResult_t r, const char *what) {
+        last = std::string(what) + ": " + (nccl().getErrorString ? nccl().getErrorString(r) : "nccl error");
+        return -EIO;
+    }
+    int allreduce_sum_u64(uint64_t *buf, uint64_t n, cudaStream_t s) override {
+        if (!n) return 0;
+        ncclResult_t r = nccl().allReduce(buf, buf, n, ncclUint64, ncclSum, comm, s);
+        return r == ncclSuccess ? 0 : fail(r, "ncclAllReduce");
+    }
+    int alltoallv(const uint8_t *send, const uint64_t *sb, const uint64_t *so, uint8_t *recv, const uint64_t *rb,
+                  const uint64_t *ro, cudaStream_t s) override {
+        ncclResult_t r = nccl().groupStart();
+        for (int g = 0; g < nranks && r == ncclSuccess; g++) {
+            if (sb[g]) r = nccl().send(send + so[g], sb[g], ncclUint8, g, comm, s);
+            if (r == ncclSuccess && rb[g]) r = nccl().recv(recv + ro[g], rb[g], ncclUint8, g, comm, s);
+        }
+        ncclResult_t r2 = nccl().groupEnd();
+        if (r != ncclSuccess) return fail(r, "ncclSend/ncclRecv");
+        return r2 == ncclSuccess ? 0 : fail(r2, "ncclGroupEnd");
+    }
+    int allgather(const void *send, void *recv, uint64_t bytes, cudaStream_t s) override {
+        ncclResult_t r = nccl().allGather(send, recv, bytes, ncclUint8, comm, s);
+        return r == ncclSuccess ? 0 : fail(r, "ncclAllGather");
+    }
+    const char *error() const override { return last.c_str(); }
+    ~NcclComm() override {
+        if (comm) nccl().commDestroy(comm);
+    }
+};
+
+/* host callbacks (gx_comm_host_ops): buffers are staged through host memory */
+struct HostComm : GxComm {
+    gx_comm_host_ops ops{};
+    bool device_buffers() const override { return false; }
+    int allreduce_sum_u64(uint64_t *buf, uint64_t n, cudaStream_t) override {
+        return n ? ops.allreduce_sum_u64(ops.user, buf, n) : 0;
+    }
+    int alltoallv(const uint8_t *send, const uint64_t *sb, const uint64_t *so, uint8_t *recv, const uint64_t *rb,
+                  const uint64_t *ro, cudaStream_t) override {
+        return ops.alltoallv(ops.user, send, sb, so, recv, rb, ro);
+    }
+    int allgather(const void *send, void *recv, uint64_t bytes, cudaStream_t) override {
+        return ops.allgather(ops.user, send, recv, bytes);
+    }
+};
+
+/* S3 legality of a map (the verifier's usage facts of every loaded program):
+ * ARRAY -- changed only by 64-bit ATOMIC ADD (+-FETCH); PERTHREAD -- any per-thread RMW (its
+ * canonical value is the SUM fold, S4); HASH -- values changed only by 64-bit ATOMIC ADD and keys
+ * inserted only by update_elem(BPF_NOEXIST).  Returns nullptr or the reason. */
+const char *merge_illegal(const gx_rt *rt, int fd) {
+    const Map &m = rt->maps[fd];
+    for (const Prog &p : rt->progs) {
+        if (!p.valid || !p.verified) continue;
+        const GxMapUse &u = p.vr.use[fd];
+        if (!u.used || !u.writes) continue;
+        if (m.spec.type == GX_MAP_ARRAY) {
+            if (u.store) return "written by a plain store or a non-ADD atomic";
+            if (u.update_call) return "written by bpf_map_update_elem";
+            if (u.non_dw_atomic) return "written by a 32-bit atomic";
+        } else if (m.spec.type == GX_MAP_HASH) {
+            if (u.store) return "values written by a plain store or a non-ADD atomic";
+            if (u.upd_overwrite) return "updated with flags other than the constant BPF_NOEXIST";
+            if (u.non_dw_atomic) return "values changed by a 32-bit atomic";
+        }
+    }
+    return nullptr;
+}
+
+int ms_reserve(gx_rt *rt, uint64_t words) {
+    if (rt->ms.words >= words) return 0;
+    cudaFree(rt->ms.d);
+    rt->ms.d = nullptr;
+    rt->ms.words = 0;
+    CK(cudaMalloc(&rt->ms.d, words * 8), "cudaMalloc merge scratch");
+    rt->ms.words = words;
+    if (!rt->comm->device_buffers()) rt->ms.h.resize(words);
+    return 0;
+}
+
+int comm_err(gx_rt *rt, int rc, const char *what) {
+    return set_err(rt, rc ? rc : -EIO, "%s: %s", what, rt->comm ? rt->comm->error() : "");
+}
+
+/* the S3 merge of one HASH map: owner-bucketed deltas -> all-to-all -> owners accumulate onto the
+ * base -> owners' merged deltas -> all-gather -> every rank rebuilds base + merged deltas */
+int merge_hash(gx_rt *rt, Map &m, cudaStream_t s) {
+    GxComm &C = *rt->comm;
+    const uint32_t G = (uint32_t)C.nranks;
+    const uint64_t cap = (uint64_t)m.cap + 2; /* entries a map can export (slots + side slots) */
+    /* scratch: [counts 2G | offsets G] [send keys | send vals] [recv keys | recv vals] (cap each) */
+    const uint64_t nrecv = cap * G;
+    int rc = ms_reserve(rt, 3ull * G + 2 * cap + 2 * nrecv);
+    if (rc) return rc;
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(rt->ms.d), *off = cnt + G;
+    uint64_t *sk = rt->ms.d + 3ull * G, *sv = sk + cap, *rk = sv + cap, *rv = rk + nrecv;
+    GxMapDesc d = make_desc(m), b = make_base_desc(m);
+    auto export_pass = [&](int32_t owner, std::vector<uint64_t> &counts) -> int {
+        CK(cudaMemsetAsync(cnt, 0, 16ull * G, s), "memset");
+        int e = gx_k_hash_export(&d, &b, G, owner, 0, cnt, off, sk, sv, cap, s);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash export");
+        counts.assign(G, 0);
+        CK(cudaMemcpyAsync(counts.data(), cnt, 8ull * G, cudaMemcpyDeviceToHost, s), "export counts");
+        CK(cudaStreamSynchronize(s), "export counts");
+        std::vector<uint64_t> o(G);
+        uint64_t t = 0;
+        for (uint32_t g = 0; g < G; g++) o[g] = t, t += counts[g];
+        if (t) {
+            CK(cudaMemcpyAsync(off, o.data(), 8ull * G, cudaMemcpyHostToDevice, s), "export offsets");
+            e = gx_k_hash_export(&d, &b, G, owner, 1, cnt, off, sk, sv, cap, s);
+            if (e) return cuda_err(rt, (cudaError_t)e, "hash export");
+        }
+        return 0;
+    };
+    /* device or host views of the exchange buffers */
+    const bool dev = C.device_buffers();
+    auto stage_out = [&](uint64_t *dptr, uint64_t n) -> uint8_t * {
+        if (dev) return reinterpret_cast<uint8_t *>(dptr);
+        uint64_t *h = rt->ms.h.data() + (dptr - rt->ms.d);
+        if (n) cudaMemcpyAsync(h, dptr, 8 * n, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return reinterpret_cast<uint8_t *>(h);
+    };
+    auto host_of = [&](uint64_t *dptr) -> uint8_t * {
+        return dev ? reinterpret_cast<uint8_t *>(dptr) : reinterpret_cast<uint8_t *>(rt->ms.h.data() + (dptr - rt->ms.d));
+    };
+    auto stage_in = [&](uint64_t *dptr, uint64_t n) -> int {
+        if (!dev && n) CK(cudaMemcpyAsync(dptr, rt->ms.h.data() + (dptr - rt->ms.d), 8 * n, cudaMemcpyHostToDevice, s), "stage in");
+        return 0;
+    };
+    /* 1. deltas grouped by owner; the G x G count matrix by all-gather */
+    std::vector<uint64_t> mine;
+    if ((rc = export_pass(-1, mine))) return rc;
+    std::vector<uint64_t> mat(G * (uint64_t)G);
+    {
+        /* counts travel through the recv-key region (device) or host staging */
+        uint64_t *tmp = rk;
+        CK(cudaMemcpyAsync(tmp, mine.data(), 8ull * G, cudaMemcpyHostToDevice, s), "counts");
+        uint8_t *src = stage_out(tmp, G);
+        uint8_t *dst = host_of(rv);
+        if ((rc = C.allgather(src, dst, 8ull * G, s))) return comm_err(rt, rc, "hash merge counts");
+        if (dev) {
+            CK(cudaMemcpyAsync(mat.data(), rv, 8ull * G * G, cudaMemcpyDeviceToHost, s), "counts");
+            CK(cudaStreamSynchronize(s), "counts");
+        } else {
+            memcpy(mat.data(), dst, 8ull * G * G);
+        }
+    }
+    /* 2. all-to-all of (key, delta) pairs: keys, then deltas */
+    std::vector<uint64_t> sb(G), so(G), rb(G), ro(G);
+    uint64_t nin = 0;
+    for (uint32_t g = 0, t = 0; g < G; g++) {
+        sb[g] = 8 * mine[g];
+        so[g] = 8ull * t;
+        t += (uint32_t)mine[g];
+        rb[g] = 8 * mat[(uint64_t)g * G + C.rank];
+        ro[g] = 8 * nin;
+        nin += mat[(uint64_t)g * G + C.rank];
+    }
+    uint64_t nout = 0;
+    for (uint32_t g = 0; g < G; g++) nout += mine[g];
+    for (int pass = 0; pass < 2; pass++) {
+        uint64_t *sp = pass ? sv : sk, *rp = pass ? rv : rk;
+        uint8_t *src = stage_out(sp, nout);
+        if ((rc = C.alltoallv(src, sb.data(), so.data(), host_of(rp), rb.data(), ro.data(), s)))
+            return comm_err(rt, rc, "hash merge all-to-all");
+        if ((rc = stage_in(rp, nin))) return rc;
+    }
+    /* 3. owner: base + every rank's deltas of its keys */
+    unsigned long long *full = cnt + 2 * G; /* one spare word after the offsets */
+    CK(cudaMemsetAsync(full, 0, 8, s), "memset");
+    CK(cudaMemcpyAsync(m.data, m.base, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash restore");
+    CK(cudaMemcpyAsync(m.aux, m.base_aux, 64, cudaMemcpyDeviceToDevice, s), "hash restore");
+    if (nin) {
+        int e = gx_k_hash_accumulate(&d, rk, rv, nin, full, s);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash accumulate");
+    }
+    /* 4. the owners' merged deltas to everybody */
+    std::vector<uint64_t> own;
+    if ((rc = export_pass((int32_t)C.rank, own))) return rc;
+    const uint64_t n_own = own[C.rank];
+    std::vector<uint64_t> all_n(G);
+    {
+        CK(cudaMemcpyAsync(rk, &n_own, 8, cudaMemcpyHostToDevice, s), "owner count");
+        uint8_t *src = stage_out(rk, 1);
+        uint8_t *dst = host_of(rv);
+        if ((rc = C.allgather(src, dst, 8, s))) return comm_err(rt, rc, "hash merge owner counts");
+        if (dev) {
+            CK(cudaMemcpyAsync(all_n.data(), rv, 8ull * G, cudaMemcpyDeviceToHost, s), "owner counts");
+            CK(cudaStreamSynchronize(s), "owner counts");
+        } else {
+            memcpy(all_n.data(), dst, 8ull * G);
+        }
+    }
+    /* the owner's entries start at its own offset in the export (owner >= 0 keeps only its keys) */
+    uint64_t own_off = 0;
+    for (int g = 0; g < C.rank; g++) own_off += own[g];
+    uint64_t ntot = 0;
+    for (uint32_t g = 0; g < G; g++) {
+        sb[g] = 8 * n_own;
+        so[g] = 8 * own_off;
+        rb[g] = 8 * all_n[g];
+        ro[g] = 8 * ntot;
+        ntot += all_n[g];
+    }
+    for (int pass = 0; pass < 2; pass++) {
+        uint64_t *sp = pass ? sv : sk, *rp = pass ? rv : rk;
+        uint8_t *src = stage_out(sp, own_off + n_own);
+        if ((rc = C.alltoallv(src, sb.data(), so.data(), host_of(rp), rb.data(), ro.data(), s)))
+            return comm_err(rt, rc, "hash merge all-gather");
+        if ((rc = stage_in(rp, ntot))) return rc;
+    }
+    /* 5. every rank: base + all merged deltas; commit as the new base */
+    CK(cudaMemcpyAsync(m.data, m.base, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash restore");
+    CK(cudaMemcpyAsync(m.aux, m.base_aux, 64, cudaMemcpyDeviceToDevice, s), "hash restore");
+    CK(cudaMemsetAsync(full, 0, 8, s), "memset");
+    if (ntot) {
+        int e = gx_k_hash_accumulate(&d, rk, rv, ntot, full, s);
+        if (e) return cuda_err(rt, (cudaError_t)e, "hash accumulate");
+    }
+    CK(cudaMemcpyAsync(m.base, m.data, m.data_bytes, cudaMemcpyDeviceToDevice, s), "hash commit");
+    CK(cudaMemcpyAsync(m.base_aux, m.aux, 64, cudaMemcpyDeviceToDevice, s), "hash commit");
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, full, 8, cudaMemcpyDeviceToHost, s), "hash full");
+    CK(cudaStreamSynchronize(s), "hash merge");
+    if (h) return set_err(rt, -E2BIG, "merged HASH union exceeds max_entries (%llu keys refused)", h);
+    return 0;
+}
+
+int comm_attach(gx_rt *rt, std::unique_ptr<GxComm> c) {
+    rt->comm = std::move(c);
+    rt->merges = 0;
+    /* the agreed initial state: every mergeable map's base snapshot, now */
+    for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+        Map &m = rt->maps[fd];
+        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) continue;
+        int rc = ensure_base(rt, m, true);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gx_comm_unique_id(void *id_out) {
+    if (!id_out) return -EINVAL;
+    NcclApi &a = nccl();
+    if (!a.ok) return -ENOSYS;
+    ncclUniqueId id;
+    if (a.getUniqueId(&id) != ncclSuccess) return -EIO;
+    memcpy(id_out, &id, sizeof id);
+    return 0;
+}
+
+int gx_comm_init(gx_rt *rt, const void *nccl_unique_id, int nranks, int rank) {
+    if (!rt || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return -EINVAL;
+    NcclApi &a = nccl();
+    if (!a.ok) return set_err(rt, -ENOSYS, "NCCL unavailable: %s", a.err.c_str());
+    CK(cudaSetDevice(rt->dev), "cudaSetDevice");
+    auto c = std::make_unique<NcclComm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof id);
+    ncclResult_t r = a.commInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess)
+        return set_err(rt, -EIO, "ncclCommInitRank: %s", a.getErrorString ? a.getErrorString(r) : "error");
+    return comm_attach(rt, std::move(c));
+}
+
+int gx_comm_init_host(gx_rt *rt, const gx_comm_host_ops *ops, int nranks, int rank) {
+    if (!rt || !ops || !ops->allreduce_sum_u64 || !ops->alltoallv || !ops->allgather || nranks < 1 || rank < 0 ||
+        rank >= nranks)
+        return -EINVAL;
+    auto c = std::make_unique<HostComm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->ops = *ops;
+    return comm_attach(rt, std::move(c));
+}
+
+int gx_merge(gx_rt *rt, void *cuda_stream) {
+    if (!rt) return -EINVAL;
+    if (!rt->comm) return set_err(rt, -EINVAL, "gx_merge before gx_comm_init");
+    CK(cudaSetDevice(rt->dev), "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    /* legality first, on every map (a refusal leaves every map untouched) */
+    for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+        const Map &m = rt->maps[fd];
+        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) continue;
+        if (const char *why = merge_illegal(rt, fd))
+            return set_err(rt, -EINVAL, "map %d cannot be merged (S3): %s", fd, why);
+    }
+    /* 1. additive maps (ARRAY, PERTHREAD folded): one packed u64 all-reduce of local - base */
+    uint64_t total = 0;
+    for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+        const Map &m = rt->maps[fd];
+        if (m.valid && (m.spec.type == GX_MAP_ARRAY || m.spec.type == GX_MAP_PERTHREAD_ARRAY))
+            total += (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+    }
+    if (total) {
+        int rc = ms_reserve(rt, total);
+        if (rc) return rc;
+        uint64_t off = 0;
+        for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+            const Map &m = rt->maps[fd];
+            if (!m.valid || (m.spec.type != GX_MAP_ARRAY && m.spec.type != GX_MAP_PERTHREAD_ARRAY)) continue;
+            rc = gx_merge_export(rt, fd, rt->ms.d + off, s);
+            if (rc) return rc;
+            off += (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+        }
+        uint64_t *buf = rt->ms.d;
+        if (!rt->comm->device_buffers()) {
+            CK(cudaMemcpyAsync(rt->ms.h.data(), rt->ms.d, 8 * total, cudaMemcpyDeviceToHost, s), "merge stage");
+            CK(cudaStreamSynchronize(s), "merge stage");
+            buf = rt->ms.h.data();
+        }
+        rc = rt->comm->allreduce_sum_u64(buf, total, s);
+        if (rc) return comm_err(rt, rc, "merge all-reduce");
+        if (!rt->comm->device_buffers())
+            CK(cudaMemcpyAsync(rt->ms.d, rt->ms.h.data(), 8 * total, cudaMemcpyHostToDevice, s), "merge stage");
+        off = 0;
+        for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+            const Map &m = rt->maps[fd];
+            if (!m.valid || (m.spec.type != GX_MAP_ARRAY && m.spec.type != GX_MAP_PERTHREAD_ARRAY)) continue;
+            rc = gx_merge_apply(rt, fd, rt->ms.d + off, s);
+            if (rc) return rc;
+            off += (uint64_t)m.spec.max_entries * m.spec.value_size / 8;
+        }
+    }
+    /* 2. HASH maps: key-sharded exchange */
+    for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
+        Map &m = rt->maps[fd];
+        if (!m.valid || m.spec.type != GX_MAP_HASH) continue;
+        int rc = ensure_base(rt, m);
+        if (rc) return rc;
+        rc = merge_hash(rt, m, s);
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(s), "merge");
+    rt->merges++;
+    return 0;
+}
+
+int gx_comm_free(gx_rt *rt) {
+    if (!rt) return -EINVAL;
+    rt->comm.reset();
     return 0;
 }
 

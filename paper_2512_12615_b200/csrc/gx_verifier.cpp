@@ -1117,7 +1117,7 @@ struct Verifier {
                 if (size < 8 && v.type == SCALAR) v.var = sc_unknown();
                 stack_write(st, sa - GX_STACK_SIZE, size, size == 8 ? &v : &val); /* narrow: bound only */
             } else if (map >= 0) {
-                out.use[map].used = out.use[map].writes = out.use[map].non_add_write = true;
+                out.use[map].used = out.use[map].writes = out.use[map].non_add_write = out.use[map].store = true;
             }
             P.pc++;
             return 0;
@@ -1143,7 +1143,7 @@ struct Verifier {
                 GxMapUse &u = out.use[map];
                 u.used = u.writes = true;
                 bool add = (r.imm & ~1) == 0x00;
-                if (!add) u.non_add_write = true;
+                if (!add) u.non_add_write = u.store = true;
                 if (size != 8) u.non_dw_atomic = true;
                 if (r.imm & 1) {
                     u.reads = true;
@@ -1444,6 +1444,7 @@ struct Verifier {
                 Reg &R4 = st.r[4];
                 if (R4.type != SCALAR) return fail(pc, R4.type == NOT_INIT ? GX_UNINIT_READ : GX_BAD_HELPER, "flags must be a scalar");
                 u.writes = u.non_add_write = u.update_call = true;
+                if (!sc_is_const(R4.var) || R4.var.t.v != 1) u.upd_overwrite = true; /* not BPF_NOEXIST */
                 P.ch += 2;
             } else {
                 P.ch += 1;

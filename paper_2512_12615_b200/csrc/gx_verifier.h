@@ -31,6 +31,8 @@ struct GxMapUse {
     bool fetch_add = false;      /* ATOMIC ADD|FETCH */
     bool update_call = false;    /* bpf_map_update_elem */
     bool non_dw_atomic = false;  /* a 32-bit atomic (privatised accumulators are u64 words) */
+    bool store = false;          /* a plain store or a non-ADD atomic (XCHG / CMPXCHG / OR / AND / XOR) */
+    bool upd_overwrite = false;  /* an update_elem whose flags are not the constant BPF_NOEXIST */
 };
 
 struct GxVerifyResult {

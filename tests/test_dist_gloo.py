@@ -1,4 +1,5 @@
-"""Multi-rank merge protocol (paper_2512_12615_b200.dist) on CPU: world_size 2 and 3 over gloo,
+"""Multi-rank S3 merge protocol (tests/merge_protocol.py, the reference implementation the C-ABI
+gx_merge is checked against on the GPU) on CPU: world_size 2 and 3 over gloo,
 each rank running its contiguous event shard on an ORACLE-backed engine.  The merged maps on every
 rank must equal (a) the oracle's own S3 snapshot-and-merge (ora_merge) and (b) for partition-
 insensitive configs, the single-environment unsharded run."""
@@ -93,7 +94,8 @@ def _worker(rank, world, port, config, n, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Oracle
-    from paper_2512_12615_b200.dist import Merger, shard_range
+    from paper_2512_12615_b200.dist import shard_range
+    from merge_protocol import ProtocolMerger as Merger
     env = Oracle()
     s = configs.setup(env, config)
     fds = [fd for fd in s.fds.values() if env.specs[fd][0] != RINGBUF]

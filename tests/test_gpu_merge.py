@@ -1,8 +1,10 @@
-"""GPU merge kernels through the C ABI (gx_merge_export / gx_merge_apply / gx_hash_export /
-gx_hash_apply) driven by the real protocol (paper_2512_12615_b200.dist.Merger): two processes
-share cuda:0 (NCCL refuses two ranks on one device, so the collectives run over gloo with host
-staging -- the 8-GPU NCCL path is the same Merger on CUDA tensors).  Every rank must end with the
-oracle's own S3 snapshot-and-merge of the same shards (loopback merge)."""
+"""The C-ABI multi-GPU merge (gx_comm_init / gx_merge, include/gx.h) against the oracle's S3
+snapshot-and-merge (SURVEY.md §8c c.3 S3, §8e loopback).  G processes share cuda:0: NCCL refuses two
+ranks on one device, so the ranks join through gx_comm_init_host with gloo collectives on host
+buffers (paper_2512_12615_b200.dist.comm_init); every other step -- delta export, packing, the
+owner-sharded HASH exchange, apply -- is the same gx_merge code the NCCL path runs.  The NCCL path
+itself runs at G = 1 here (and at G = 2..8 in `bench.py --gpus N`).  Every rank must end with the
+oracle's merged maps, at G = 2, 3 and 8 (C5 at 2^24 events: SURVEY.md §8d parity matrix)."""
 import os
 import socket
 
@@ -30,36 +32,11 @@ def _worker(rank, world, port, config, n, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2512_12615_b200 as gx
-    from paper_2512_12615_b200.dist import GxEngine, Merger, shard_range
-
-    class Staged(GxEngine):
-        def __init__(self, rt):
-            super().__init__(rt)
-            self.gpu = self.device
-            self.device = torch.device("cpu")
-
-        def merge_export(self, fd, out):
-            tmp = torch.empty(out.shape, dtype=out.dtype, device=self.gpu)
-            super().merge_export(fd, tmp)
-            out.copy_(tmp.cpu())
-
-        def merge_apply(self, fd, total):
-            super().merge_apply(fd, total.to(self.gpu))
-            torch.cuda.synchronize()
-
-        def hash_export(self, fd, nranks, owner):
-            self.device = self.gpu
-            k, v, c = super().hash_export(fd, nranks, owner)
-            self.device = torch.device("cpu")
-            return k.cpu(), v.cpu(), c
-
-        def hash_apply(self, fd, keys, vals, restore, commit):
-            super().hash_apply(fd, keys.to(self.gpu), vals.to(self.gpu), restore, commit)
+    from paper_2512_12615_b200.dist import Merger, shard_range
 
     rt = gx.Runtime(0)
     s = configs.setup(rt, config)
-    fds = [fd for fd in s.fds.values() if rt.specs[fd][0] != RINGBUF]
-    m = Merger(Staged(rt), fds)
+    m = Merger(rt)
     i0, i1 = shard_range(n, rank, world)
     ev = configs.events(config, configs.SEEDS[config], i1 - i0, i0, n)
     d_ev = torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda()
@@ -73,18 +50,19 @@ def _worker(rank, world, port, config, n, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("config", ["C2", "C3", "C5"])
-def test_gpu_merge_matches_oracle_s3(gpu, config):
+@pytest.mark.parametrize("config,world,lg", [("C2", 2, 16), ("C3", 2, 16), ("C4", 3, 16), ("C5", 2, 16),
+                                             ("C5", 8, 24)])
+def test_gpu_merge_matches_oracle_s3(gpu, config, world, lg):
     from oracle.oracle import Oracle
     from paper_2512_12615_b200.dist import shard_range
-    world, n = 2, (1 << 16) + 64
+    n = (1 << lg) + 64
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, config, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=300) for _ in range(world))
+    res = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
@@ -103,3 +81,43 @@ def test_gpu_merge_matches_oracle_s3(gpu, config):
     want = {key: init.dump(fd) for key, fd in si.fds.items() if init.specs[fd][0] != RINGBUF}
     for r in range(world):
         assert res[r] == want, (config, r)
+
+
+def test_merge_nccl_single_rank(gpu):
+    """The NCCL transport itself (gx_comm_init at G = 1): a merge leaves every map as it is."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    rt = gx.Runtime(0)
+    s = configs.setup(rt, "C5")
+    gx.gx_comm_init(rt.rt, gx.gx_comm_unique_id(), 1, 0)
+    ev = configs.events("C5", configs.SEEDS["C5"], 1 << 16)
+    rt.run(torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda(), s.prog_arg)
+    before = {key: rt.dump(fd) for key, fd in s.fds.items() if rt.specs[fd][0] != RINGBUF}
+    gx.gx_merge(rt.rt)
+    after = {key: rt.dump(fd) for key, fd in s.fds.items() if rt.specs[fd][0] != RINGBUF}
+    assert before == after
+    rt.run(torch.from_numpy(ev.view(np.uint8).reshape(-1, 32)).cuda(), s.prog_arg)
+    gx.gx_merge(rt.rt)   # the base advanced: a second batch merges onto the first
+    rt.close()
+
+
+def test_merge_refuses_non_additive_maps(gpu):
+    """S3 legality: an ARRAY written by a plain store (or a HASH updated with BPF_ANY) has no
+    snapshot-and-merge -- gx_merge returns -EINVAL and leaves every map untouched."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import asm
+    for text, spec in (("ldxdw r2, [r1+0]\nstdw [r10-8], 0\nmov64 r3, 0\nstxw [r10-4], r3\nlddw r1, map:m\n"
+                        "mov64 r2, r10\nadd64 r2, -4\ncall 1\njeq r0, 0, +1\nstdw [r0+0], 7\nmov64 r0, 0\nexit",
+                        (2, 4, 8, 4)),
+                       ("ldxdw r2, [r1+0]\nstxdw [r10-8], r2\nstdw [r10-16], 1\nlddw r1, map:m\nmov64 r2, r10\n"
+                        "add64 r2, -8\nmov64 r3, r10\nadd64 r3, -16\nmov64 r4, 0\ncall 2\nmov64 r0, 0\nexit",
+                        (1, 8, 8, 64))):
+        rt = gx.Runtime(0)
+        fd = rt.create_map(*spec)
+        rt.load_prog(asm.assemble(text, {"m": fd}))
+        gx.gx_comm_init(rt.rt, gx.gx_comm_unique_id(), 1, 0)
+        with pytest.raises(gx.GxError) as e:
+            gx.gx_merge(rt.rt)
+        assert e.value.errno == 22
+        rt.close()
