@@ -931,15 +931,12 @@ ORA_EXPORT int ora_sched_run(ora_env *e, int prog, uint32_t n_units, const uint3
 
 /* ------------------------------------------------------------------ canonical dumps (O8) */
 
-static int cmp_key_le(const uint8_t *a, const uint8_t *b, uint32_t n) {
-    for (int k = (int)n - 1; k >= 0; k--) if (a[k] != b[k]) return a[k] < b[k] ? -1 : 1;
-    return 0;
-}
-
-static uint32_t g_sort_ksz;
+/* hash dump order: keys (at most 8 bytes) as unsigned little-endian integers; the sort key travels
+ * with each entry (no global: environments may be dumped from several threads at once) */
+typedef struct { uint64_t k; const hnode *n; } hsort_t;
 static int hcmp(const void *x, const void *y) {
-    const hnode *a = *(hnode *const *)x, *b = *(hnode *const *)y;
-    return cmp_key_le(a->key, b->key, g_sort_ksz);
+    const hsort_t *a = x, *b = y;
+    return a->k < b->k ? -1 : a->k > b->k ? 1 : 0;
 }
 
 /* ARRAY: max*vs bytes.  PT: per key, per 8-byte word, the SUM over shards (S4).  HASH: entries
@@ -970,15 +967,17 @@ ORA_EXPORT int ora_map_dump(ora_env *e, int fd, void *buf, uint64_t cap, uint64_
     if (m->type == MAP_HASH) {
         uint64_t es = m->key_size + m->value_size;
         if (m->count * es > cap) return -E_2BIG;
-        hnode **all = malloc((m->count + 1) * sizeof *all);
+        hsort_t *all = malloc((m->count + 1) * sizeof *all);
         uint64_t c = 0;
         for (uint64_t b = 0; b < m->nbuckets; b++)
-            for (hnode *n = m->buckets[b]; n; n = n->next) all[c++] = n;
-        g_sort_ksz = m->key_size;
+            for (hnode *n = m->buckets[b]; n; n = n->next) {
+                all[c].k = load_le(n->key, m->key_size);
+                all[c++].n = n;
+            }
         qsort(all, c, sizeof *all, hcmp);
         for (uint64_t i = 0; i < c; i++) {
-            memcpy(out + i * es, all[i]->key, m->key_size);
-            memcpy(out + i * es + m->key_size, all[i]->val, m->value_size);
+            memcpy(out + i * es, all[i].n->key, m->key_size);
+            memcpy(out + i * es + m->key_size, all[i].n->val, m->value_size);
         }
         free(all);
         *n_out = c;
