@@ -322,15 +322,18 @@ def program(seed: int, n_snippets: int | None = None, allow=None) -> str:
     return _Gen(rng, n, allow).program()
 
 
-def events(seed: int, n: int, n_tenants: int = 1, skip_tenant: bool = False) -> np.ndarray:
+def events(seed: int, n: int, n_tenants: int = 1, skip_tenant: bool = False, contract: bool = False) -> np.ndarray:
     """n <= 8192 events: the low 13 address bits are a permutation of [0, 8192) (unique keys);
-    every other field is either record-uniform or lane-varying, per field and batch."""
+    every other field is either record-uniform or lane-varying, per field and batch
+    (`contract`: every field §8b tags UNIFORM is record-uniform, as a warp-level hook produces it)."""
     assert n <= MAX_EVENTS
     rng = np.random.default_rng(seed ^ 0xF022)
     rec = np.arange(n) >> 5
 
     def field(bits, uniform_p=0.5):
         hi = (1 << bits) - 1
+        if contract and uniform_p != 0.3:
+            uniform_p = 1.0
         if rng.random() < uniform_p:
             per_rec = rng.integers(0, hi, size=rec[-1] + 1 if n else 1, dtype=np.uint64, endpoint=True)
             return per_rec[rec] if n else per_rec[:0]
@@ -339,8 +342,10 @@ def events(seed: int, n: int, n_tenants: int = 1, skip_tenant: bool = False) -> 
     u = rng.permutation(MAX_EVENTS)[:n].astype(np.uint64)
     addr = (field(51, 0.3) << np.uint64(UBITS)) | u
     tenants = n_tenants + (1 if skip_tenant else 0)
-    ten = rng.integers(0, tenants, size=n) if rng.random() < 0.5 else rng.integers(0, tenants, size=rec[-1] + 1 if n else 1)[rec]
+    ten = rng.integers(0, tenants, size=n) if rng.random() < 0.5 and not contract else rng.integers(0, tenants, size=rec[-1] + 1 if n else 1)[rec]
     kind = np.where(rng.random(n) < 0.2, 2, 0) if n_tenants > 1 else np.zeros(n, dtype=np.int64)
+    if contract and n and n_tenants > 1:
+        kind = np.where(rng.random(rec[-1] + 1) < 0.2, 2, 0)[rec]
     hook = (kind | (ten.astype(np.int64) << 8)).astype(np.uint32) if n else np.zeros(0, dtype=np.uint32)
     return gen.records(n, addr=addr, ts=field(64), hook=hook, block_id=field(32).astype(np.uint32),
                        sm_id=field(16).astype(np.uint16), warp_id=field(8).astype(np.uint8),

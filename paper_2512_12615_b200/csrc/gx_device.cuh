@@ -164,8 +164,12 @@ __device__ __forceinline__ uint64_t *hash_find(const GxMapDesc &m, uint64_t key)
     return nullptr;
 }
 
+/* 1: the doing lanes of a warp run their insert attempts in lock-step rounds (required: with each
+ * lane on its own, a lane waiting for reservations can starve a reservation holder of its own warp --
+ * independent thread scheduling gives a spinning branch no fairness -- until the safety valve
+ * refuses the insert; the fuzz caught it at a 1024-entry map filled to capacity) */
 #ifndef GX_HASH_LOCKSTEP
-#define GX_HASH_LOCKSTEP 0
+#define GX_HASH_LOCKSTEP 1
 #endif
 #ifndef GX_HASH_VALVE
 #define GX_HASH_VALVE (1u << 20)
@@ -347,8 +351,7 @@ __device__ GXD_COLD int64_t hash_update_coop(const GxMapDesc m, uint64_t key, ui
         }
     }
 #else
-    /* each doing lane on its own: a lane that has to wait for in-flight reservations backs off with
-     * __nanosleep, which lets a reservation holder of its own warp run (hash_update) */
+    /* each doing lane on its own (measurement knob only; see GX_HASH_LOCKSTEP) */
     int64_t rc = 0;
     if (is_doer) {
         bool f;

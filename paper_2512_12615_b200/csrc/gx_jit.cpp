@@ -331,12 +331,24 @@ struct Gen {
         if (dmode_) st("mypc = " + std::to_string(t) + "u; continue;");
         else st("goto U" + std::to_string(t) + ";");
     }
-    void branch(const std::string &cond, uint32_t t, uint32_t nx) {
+    /* a conditional branch.  `uni`: the verifier's divergence analysis proved the condition warp-
+     * uniform (GXF_UNIFORM: every lane that reaches the branch together takes it the same way), so
+     * the uniform copy branches without a ballot.  GX_JIT_UNIFORM_CHECK=1 keeps the ballot and
+     * counts any split of such a branch in the divergent_steps stat (tests: it must stay 0). */
+    void branch(const std::string &cond, uint32_t t, uint32_t nx, bool uni = false) {
         if (dmode_) {
             st("mypc = (" + cond + ") ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; continue;");
             return;
         }
+        const bool check = getenv("GX_JIT_UNIFORM_CHECK") && atoi(getenv("GX_JIT_UNIFORM_CHECK")) != 0;
+        if (uni && !check) {
+            st("if (" + cond + ") goto U" + std::to_string(t) + "; goto U" + std::to_string(nx) + ";");
+            return;
+        }
         st("{ const bool t_ = " + cond + "; const unsigned tb_ = __ballot_sync(active, t_);");
+        if (uni)
+            st("  if (tb_ != active && tb_ != 0 && (threadIdx.x & 31) == (unsigned)(__ffs(active) - 1)) "
+               "atomicAdd((unsigned long long *)" + hex(L.stats) + " + " + std::to_string(GXS_DIVERGENT) + ", 1ull);");
         st("  if (tb_ == active) goto U" + std::to_string(t) + "; if (tb_ == 0) goto U" + std::to_string(nx) + ";");
         st("  mypc = t_ ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; goto DIV; }");
     }
@@ -477,8 +489,8 @@ struct Gen {
                 me("const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
                    " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0;");
             }
-            if (g.flags & GXF_FETCH) branch("r0 == 0", (uint32_t)g.imm, i + 1);
-            if (g.flags & GXF_W32) branch("r0 != 0", (uint32_t)g.imm, i + 1);
+            if (g.flags & GXF_FETCH) branch("r0 == 0", (uint32_t)g.imm, i + 1, (g.flags & GXF_UNIFORM) != 0);
+            if (g.flags & GXF_W32) branch("r0 != 0", (uint32_t)g.imm, i + 1, (g.flags & GXF_UNIFORM) != 0);
             break;
         }
         case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: {
@@ -582,7 +594,7 @@ struct Gen {
                     goto_next(v.join);
                     st("}");
                 } else {
-                    branch(c, g.aux, i + 1);
+                    branch(c, g.aux, i + 1, (g.flags & GXF_UNIFORM) != 0);
                 }
             } else {
                 st("c_herr++;");
@@ -659,7 +671,7 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_PIN")) o << "#define GX_PIN " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_ATOM_MIXED")) o << "#define GX_ATOM_MIXED " << atoi(e) << "\n";
         if (getenv("GX_JIT_COLD_INLINE")) o << "#define GX_COLD_INLINE 1\n";
-        if (getenv("GX_JIT_LOCKSTEP")) o << "#define GX_HASH_LOCKSTEP 1\n";
+        if (const char *e = getenv("GX_JIT_LOCKSTEP")) o << "#define GX_HASH_LOCKSTEP " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PROBE_W")) o << "#define GX_HASH_PROBE_W " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";

@@ -1593,6 +1593,212 @@ struct Verifier {
         return U_UNI;
     }
 
+    /* ---------------------------------------------------------------- stage 4b: divergence analysis
+     * Sound warp-uniformity of each conditional branch, for the JIT's ballot-free branches
+     * (GXF_UNIFORM).  Data flow as in simt(), except that EVERY ctx field is LANE_VARYING (§8b's
+     * UNIFORM tags are a performance contract, not a guarantee), plus control dependence: at the
+     * immediate post-dominator of a branch whose condition is LANE_VARYING, everything written
+     * between the branch and that join is LANE_VARYING -- lanes arrive there from different paths
+     * or after different iteration counts.  A branch whose operands stay UNIFORM is taken the same
+     * way by every lane that reaches it together (a counted loop's exit, C4's 12 binary-search
+     * steps), so it needs no ballot. */
+    void divergence() {
+        const uint32_t N = n, X = n; /* X: virtual exit */
+        std::vector<std::vector<uint32_t>> succ(N);
+        std::vector<uint8_t> is_insn(N, 0), is_jcc(N, 0);
+        for (uint32_t pc = 0; pc < N; pc++) {
+            if (pc > 0 && is_insn[pc - 1] && (ins[pc - 1].code & 7) == CL_LD) continue; /* 2nd ldimm64 slot */
+            is_insn[pc] = 1;
+            const Raw &r = ins[pc];
+            const uint32_t cls = r.code & 7, op = r.code & 0xF0;
+            if (cls == CL_LD) succ[pc].push_back(pc + 2);
+            else if (cls == CL_JMP || cls == CL_JMP32) {
+                if (op == 0x90) { /* exit */
+                } else if (op == 0x80) succ[pc].push_back(pc + 1);
+                else if (op == 0x00) succ[pc].push_back(pc + 1 + r.off);
+                else {
+                    is_jcc[pc] = 1;
+                    succ[pc].push_back(pc + 1 + r.off);
+                    succ[pc].push_back(pc + 1);
+                }
+            } else succ[pc].push_back(pc + 1);
+            for (uint32_t &s : succ[pc])
+                if (s >= N) s = X;
+        }
+        /* post-dominators (bit sets over N + 1 nodes) */
+        const uint32_t W = (N + 1 + 63) / 64;
+        std::vector<uint64_t> pd((uint64_t)(N + 1) * W, ~0ull);
+        auto row = [&](uint32_t v) { return pd.data() + (uint64_t)v * W; };
+        std::fill(row(X), row(X) + W, 0ull);
+        row(X)[X / 64] |= 1ull << (X % 64);
+        for (bool ch = true; ch;) {
+            ch = false;
+            for (int64_t p = (int64_t)N - 1; p >= 0; p--) {
+                if (!is_insn[p]) continue;
+                std::vector<uint64_t> t(W, ~0ull);
+                if (succ[p].empty()) { /* exit */
+                    std::fill(t.begin(), t.end(), 0ull);
+                    t[X / 64] |= 1ull << (X % 64);
+                } else {
+                    for (uint32_t s : succ[p])
+                        for (uint32_t w = 0; w < W; w++) t[w] &= row(s)[w];
+                }
+                t[p / 64] |= 1ull << (p % 64);
+                for (uint32_t w = 0; w < W; w++)
+                    if (row((uint32_t)p)[w] != t[w]) {
+                        std::copy(t.begin(), t.end(), row((uint32_t)p));
+                        ch = true;
+                        break;
+                    }
+            }
+        }
+        auto popc = [&](uint32_t v) {
+            uint32_t c = 0;
+            for (uint32_t w = 0; w < W; w++) c += (uint32_t)__builtin_popcountll(row(v)[w]);
+            return c;
+        };
+        auto ipdom = [&](uint32_t b) -> uint32_t { /* the strict post-dominator with the most post-dominators */
+            const uint32_t want = popc(b) - 1;
+            for (uint32_t v = 0; v <= N; v++)
+                if (v != b && ((row(b)[v / 64] >> (v % 64)) & 1) && (v == X || is_insn[v]) && popc(v) == want) return v;
+            return X;
+        };
+        /* written variables of one instruction: registers 0..10, stack slots 11.. */
+        auto defs = [&](uint32_t pc, std::vector<uint32_t> &out) {
+            const Raw &r = ins[pc];
+            const Fact &f = facts[pc];
+            const uint32_t cls = r.code & 7, op = r.code & 0xF0;
+            if (cls == CL_ALU || cls == CL_ALU64 || cls == CL_LD || cls == CL_LDX) out.push_back(r.dst);
+            else if (cls == CL_ST || cls == CL_STX) {
+                if (f.kind == MK_STACK) out.push_back(11 + f.stack_addr / 8);
+                if (cls == CL_STX && (r.code & 0xE0) == 0xC0 && (r.imm & 1)) out.push_back(r.imm == 0xF1 ? 0 : r.src);
+            } else if ((cls == CL_JMP || cls == CL_JMP32) && op == 0x80) out.push_back(0);
+        };
+        std::vector<UState> in(N);
+        std::vector<uint8_t> has(N, 0), var_br(N, 0);
+        std::vector<UState> inject(N);
+        std::vector<uint8_t> has_inj(N, 0);
+        auto join = [](UState &a, const UState &b) {
+            bool c = false;
+            for (int i = 0; i < 11; i++)
+                if (b.r[i] > a.r[i]) a.r[i] = b.r[i], c = true;
+            for (int i = 0; i < GX_STACK_SIZE / 8; i++)
+                if (b.s[i] > a.s[i]) a.s[i] = b.s[i], c = true;
+            return c;
+        };
+        for (int round = 0; round < 64; round++) {
+            std::fill(has.begin(), has.end(), 0);
+            UState e{};
+            e.r[1] = U_VAR; /* the ctx pointer differs per lane; its loads are LANE_VARYING below anyway */
+            e.r[10] = U_UNI;
+            in[0] = e;
+            has[0] = 1;
+            if (has_inj[0]) join(in[0], inject[0]);
+            std::vector<uint32_t> work{0};
+            while (!work.empty()) {
+                const uint32_t pc = work.back();
+                work.pop_back();
+                UState u = in[pc];
+                const Raw &r = ins[pc];
+                const Fact &f = facts[pc];
+                const uint32_t cls = r.code & 7, op = r.code & 0xF0;
+                const bool x = r.code & 0x08;
+                if (cls == CL_ALU || cls == CL_ALU64) {
+                    if (op == 0xB0 && r.off == 0) u.r[r.dst] = x ? u.r[r.src] : U_UNI;
+                    else if (x) u.r[r.dst] = std::max(u.r[r.dst], u.r[r.src]);
+                } else if (cls == CL_LD) {
+                    u.r[r.dst] = U_UNI;
+                } else if (cls == CL_LDX) {
+                    if (f.kind == MK_STACK) u.r[r.dst] = std::max(u.s[f.stack_addr / 8], u.r[r.src]);
+                    else u.r[r.dst] = U_VAR; /* ctx (every field) and map values */
+                } else if (cls == CL_ST || cls == CL_STX) {
+                    if ((r.code & 0xE0) == 0xC0) {
+                        if (r.imm & 1) u.r[r.imm == 0xF1 ? 0 : r.src] = U_VAR;
+                        if (f.kind == MK_STACK) u.s[f.stack_addr / 8] = U_VAR;
+                    } else if (f.kind == MK_STACK) {
+                        const uint8_t v = std::max(cls == CL_ST ? (uint8_t)U_UNI : u.r[r.src], u.r[r.dst]);
+                        const uint32_t sz = size_of(r.code);
+                        u.s[f.stack_addr / 8] = sz == 8 ? v : std::max(u.s[f.stack_addr / 8], v);
+                    }
+                } else if ((cls == CL_JMP || cls == CL_JMP32) && op == 0x80) {
+                    uint8_t keyu = U_UNI;
+                    if (f.key_kind == MK_STACK) {
+                        const GxMapInfo &mi = maps[f.map];
+                        for (uint32_t b = 0; b < mi.key_size; b += 8) keyu = std::max(keyu, u.s[(f.key_addr + b) / 8]);
+                    } else if (f.key_kind == MK_MAPV) {
+                        keyu = U_VAR;
+                    }
+                    const bool shared = f.map >= 0 && maps[f.map].type != PT;
+                    for (int i = 1; i <= 5; i++) u.r[i] = U_UNINIT;
+                    u.r[0] = (r.imm == 1 && shared && keyu == U_UNI) ? U_UNI : U_VAR;
+                } else if (is_jcc[pc]) {
+                    const uint8_t c = std::max(u.r[r.dst], x ? u.r[r.src] : (uint8_t)U_UNI);
+                    if (c == U_VAR) var_br[pc] = 1;
+                }
+                for (uint32_t s : succ[pc]) {
+                    if (s >= N) continue;
+                    if (!has[s]) {
+                        in[s] = u;
+                        if (has_inj[s]) join(in[s], inject[s]);
+                        has[s] = 1;
+                        work.push_back(s);
+                    } else if (join(in[s], u)) {
+                        work.push_back(s);
+                    }
+                }
+            }
+            /* control dependence ("sync dependence"): lanes that split at a LANE_VARYING branch meet
+             * again at every node reachable from both of its sides (up to the immediate post-
+             * dominator, which both reach); everything written on the way is LANE_VARYING there */
+            bool grew = false;
+            for (uint32_t b = 0; b < N; b++) {
+                if (!var_br[b] || succ[b].size() != 2 || succ[b][0] == succ[b][1]) continue;
+                const uint32_t j = ipdom(b);
+                std::vector<uint8_t> side[2] = {std::vector<uint8_t>(N, 0), std::vector<uint8_t>(N, 0)};
+                for (int k = 0; k < 2; k++) {
+                    std::vector<uint32_t> st2;
+                    const uint32_t s0 = succ[b][k];
+                    if (s0 < N && s0 != j) side[k][s0] = 1, st2.push_back(s0);
+                    while (!st2.empty()) {
+                        const uint32_t p = st2.back();
+                        st2.pop_back();
+                        for (uint32_t q : succ[p])
+                            if (q < N && q != j && !side[k][q]) side[k][q] = 1, st2.push_back(q);
+                    }
+                }
+                std::vector<uint32_t> dv;
+                for (uint32_t p = 0; p < N; p++)
+                    if (side[0][p] || side[1][p]) defs(p, dv);
+                if (dv.empty()) continue;
+                UState add{};
+                for (uint32_t v : dv) {
+                    if (v < 11) add.r[v] = U_VAR;
+                    else add.s[v - 11] = U_VAR;
+                }
+                auto put = [&](uint32_t v) {
+                    if (!has_inj[v]) {
+                        inject[v] = add;
+                        has_inj[v] = 1;
+                        grew = true;
+                    } else if (join(inject[v], add)) {
+                        grew = true;
+                    }
+                };
+                if (j < N) put(j);
+                for (uint32_t p = 0; p < N; p++)
+                    if (side[0][p] && side[1][p]) put(p);
+            }
+            if (!grew) break;
+        }
+        for (uint32_t pc = 0; pc < N; pc++)
+            if (is_jcc[pc]) hint_uniform[pc] = (has[pc] && !var_br[pc]) ? 1 : 0;
+        if (getenv("GX_VERIFY_DEBUG"))
+            for (uint32_t pc = 0; pc < N; pc++)
+                if (is_jcc[pc])
+                    fprintf(stderr, "divergence: pc %u %s (dst %u: %d, src %u: %d)\n", pc, hint_uniform[pc] ? "UNIFORM" : "varying",
+                            ins[pc].dst, has[pc] ? in[pc].r[ins[pc].dst] : -1, ins[pc].src, has[pc] ? in[pc].r[ins[pc].src] : -1);
+    }
+
     bool simt(bool strict, uint32_t &all_uniform) {
         std::vector<UState> in(n);
         std::vector<uint8_t> has(n, 0);
@@ -2026,6 +2232,7 @@ struct Verifier {
             } else if ((a.op == GX_CALL_LOOKUP_ARRAY || a.op == GX_CALL_LOOKUP_PT || a.op == GX_CALL_LOOKUP_HASH) &&
                        (b.op == GX_JEQ || b.op == GX_JNE) && b.dst == 0 && !(b.flags & GXF_X) && b.imm == 0) {
                 a.flags |= b.op == GX_JEQ ? GXF_FETCH /* jump if NULL */ : GXF_W32 /* jump if not NULL */;
+                a.flags |= b.flags & GXF_UNIFORM; /* a warp-uniform key: every lane finds the same entry */
                 a.imm = b.aux;
                 removed[j] = 1;
             } else if (a.op == GX_MOV64 && !(a.flags & GXF_X) &&
@@ -2083,6 +2290,7 @@ int gx_verify_program(const uint8_t *slots, uint32_t n, const GxMapInfo *maps, c
     if (ok) {
         v.hint_uniform.assign(n, 1);
         ok = v.simt(opts.simt_strict != 0, all_uniform);
+        if (ok) v.divergence(); /* the sound GXF_UNIFORM branch hints the JIT relies on */
     } else if (st_ok && opts.simt_strict && !v.viol.empty() &&
                (v.viol[0].rule == GX_BUDGET || v.viol[0].rule == GX_COMPLEXITY || v.viol[0].rule == GX_UNBOUNDED_LOOP)) {
         /* strict mode: a loop that never terminates in exploration is usually a lane-varying loop

@@ -32,7 +32,7 @@ def setup(engine, texts, seed, verify=None):
     return fds, -1
 
 
-def outputs(engine, fds):
+def outputs(engine, fds, keep_stats=False):
     out = {}
     for name, fd in fds.items():
         if fp.MAPS[name][0] == RINGBUF:
@@ -41,6 +41,8 @@ def outputs(engine, fds):
             out[name] = engine.dump(fd)
     st = engine.stats()
     out["stats"] = tuple(st[k] for k in COMPARED_STATS)
+    if keep_stats:
+        out["_stats"] = st
     return out
 
 

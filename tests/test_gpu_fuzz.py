@@ -40,7 +40,7 @@ def _gpu(texts, ev, seed, rt):
     rt.run(d_ev, prog, ret=ret)
     torch.cuda.synchronize()
     r0 = ret.cpu().numpy().view(np.uint64)
-    return r0, fu.outputs(rt, fds)
+    return r0, fu.outputs(rt, fds, keep_stats=True)
 
 
 def _check(seed, engine):
@@ -49,6 +49,7 @@ def _check(seed, engine):
     rt = make_runtime(engine, set_env=False)
     try:
         r0g, og = _gpu(texts, ev, seed, rt)
+        split = og.pop("_stats")["divergent_steps"] if engine == "jit" else og.pop("_stats") and 0
     finally:
         rt.close()
     bad = np.nonzero(r0o != r0g)[0]
@@ -59,6 +60,8 @@ def _check(seed, engine):
     for k in oo:
         if oo[k] != og[k]:
             errs.append(f"{k}: {fu.first_diff(oo[k], og[k])}")
+    if split:   # GX_JIT_UNIFORM_CHECK=1: a branch the divergence analysis called uniform split
+        errs.append(f"{split} warp splits at GXF_UNIFORM branches")
     return seed, len(texts), errs, texts
 
 
@@ -83,10 +86,14 @@ def test_fuzz_interp(gpu):
 
 def test_fuzz_jit(gpu):
     os.environ.pop("GX_JIT_INGEST", None)
+    os.environ["GX_JIT_UNIFORM_CHECK"] = "1"   # ballot kept at GXF_UNIFORM branches, splits counted
     ncpu = len(os.sched_getaffinity(0))
     k = max(50, N_CASES // 5)
-    n = _run_cases("jit", list(range(10000, 10000 + k)), threads=max(4, ncpu))
-    print(f"jit (register ingest): {k} cases, {n} programs byte-equal to the oracle")
+    try:
+        n = _run_cases("jit", list(range(10000, 10000 + k)), threads=max(4, ncpu))
+    finally:
+        os.environ.pop("GX_JIT_UNIFORM_CHECK", None)
+    print(f"jit (register ingest): {k} cases, {n} programs byte-equal to the oracle, no split at a GXF_UNIFORM branch")
 
 
 def test_fuzz_jit_ring(gpu):
