@@ -271,7 +271,8 @@ def config_records(device, args):
                            "bound": bound, "frac": comp[bound] / ms, "R_atom_per_s": r_atom, "A_alg": A_ALG[config],
                            "insns_per_event": insns, "f_sm_mhz": f_sm / 1e6,
                            "parity": ("exact" if same else "mismatch") + " (2^16-event sample vs oracle)",
-                           "events_accounted": bool(run_ok)}
+                           "events_accounted": bool(run_ok), "ringbuf_drops": st["ringbuf_drops"],
+                           "hash_full": st["hash_full"]}
             del ev
             rt.close()
         except Exception as exc:  # pragma: no cover - box-dependent
@@ -499,10 +500,11 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.extra:
-            extra_lines(rt, args)
-            f2_lines()
-            f4_lines()
-            f3_lines()
+            for fn in (lambda: extra_lines(rt, args), f2_lines, f2_l2_line, f4_lines, f3_lines):
+                try:
+                    fn()
+                except Exception as exc:  # pragma: no cover - box-dependent; the headline is printed
+                    print(json.dumps({"extra_error": repr(exc)[:300]}), file=sys.stderr, flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -686,6 +688,60 @@ def f2_lines():
         del ev
 
 
+def f2_l2_line():
+    """SURVEY.md §8f f2, the device half (stderr): the paper's prefetch microbenchmark shape
+    (a vector add over managed memory whose pages start on the host; device-side
+    prefetch.global.L2 "trigger[s] non-blocking page faults").  c = a + b over 2^28 floats in one
+    managed buffer, P7 (L2 stride prefetch, distance d ahead of every hooked load) inlined on both
+    loads; controls: the kernel without hooks, and with hooks whose prefetch length is 0 (-EINVAL:
+    the hook cost without any prefetch).  Pages are moved back to the host before every launch."""
+    import torch
+    import cuda.bindings.runtime as cr
+    import paper_2512_12615_b200 as gx
+    from gxin import asm, instrument
+    n = 1 << 28
+    err, buf = cr.cudaMallocManaged(8 * n, cr.cudaMemAttachFlags.cudaMemAttachGlobal)
+    if int(err) != 0:
+        print(json.dumps({"f2": "l2_uvm", "skipped": f"cudaMallocManaged: {err}"}), file=sys.stderr, flush=True)
+        return
+    a, b = int(buf), int(buf) + 4 * n
+    c = torch.empty(n, device="cuda")
+    rt = gx.Runtime(0)
+    region = rt.region_map(int(buf), 8 * n)
+
+    def timed(k, reps=4):
+        out = []
+        for i in range(reps + 1):
+            cr.cudaMemPrefetchAsync(buf, 8 * n, -1, 0)                # back to the host (cudaCpuDeviceId)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gx.gx_kernel_launch(rt.rt, k, "vadd", ((n + 255) // 256,), (256,), [a, b, c, 0, n])
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                out.append(e0.elapsed_time(e1))
+        return float(np.median(out))
+
+    line = {"f2": "l2_uvm", "elements": n, "bytes": 12 * n}
+    k0 = gx.gx_instrument(rt.rt, rt.load_prog(asm.assemble("mov64 r0, 0\nexit")), "#define GX_HOOKS 0\n" + instrument.VADD)
+    line["ms_plain"] = timed(k0)
+    gx.gx_kernel_free(rt.rt, k0)
+    for dist, ln in ((0, 0), (1 << 20, 128), (4 << 20, 128), (16 << 20, 128)):
+        fds = instrument.setup_l2(rt, region, dist, ln)
+        k = gx.gx_instrument(rt.rt, rt.load_prog(asm.assemble(instrument.P7_L2_STRIDE, fds)), instrument.VADD)
+        key = "ms_hooks_no_prefetch" if ln == 0 else f"ms_l2_dist_{dist >> 20}MiB"
+        line[key] = timed(k)
+        line[key.replace("ms_", "outcome_")] = rt.array_u64(fds["outcome"]).tolist()
+        gx.gx_kernel_free(rt.rt, k)
+    best = min(v for kk, v in line.items() if kk.startswith("ms_l2"))
+    line["speedup_best_vs_plain"] = line["ms_plain"] / best
+    line["speedup_best_vs_hooks"] = line["ms_hooks_no_prefetch"] / best
+    print(json.dumps(line), file=sys.stderr, flush=True)
+    rt.close()
+    cr.cudaFree(buf)
+
+
 def f4_lines():
     """the paper's hook-overhead microbenchmark shape (PAPER.md:466-471,
     530): c = a + b over 2^28 floats with the counter policy inlined as a hook on both loads
@@ -736,11 +792,26 @@ def f3_lines():
         cost, home = sched.workload(kind, W)
         budget = int(cost.sum() / W * 0.2)
         line = {"f3": kind, "workers": W, "units": len(cost), "work_us": int(cost.sum())}
-        for policy in ("fixed", "greedy", "latency_budget"):
+        for policy in ("fixed", "greedy", "latency_budget", "max_steals"):
             rt = gx.Runtime(0)
-            prog, fds = sched.setup(rt, policy, W, budget_us=budget)
+            prog, fds = sched.setup(rt, policy, W, budget_us=budget, max_steals=2)
             r = gx.gx_sched_run(rt.rt, prog, cost, home, W, 2)
             line[policy] = {"makespan_us": r["makespan_ns"] / 1e3, "steals": int(r["steals"].sum())}
+            rt.close()
+        print(json.dumps(line), file=sys.stderr, flush=True)
+    # CLC mode ("MaxSteals (CLC)"): one block per unit, one block resident per SM
+    # (200 KiB of shared memory each); a stealing block cancels pending blocks instead of exiting
+    U = 8 * W
+    for kind, cost in (("equal", np.full(U, 20, dtype=np.uint32)),
+                       ("heavy", sched.workload("heavy", W)[0])):
+        line = {"f3": "clc_" + kind, "units": len(cost), "work_us": int(cost.sum())}
+        for policy, cap in (("fixed", 0), ("max_steals", 1), ("max_steals", 4), ("greedy", 0)):
+            rt = gx.Runtime(0)
+            prog, fds = sched.setup(rt, policy, len(cost), max_steals=cap)
+            r = gx.gx_sched_run_ex(rt.rt, prog, cost, None, 0, 0, flags=gx.GX_SCHED_CLC, smem_per_block=200 * 1024)
+            name = policy if policy != "max_steals" else f"max_steals_{cap}"
+            line[name] = {"makespan_us": r["makespan_ns"] / 1e3, "steals": int(r["steals"].sum()),
+                          "blocks_started": int((r["end_ns"] > 0).sum())}
             rt.close()
         print(json.dumps(line), file=sys.stderr, flush=True)
 

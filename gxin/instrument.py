@@ -43,3 +43,52 @@ PI = """
     and64 r0, 7
     exit
 """
+
+# P7: GPU L2 stride prefetch (PAPER.md:342, Table 1 "GPU L2 Stride Prefetch ... Device"): on an access
+# at addr, prefetch [addr + dist, addr + dist + len) into L2 (gdev_prefetch_l2, helper 1001) with
+# dist and len from cfg (the host side of the policy sets the stride distance); R0 = the helper's
+# result; outcome[0 | 1 | 2] counts issued / -EINVAL / -EFAULT
+P7_L2_STRIDE = """
+    ldxdw r6, [r1+0]          ; addr
+    stw [r10-4], 0
+    lddw r1, map:cfg
+    mov64 r2, r10
+    add64 r2, -4
+    call 1
+    jeq r0, 0, out
+    ldxdw r7, [r0+0]          ; dist
+    ldxdw r3, [r0+8]          ; len
+    mov64 r2, r6
+    add64 r2, r7
+    lddw r1, map:region
+    call 1001
+    mov64 r9, r0
+    mov64 r2, 0
+    jeq r9, 0, count
+    mov64 r2, 1
+    jeq r9, -22, count
+    mov64 r2, 2
+count:
+    stxw [r10-8], r2
+    lddw r1, map:outcome
+    mov64 r2, r10
+    add64 r2, -8
+    call 1
+    jeq r0, 0, +2
+    mov64 r1, 1
+    atomic_add64 [r0+0], r1
+    mov64 r0, r9
+    exit
+out:
+    mov64 r0, 0
+    exit
+"""
+
+
+def setup_l2(engine, region_fd, dist, length):
+    """Maps of P7 on `engine` (oracle or runtime) around an existing region map: cfg {dist, len},
+    outcome[3].  Returns the asm symbol table."""
+    ARRAY = 2
+    cfg = engine.create_map(ARRAY, 4, 16, 1)
+    engine.update_map(cfg, (0).to_bytes(4, "little"), int(dist).to_bytes(8, "little") + int(length).to_bytes(8, "little"))
+    return {"region": region_fd, "cfg": cfg, "outcome": engine.create_map(ARRAY, 4, 8, 3)}

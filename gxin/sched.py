@@ -1,5 +1,5 @@
 """f3 inputs (F-5): the thread-block scheduling policies of PAPER.md §6.2.1
-(FixedWork, Greedy, LatencyBudget) as eBPF on the ENTER / EXIT / STEAL hooks, and the seeded work-unit
+(FixedWork, Greedy, LatencyBudget, MaxSteals) as eBPF on the ENTER / EXIT / STEAL hooks, and the seeded work-unit
 sets (moderate imbalance; heavy tail clustered on 10 % of the workers, "10% of blocks
 perform 100--200x more work").  INPUT description only."""
 from __future__ import annotations
@@ -81,16 +81,47 @@ steal:
     exit
 """
 
-POLICIES = {"fixed": FIXED, "greedy": GREEDY, "latency_budget": LATENCY_BUDGET}
+# MaxSteals (PAPER.md:497 "MaxSteals (CLC)", Table 1): a worker may steal at most cfg[0] times;
+# steals[worker] counts its granted STEAL decisions (only that worker's hooks touch its slot)
+MAX_STEALS = _COUNT + """
+    jne r2, 5, none
+    stw [r10-12], 0
+    lddw r1, map:cfg
+    mov64 r2, r10
+    add64 r2, -12
+    call 1
+    jeq r0, 0, none
+    ldxdw r9, [r0+0]          ; the cap
+    stxw [r10-8], r7
+    lddw r1, map:steals
+    mov64 r2, r10
+    add64 r2, -8
+    call 1
+    jeq r0, 0, none
+    ldxdw r3, [r0+0]
+    jge r3, r9, none
+    add64 r3, 1
+    stxdw [r0+0], r3
+    mov64 r0, 1
+    exit
+none:
+    mov64 r0, 0
+    exit
+"""
+
+POLICIES = {"fixed": FIXED, "greedy": GREEDY, "latency_budget": LATENCY_BUDGET, "max_steals": MAX_STEALS}
+HOOK_PROBE, HOOK_RETPROBE = 6, 7
 
 
-def setup(engine, policy: str, n_workers: int, budget_us: int = 0):
-    """Creates the policy's maps on `engine` (oracle or runtime) and loads the program.
-    Returns (prog handle, {map name: fd})."""
+def setup(engine, policy: str, n_workers: int, budget_us: int = 0, max_steals: int = 0):
+    """Creates the policy's maps on `engine` (oracle or runtime) and loads the program.  cfg[0] =
+    budget_us (latency_budget) or max_steals (max_steals).  Returns (prog handle, {map name: fd})."""
     fds = {"kcount": engine.create_map(ARRAY, 4, 8, 8),
            "stolen_us": engine.create_map(ARRAY, 4, 8, max(1, n_workers)),
+           "steals": engine.create_map(ARRAY, 4, 8, max(1, n_workers)),
            "cfg": engine.create_map(ARRAY, 4, 8, 1)}
-    engine.update_map(fds["cfg"], (0).to_bytes(4, "little"), int(budget_us).to_bytes(8, "little"), 0)
+    cfg = max_steals if policy == "max_steals" else budget_us
+    engine.update_map(fds["cfg"], (0).to_bytes(4, "little"), int(cfg).to_bytes(8, "little"), 0)
     return engine.load_prog(assemble(POLICIES[policy], fds)), fds
 
 

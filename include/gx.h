@@ -24,6 +24,8 @@
  *     tensors) and must stay alive until the stream work completes (stream-ordered).
  *   - Maps are runtime-owned device memory, freed by gx_close.  Host map reads/writes are
  *     synchronous and ordered after all prior gx_run_batch calls on any stream of the runtime.
+ *   - Batches of one gx_rt run one after another in submission order, even when they are given
+ *     different streams (a stream change makes the new stream wait for the previous one).
  *   - One gx_rt per CUDA device.  A gx_rt is not thread-safe.
  *
  * Event record (the ctx every program sees in r1; read-only; 32 B, 32-B aligned):
@@ -48,7 +50,10 @@ typedef struct gx_rt gx_rt;
 enum { GX_MAP_HASH = 1, GX_MAP_ARRAY = 2, GX_MAP_PERTHREAD_ARRAY = 6, GX_MAP_RINGBUF = 27,
        /* device->host prefetch request queue (F-2): key_size = value_size
         * = 0, max_entries = capacity in requests (a power of two in [64, 2^24]) */
-       GX_MAP_PREFETCH_QUEUE = 64 };
+       GX_MAP_PREFETCH_QUEUE = 64,
+       /* device region (F-7): caller-owned device memory [base, base + len) that
+        * gdev_prefetch_l2 may prefetch; made by gx_region_map, never by gx_create_map */
+       GX_MAP_REGION = 65 };
 /* Device helper ids beyond Linux's: gdev_mem_prefetch (§4.3.1 listing
  * "Request prefetch, triggers handler in host driver"), called as
  *     r0 = gdev_mem_prefetch(r1 = prefetch-queue map, r2 = addr, r3 = len)
@@ -58,6 +63,13 @@ enum { GX_MAP_HASH = 1, GX_MAP_ARRAY = 2, GX_MAP_PERTHREAD_ARRAY = 6, GX_MAP_RIN
  * Prefetching is idempotent: the queue's content is a SET, and the device merges identical
  * requests of one warp group (PAPER.md:286 warp-level aggregation). */
 enum { GX_FN_MEM_PREFETCH = 1000 };
+/* gdev_prefetch_l2 ("Device-side L2 prefetch instructions (prefetch.global.L2)",
+ * Table 1 "GPU L2 Stride Prefetch ... Device"), called as
+ *     r0 = gdev_prefetch_l2(r1 = region map, r2 = addr, r3 = len)
+ * issues one prefetch.global.L2 per 128-B line of [addr, addr + len) and returns 0, or -EINVAL
+ * (-22) if len == 0 or len > 64 KiB, or -EFAULT (-14) if the range is not inside the region (no
+ * prefetch is issued then).  A hint: no map or event state changes. */
+enum { GX_FN_PREFETCH_L2 = 1001 };
 /* hook kinds (event hook word bits 0-7): PAPER.md:225-230 (gdev_mem_ops.access), 260-262
  * (gdev_sched_ops.enter), 303 (fault-style records) */
 enum { GX_HOOK_MEM_ACCESS = 0, GX_HOOK_BLOCK_ENTER = 1, GX_HOOK_FAULT = 2 };
@@ -127,6 +139,11 @@ const char *gx_last_error(gx_rt *rt);                   /* text of the last fail
 /* ---------------------------------------------------------------- maps */
 /* Creates a zero-initialised map in device memory; *map_fd = its handle. */
 int  gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd);
+/* Registers caller-owned device memory [dev_ptr, dev_ptr + len) (len > 0; it must outlive the map
+ * and every launch that uses it) as a GX_MAP_REGION map for gdev_prefetch_l2.  A region has no
+ * content: gx_update_map / gx_read_map return -EINVAL and merges skip it.  -EINVAL if dev_ptr is
+ * NULL, len is 0 or dev_ptr + len wraps. */
+int  gx_region_map(gx_rt *rt, const void *dev_ptr, uint64_t len, int *map_fd);
 /* Host control-plane write of n (key, value) pairs, packed back to back (key_size / value_size
  * bytes each, host memory), with bpf_map_update_elem semantics (bpf.h:1762-1776).  PERTHREAD:
  * writes shard 0 and zeroes the other shards.  Synchronous.  Returns 0 or the first -errno. */
@@ -154,6 +171,10 @@ int  gx_prefetch_drain(gx_rt *rt, int map_fd, uint64_t *reqs, uint64_t cap, uint
  * together with user_src (CUDA C++ with extern "C" __global__ kernels) in one NVRTC sm_100a module:
  *     uint64_t gx_hook_access(unsigned group, const void *addr, uint32_t size, bool is_write);
  *     uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost);
+ *     uint64_t gx_hook_probe(unsigned group, uint64_t fn);                     (kind GX_HOOK_PROBE)
+ *     uint64_t gx_hook_retprobe(unsigned group, uint64_t fn, uint32_t retval);  (kind GX_HOOK_RETPROBE)
+ *     uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size,
+ *                            uint32_t *rec = nullptr);  (any kind; rec receives the 8-word record)
  * Each call runs the program once per lane of `group` on an event record built in registers
  * (addr, globaltimer ts, hook word, linear block id, %smid, hardware warp slot, lane, size) and
  * returns that lane's R0 (the policy decision).  `group` must be exactly the set of lanes making the
@@ -182,10 +203,32 @@ void gx_kernel_free(gx_rt *rt, gx_kernel *k);
  * worker, size = cost_us.  prog_fd (verified) is compiled into the worker kernel (gx_instrument).
  * Outputs (host arrays): executed_by[n_units] (worker), stolen[n_units], busy_ns / end_ns (from
  * the first worker's start) / steals [n_workers], *makespan_ns (device globaltimer).  Synchronous. */
-enum { GX_HOOK_BLOCK_EXIT = 4, GX_HOOK_STEAL = 5 };
+enum { GX_HOOK_BLOCK_EXIT = 4, GX_HOOK_STEAL = 5, GX_HOOK_PROBE = 6, GX_HOOK_RETPROBE = 7 };
 int  gx_sched_run(gx_rt *rt, int prog_fd, uint32_t n_units, const uint32_t *cost_us, const uint32_t *home,
                   uint32_t n_workers, uint32_t steal_cost_us, uint32_t *executed_by, uint8_t *stolen,
                   uint64_t *busy_ns, uint64_t *end_ns, uint32_t *steals, uint64_t *makespan_ns);
+/* gx_sched_run with modes and a hook log (F-6).
+ * flags: GX_SCHED_CLC -- no deques: the grid has one block per unit (unit u = block u; home must be
+ *   NULL, n_workers is ignored and every per-worker array has n_units entries).  After its unit a
+ *   block runs the STEAL hook; R0 != 0 cancels a not-yet-launched block with Blackwell cluster launch
+ *   control (clusterlaunchcontrol.try_cancel) and runs that block's unit with the stolen bit (the
+ *   paper's "MaxSteals (CLC)" row); R0 == 0 or a failed cancel ends the block.  A
+ *   cancelled block never starts (its end_ns is 0).
+ *   GX_SCHED_PROBES -- the unit body is bracketed by PROBE (addr = 1, size = 0) and RETPROBE (addr = 1,
+ *   size = unit) hooks: device function 1 starts / returns (gdev_sched_ops.probe/.retprobe,
+ *   PAPER.md:265-267).
+ * smem_per_block: dynamic shared memory per block (bytes; limits residency so that blocks stay
+ *   pending for CLC to cancel).
+ * log (host, log_cap entries, may be NULL with log_cap 0): every hook call in completion order --
+ *   the 32-B record the program ran on, its R0, the worker (block) and the worker's hook sequence
+ *   number 0, 1, ...; *log_n = hooks that ran.  -ENOSPC (after all outputs are written) when
+ *   *log_n > log_cap (the first log_cap completed calls are kept). */
+enum { GX_SCHED_CLC = 1, GX_SCHED_PROBES = 2 };
+typedef struct { uint8_t rec[32]; uint64_t r0; uint32_t worker, seq; } gx_hook_log;
+int  gx_sched_run_ex(gx_rt *rt, int prog_fd, uint32_t flags, uint32_t n_units, const uint32_t *cost_us,
+                     const uint32_t *home, uint32_t n_workers, uint32_t steal_cost_us, uint32_t smem_per_block,
+                     uint32_t *executed_by, uint8_t *stolen, uint64_t *busy_ns, uint64_t *end_ns, uint32_t *steals,
+                     uint64_t *makespan_ns, gx_hook_log *log, uint64_t log_cap, uint64_t *log_n);
 
 /* ---------------------------------------------------------------- runtime daemon (§8f f2)
  * "A runtime daemon asynchronously flushes GPU-local shards to host-visible canonical map

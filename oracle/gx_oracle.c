@@ -37,11 +37,14 @@
 
 /* ---- constants from bpf.h / bpf_common.h (restated, not included) ---- */
 enum { CL_LD = 0, CL_LDX = 1, CL_ST = 2, CL_STX = 3, CL_ALU = 4, CL_JMP = 5, CL_JMP32 = 6, CL_ALU64 = 7 };
-enum { MAP_HASH = 1, MAP_ARRAY = 2, MAP_PT = 6, MAP_RINGBUF = 27, MAP_PFQ = 64 };
+enum { MAP_HASH = 1, MAP_ARRAY = 2, MAP_PT = 6, MAP_RINGBUF = 27, MAP_PFQ = 64, MAP_REGION = 65 };
 /* gdev_mem_prefetch (§4.3.1 listing "Request prefetch, triggers handler in host
  * driver"), this build's helper id (reading F-1) */
 enum { FN_MEM_PREFETCH = 1000 };
-enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_NOMEM = 12, E_EXIST = 17, E_INVAL = 22 };
+/* gdev_prefetch_l2 ("Device-side L2 prefetch instructions (prefetch.global.L2)"),
+ * this build's helper id (reading F-7) */
+enum { FN_PREFETCH_L2 = 1001 };
+enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_NOMEM = 12, E_FAULT = 14, E_EXIST = 17, E_INVAL = 22 };
 #define STACK_SIZE 512
 #define POISON 0xDEADBEEFDEADBEEFull
 #define MAX_MAPS 64
@@ -81,6 +84,8 @@ typedef struct {
     /* PREFETCH QUEUE (F-2): requests {u64 first_page, u32 npages, u32 0} in call order */
     uint64_t *pfq;          /* 2 words per request */
     uint64_t pfq_n;
+    /* REGION (F-7): the device byte range [region_base, region_base + region_len) */
+    uint64_t region_base, region_len;
 } map_t;
 
 typedef struct {
@@ -301,12 +306,39 @@ static int map_update(ora_env *e, map_t *m, const uint8_t *key, const uint8_t *v
     return -E_INVAL;
 }
 
+/* gx_region_map: a device range for gdev_prefetch_l2 (F-7).  Returns the fd or -errno. */
+ORA_EXPORT int ora_region_map(ora_env *e, uint64_t base, uint64_t len) {
+    if (base == 0 || len == 0 || base + len < base) return -E_INVAL;
+    int fd = -1;
+    for (int i = 0; i < MAX_MAPS; i++) if (!e->maps[i].used) { fd = i; break; }
+    if (fd < 0) return -E_NOMEM;
+    map_t *m = &e->maps[fd];
+    memset(m, 0, sizeof *m);
+    m->type = MAP_REGION;
+    m->max_entries = 1;
+    m->region_base = base;
+    m->region_len = len;
+    m->used = 1;
+    return fd;
+}
+
+/* gdev_prefetch_l2(region, addr, len) (F-7).  The prefetch itself is a hint
+ * with no observable effect; the result is the only output: -EINVAL unless 1 <= len <= 64 KiB,
+ * else -EFAULT unless region_base <= addr and addr + len <= region_base + region_len (in exact
+ * 128-bit arithmetic), else 0. */
+static int64_t prefetch_l2(const map_t *m, uint64_t addr, uint64_t len) {
+    if (len == 0 || len > 65536) return -E_INVAL;
+    if (addr < m->region_base) return -E_FAULT;
+    if ((unsigned __int128)addr + len > (unsigned __int128)m->region_base + m->region_len) return -E_FAULT;
+    return 0;
+}
+
 /* Host control-plane write (SURVEY.md §8b gx_update_map): per-thread maps write shard 0 and
  * zero the other shards (§8c S4). */
 ORA_EXPORT int ora_map_update(ora_env *e, int fd, const void *key, const void *val, uint64_t flags) {
     if (fd < 0 || fd >= MAX_MAPS || !e->maps[fd].used) return -E_INVAL;
     map_t *m = &e->maps[fd];
-    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return -E_INVAL;
+    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ || m->type == MAP_REGION) return -E_INVAL;
     int r = map_update(e, m, key, val, flags, 0);
     if (r == 0 && m->type == MAP_PT) {
         uint32_t k;
@@ -660,12 +692,13 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                 if (!is64 || src != 0) return fault(env, ev, pc, "bpf-to-bpf / kfunc calls unsupported");
                 reg_t *R1 = &vm->r[1], *R2 = &vm->r[2], *R3 = &vm->r[3], *R4 = &vm->r[4];
                 int64_t ret;
-                if (imm == 1 || imm == 2 || imm == 130 || imm == FN_MEM_PREFETCH) {
+                if (imm == 1 || imm == 2 || imm == 130 || imm == FN_MEM_PREFETCH || imm == FN_PREFETCH_L2) {
                     if (R1->tag != T_MAPH) return fault(env, ev, pc, "helper r1 is not a map handle");
                 }
                 if (imm == 1) {
                     map_t *m = &env->maps[R1->map];
-                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return fault(env, ev, pc, "lookup on ringbuf / prefetch queue");
+                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ || m->type == MAP_REGION)
+                        return fault(env, ev, pc, "lookup on ringbuf / prefetch queue / region");
                     const uint8_t *key = arg_bytes(vm, R2, m->key_size, pc);
                     if (!key) return -1;
                     uint8_t *v = map_lookup(m, key, vm->shard);
@@ -676,7 +709,8 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                     continue;
                 } else if (imm == 2) {
                     map_t *m = &env->maps[R1->map];
-                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ) return fault(env, ev, pc, "update on ringbuf / prefetch queue");
+                    if (m->type == MAP_RINGBUF || m->type == MAP_PFQ || m->type == MAP_REGION)
+                        return fault(env, ev, pc, "update on ringbuf / prefetch queue / region");
                     const uint8_t *key = arg_bytes(vm, R2, m->key_size, pc);
                     if (!key) return -1;
                     const uint8_t *val = arg_bytes(vm, R3, m->value_size, pc);
@@ -699,6 +733,11 @@ static int run_one(ora_env *env, prog_t *p, const uint8_t *ctx, uint64_t ev, uin
                     if (m->type != MAP_PFQ) return fault(env, ev, pc, "mem_prefetch on a non-prefetch-queue map");
                     if (!scalar(R2) || !scalar(R3)) return fault(env, ev, pc, "prefetch addr/len not scalar");
                     ret = mem_prefetch(env, m, R2->v, R3->v);
+                } else if (imm == FN_PREFETCH_L2) {
+                    map_t *m = &env->maps[R1->map];
+                    if (m->type != MAP_REGION) return fault(env, ev, pc, "prefetch_l2 on a non-region map");
+                    if (!scalar(R2) || !scalar(R3)) return fault(env, ev, pc, "prefetch addr/len not scalar");
+                    ret = prefetch_l2(m, R2->v, R3->v);
                 } else {
                     return fault(env, ev, pc, "unknown or forbidden helper");
                 }

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 SRC_PATH = os.path.join(_HERE, "gx_oracle.c")
 
-HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF, PREFETCH_QUEUE = 1, 2, 6, 27, 64
+HASH, ARRAY, PERTHREAD_ARRAY, RINGBUF, PREFETCH_QUEUE, REGION = 1, 2, 6, 27, 64, 65
 FN_MEM_PREFETCH = 1000   # gdev_mem_prefetch (F-1)
 STATS = ("events_run", "events_skipped", "ringbuf_drops", "hash_full", "helper_errors", "insns")
 
@@ -43,6 +43,7 @@ def lib():
         L.ora_stats.argtypes = [vp, p64]
         L.ora_reset_stats.argtypes = [vp]
         L.ora_map_create.argtypes = [vp, u32, u32, u32, u32]
+        L.ora_region_map.argtypes = [vp, u64, u64]
         L.ora_map_update.argtypes = [vp, i32, vp, vp, u64]
         L.ora_map_update_n.argtypes = [vp, i32, vp, vp, u64, u64]
         L.ora_prog_load.argtypes = [vp, vp, u32]
@@ -87,6 +88,14 @@ class Oracle:
         if fd < 0:
             raise OSError(-fd, "ora_map_create")
         self.specs[fd] = (type, key_size, value_size, max_entries)
+        return fd
+
+    def region_map(self, base: int, length: int) -> int:
+        """A device byte range [base, base + length) for gdev_prefetch_l2 (F-7)."""
+        fd = self.L.ora_region_map(self.h, base, length)
+        if fd < 0:
+            raise OSError(-fd, "ora_region_map")
+        self.specs[fd] = (REGION, 0, 0, 1)
         return fd
 
     def update_map(self, fd, key: bytes, val: bytes, flags=0) -> int:

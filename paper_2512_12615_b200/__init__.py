@@ -21,8 +21,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgx.so")
 
-GX_MAP_HASH, GX_MAP_ARRAY, GX_MAP_PERTHREAD_ARRAY, GX_MAP_RINGBUF, GX_MAP_PREFETCH_QUEUE = 1, 2, 6, 27, 64
-GX_FN_MEM_PREFETCH = 1000
+GX_MAP_HASH, GX_MAP_ARRAY, GX_MAP_PERTHREAD_ARRAY, GX_MAP_RINGBUF, GX_MAP_PREFETCH_QUEUE, GX_MAP_REGION = 1, 2, 6, 27, 64, 65
+GX_FN_MEM_PREFETCH, GX_FN_PREFETCH_L2 = 1000, 1001
 RULES = ("OK", "BAD_INSN", "BAD_REG", "BAD_JUMP", "FALLTHROUGH", "UNREACHABLE", "UNINIT_READ", "OOB_ACCESS",
          "NULL_DEREF", "MISALIGNED", "PTR_LEAK", "SHIFT_RANGE", "BAD_HELPER", "FORBIDDEN_SYNC", "UNBOUNDED_LOOP",
          "COMPLEXITY", "BUDGET", "UNIFORM_BRANCH", "UNIFORM_LOOP_BOUND", "UNIFORM_MAP_KEY", "NON_UNIFORM_ATOMIC",
@@ -32,8 +32,8 @@ EXPORTS = ("gx_open", "gx_close", "gx_last_error", "gx_create_map", "gx_update_m
            "gx_get_stats", "gx_exec_info", "gx_set_engine", "gx_get_engine", "gx_merge_snapshot", "gx_merge_words", "gx_merge_export", "gx_merge_apply",
            "gx_hash_export", "gx_hash_apply", "gx_prefetch_drain", "gx_daemon_start", "gx_daemon_stop", "gx_daemon_watch",
            "gx_snapshot_read", "gx_daemon_get_stats", "gx_daemon_prefetch_range", "gx_instrument",
-           "gx_kernel_launch", "gx_kernel_free", "gx_sched_run", "gx_comm_unique_id", "gx_comm_init",
-           "gx_comm_init_host", "gx_merge", "gx_comm_free")
+           "gx_kernel_launch", "gx_kernel_free", "gx_sched_run", "gx_sched_run_ex", "gx_comm_unique_id", "gx_comm_init",
+           "gx_comm_init_host", "gx_merge", "gx_comm_free", "gx_region_map")
 
 
 class gx_map_spec(C.Structure):
@@ -110,7 +110,10 @@ def lib():
         "gx_kernel_free": (None, [vp, vp]),
         "gx_sched_run": (i32, [vp, i32, u32, C.POINTER(u32), C.POINTER(u32), u32, u32, C.POINTER(u32),
                                C.POINTER(C.c_uint8), p64, p64, C.POINTER(u32), p64]),
+        "gx_sched_run_ex": (i32, [vp, i32, u32, u32, C.POINTER(u32), C.POINTER(u32), u32, u32, u32, C.POINTER(u32),
+                                  C.POINTER(C.c_uint8), p64, p64, C.POINTER(u32), p64, vp, u64, p64]),
         "gx_load_prog": (i32, [vp, u32, vp, u32, C.POINTER(i32)]),
+        "gx_region_map": (i32, [vp, vp, u64, C.POINTER(i32)]),
         "gx_verify": (i32, [vp, i32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report), C.c_char_p, u64]),
         "gx_verify_offline": (i32, [vp, u32, vp, u32, C.POINTER(gx_verify_opts), C.POINTER(gx_verify_report),
                                     C.c_char_p, u64]),
@@ -182,6 +185,12 @@ def gx_create_map(rt, type, key_size, value_size, max_entries, flags=0) -> int:
     fd = C.c_int()
     spec = gx_map_spec(type, key_size, value_size, max_entries, flags)
     _check(lib().gx_create_map(rt, C.byref(spec), C.byref(fd)), "gx_create_map", rt)
+    return fd.value
+
+
+def gx_region_map(rt, base: int, length: int) -> int:
+    fd = C.c_int()
+    _check(lib().gx_region_map(rt, C.c_void_p(base), length, C.byref(fd)), "gx_region_map", rt)
     return fd.value
 
 
@@ -411,6 +420,37 @@ def gx_sched_run(rt, prog_fd, cost_us, home, n_workers, steal_cost_us=0) -> dict
     return dict(executed_by=ex, stolen=st, busy_ns=busy, end_ns=end, steals=steals, makespan_ns=ms.value)
 
 
+GX_SCHED_CLC, GX_SCHED_PROBES = 1, 2
+# gx_hook_log (include/gx.h): the 32-B record, R0, worker, the worker's hook sequence number
+HOOK_LOG = np.dtype([("rec", np.uint8, 32), ("r0", np.uint64), ("worker", np.uint32), ("seq", np.uint32)])
+
+
+def gx_sched_run_ex(rt, prog_fd, cost_us, home=None, n_workers=0, steal_cost_us=0, flags=0, smem_per_block=0,
+                    log_cap=0) -> dict:
+    """f3: gx_sched_run with modes (GX_SCHED_CLC: one block per unit, steals by cluster launch
+    control; GX_SCHED_PROBES) and a hook log (include/gx.h).  Returns gx_sched_run's dict plus
+    'log' (HOOK_LOG records, completion order) and 'log_n'."""
+    cost = np.ascontiguousarray(cost_us, dtype=np.uint32)
+    U = len(cost)
+    hm = None if home is None else np.ascontiguousarray(home, dtype=np.uint32)
+    W = U if flags & GX_SCHED_CLC else n_workers
+    ex = np.zeros(U, dtype=np.uint32)
+    st = np.zeros(U, dtype=np.uint8)
+    busy = np.zeros(W, dtype=np.uint64)
+    end = np.zeros(W, dtype=np.uint64)
+    steals = np.zeros(W, dtype=np.uint32)
+    log = np.zeros(log_cap, dtype=HOOK_LOG)
+    ms, ln = C.c_uint64(), C.c_uint64()
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+    _check(lib().gx_sched_run_ex(rt, prog_fd, flags, U, P(cost, C.c_uint32),
+                                 None if hm is None else P(hm, C.c_uint32), n_workers, steal_cost_us, smem_per_block,
+                                 P(ex, C.c_uint32), P(st, C.c_uint8), P(busy, C.c_uint64), P(end, C.c_uint64),
+                                 P(steals, C.c_uint32), C.byref(ms), log.ctypes.data if log_cap else None, log_cap,
+                                 C.byref(ln)), "gx_sched_run_ex", rt)
+    return dict(executed_by=ex, stolen=st, busy_ns=busy, end_ns=end, steals=steals, makespan_ns=ms.value,
+                log=log[:min(ln.value, log_cap)], log_n=ln.value)
+
+
 def gx_kernel_free(rt, handle):
     lib().gx_kernel_free(rt, handle)
 
@@ -556,6 +596,12 @@ class Runtime:
     def create_map(self, type, key_size, value_size, max_entries) -> int:
         fd = gx_create_map(self.rt, type, key_size, value_size, max_entries)
         self.specs[fd] = (type, key_size, value_size, max_entries)
+        return fd
+
+    def region_map(self, base: int, length: int) -> int:
+        """gx_region_map: caller-owned device memory [base, base + length) for gdev_prefetch_l2."""
+        fd = gx_region_map(self.rt, base, length)
+        self.specs[fd] = (GX_MAP_REGION, 0, 0, 1)
         return fd
 
     def update_map(self, fd, key: bytes, val: bytes, flags=0) -> int:

@@ -11,7 +11,7 @@
 
 namespace gxd {
 
-enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_EXIST = 17, E_INVAL = 22 };
+enum { E_NOENT = 2, E_2BIG = 7, E_AGAIN = 11, E_FAULT = 14, E_EXIST = 17, E_INVAL = 22 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 30;
@@ -422,6 +422,20 @@ __device__ __forceinline__ int64_t pfq_request_coop(const GxMapDesc &md, uint64_
         drops++;
         return -(int64_t)E_AGAIN;
     }
+    return 0;
+}
+
+/* gdev_prefetch_l2(region, addr, len) (F-7; "Device-side L2 prefetch
+ * instructions (prefetch.global.L2)", Table 1 "GPU L2 Stride Prefetch"): per lane, one
+ * prefetch.global.L2 per 128-B line of [addr, addr + len) when the range lies inside the REGION map
+ * [md.data, md.data + md.aux) (caller-owned device memory registered with gx_region_map).  R0: 0,
+ * -EINVAL (len 0 or > 64 KiB), -EFAULT (not inside the region).  A hint: no state changes. */
+__device__ __forceinline__ int64_t l2_prefetch(const GxMapDesc &md, uint64_t addr, uint64_t len) {
+    if (len == 0 || len > 65536) return -(int64_t)E_INVAL;
+    const uint64_t off = addr - md.data;
+    if (addr < md.data || off > md.aux || len > md.aux - off) return -(int64_t)E_FAULT;
+    const uint64_t end = addr + len;
+    for (uint64_t a = addr & ~127ull; a < end; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
     return 0;
 }
 

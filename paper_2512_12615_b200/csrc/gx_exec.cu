@@ -707,6 +707,15 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     break;
                 }
 
+                case GX_CALL_PREFETCH_L2: {
+                    if (me) {
+                        const int64_t rc = gxd::l2_prefetch(M[in.aux], R[2 * 32 + lane], R[3 * 32 + lane]);
+                        if (rc) c_herr++;
+                        R[lane] = (uint64_t)rc;
+                    }
+                    break;
+                }
+
                 case GX_CALL_MEM_PREFETCH: {
                     const int64_t rc = gxd::pfq_request_coop(M[in.aux], R[2 * 32 + lane], R[3 * 32 + lane], me, GX_FULL, c_drop);
                     if (me) {

@@ -17,6 +17,8 @@
 #define GX_NREGS 11
 #define GX_FN_MEM_PREFETCH 1000   /* gdev_mem_prefetch helper id (F-1) */
 #define GX_MAP_TYPE_PFQ 64        /* prefetch queue map type (F-2) */
+#define GX_FN_PREFETCH_L2 1001    /* gdev_prefetch_l2 helper id (F-7) */
+#define GX_MAP_TYPE_REGION 65     /* device region map: caller-owned device memory (F-7) */
 /* request filter after a queue's records (F-2 set semantics): clamp(capacity, 2^12, 2^20) words,
  * the count carried in GxMapDesc.nshards / GxPublishItem.nshards */
 #define GX_PFQ_FILTER_WORDS(cap) ((cap) < 4096u ? 4096u : (cap) > (1u << 20) ? (1u << 20) : (cap))
@@ -79,15 +81,16 @@ enum GxOp : uint8_t {
     GX_CALL_UPDATE_ARRAY, GX_CALL_UPDATE_PT, GX_CALL_UPDATE_HASH,
     GX_CALL_RINGBUF_OUTPUT,
     GX_CALL_MEM_PREFETCH,         /* gdev_mem_prefetch(queue = aux, addr = r2, len = r3) (f2) */
+    GX_CALL_PREFETCH_L2,          /* gdev_prefetch_l2(region = aux, addr = r2, len = r3) (f2) */
     GX_OP_COUNT
 };
 
 /* ---- device-side map descriptor ---- */
 struct GxMapDesc {
     uint64_t data;         /* ARRAY: values; PT: shards [word][shard]; HASH: slots (cap+1) x 16 B;
-                              RINGBUF: bytes; PREFETCH QUEUE: 16-B requests */
+                              RINGBUF: bytes; PREFETCH QUEUE: 16-B requests; REGION: base */
     uint64_t aux;          /* HASH: u64 counters {count}; RINGBUF: u64 {prod, used};
-                              PREFETCH QUEUE: u64 {reserved} */
+                              PREFETCH QUEUE: u64 {reserved}; REGION: byte length */
     uint32_t type, key_size, value_size, max_entries;
     uint32_t nshards;      /* PT: shards; PREFETCH QUEUE: request-filter words (a power of two) */
     uint32_t cap_mask;     /* HASH: capacity-1; RINGBUF: capacity-1; PREFETCH QUEUE: capacity-1 */

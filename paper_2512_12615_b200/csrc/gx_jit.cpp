@@ -532,6 +532,9 @@ struct Gen {
             st("  if (rc) c_herr++; if (rc == -7) c_hfull++; r0 = (uint64_t)rc; }");
             break;
         }
+        case GX_CALL_PREFETCH_L2:
+            st("{ const int64_t rc_ = gxd::l2_prefetch(" + md(g.aux) + ", r2, r3); r0 = (uint64_t)rc_; if (rc_) c_herr++; }");
+            break;
         case GX_CALL_MEM_PREFETCH:
             st("{ const int64_t rc_ = gxd::pfq_request_coop(" + md(g.aux) + ", r2, r3, true, " + M() +
                ", c_drop); r0 = (uint64_t)rc_; if (rc_) c_herr++; }");
@@ -731,7 +734,9 @@ struct Gen {
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         program(0, image, n);
-        o << "__device__ __forceinline__ uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size) {\n"
+        o << "/* rec (optional): receives the 32-B event record the program ran on (hook logs) */\n"
+             "__device__ __forceinline__ uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size,\n"
+             "                                                  uint32_t *rec = nullptr) {\n"
              "  uint32_t smid, wslot;\n"
              "  asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid));\n"
              "  asm volatile(\"mov.u32 %0, %%warpid;\" : \"=r\"(wslot));\n"
@@ -742,6 +747,7 @@ struct Gen {
              "  Ctx c;\n"
              "  c.w[0] = (uint32_t)addr; c.w[1] = (uint32_t)(addr >> 32); c.w[2] = (uint32_t)ts; c.w[3] = (uint32_t)(ts >> 32);\n"
              "  c.w[4] = hook; c.w[5] = blk; c.w[6] = (smid & 0xFFFF) | ((wslot & 63) << 16) | (lane << 24); c.w[7] = size;\n"
+             "  if (rec) { for (int k = 0; k < 8; k++) rec[k] = c.w[k]; }\n"
              "  /* unique among resident threads; the shards are sized from %nsmid (gx_open), the modulo\n"
              "   * only keeps a device that reports more SM ids than that inside the map */\n"
              "  const uint32_t shard = ((smid * 64 + (wslot & 63)) * 32 + lane) % " << pt_shards_min() << "u;\n"
@@ -765,6 +771,14 @@ struct Gen {
              "/* block-entry hook (gdev_sched_ops.enter, PAPER.md:260-262) */\n"
              "__device__ __forceinline__ uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost) {\n"
              "  return gx_hook_event(group, unit, 1u, cost);\n"
+             "}\n"
+             "/* device-function entry / return hooks (gdev_sched_ops.probe / .retprobe, PAPER.md:265-267):\n"
+             " * addr = the caller's function id, size = the low 32 bits of the return value (retprobe) */\n"
+             "__device__ __forceinline__ uint64_t gx_hook_probe(unsigned group, uint64_t fn) {\n"
+             "  return gx_hook_event(group, fn, 6u, 0u);\n"
+             "}\n"
+             "__device__ __forceinline__ uint64_t gx_hook_retprobe(unsigned group, uint64_t fn, uint32_t retval) {\n"
+             "  return gx_hook_event(group, fn, 7u, retval);\n"
              "}\n\n#line 1 \"user.cu\"\n"
           << user << "\n";
     }

@@ -223,6 +223,10 @@ struct gx_rt {
     cudaEvent_t ev_copied[2], ev_done[2];
     bool pipe_init = false;
     Daemon dmn;
+    /* batch order across streams (order_after_last) */
+    cudaEvent_t ev_order = nullptr;
+    cudaStream_t order_stream = nullptr;
+    bool order_valid = false;
     /* gx_comm_init / gx_merge */
     std::unique_ptr<GxComm> comm;
     MergeScratch ms;
@@ -262,6 +266,7 @@ GxMapDesc make_desc(const Map &m) {
     d.cap_mask = (uint32_t)(m.cap ? m.cap - 1 : 0);
     d.priv_off = 0xFFFFFFFFu;
     d.coherent = 0;
+    if (m.spec.type == GX_MAP_REGION) d.aux = m.data_bytes; /* [data, data + aux): caller-owned */
     return d;
 }
 
@@ -554,8 +559,24 @@ void daemon_main(gx_rt *rt) {
     }
 }
 
+/* Batches of one runtime run in submission order whatever streams they are given: per-thread
+ * shards are plain read-modify-writes keyed by the resident thread, and the privatised and
+ * hash-cache flushes assume one batch at a time.  Same-stream order is free; on a stream change the
+ * previous stream gets an event (recorded now: after everything already submitted to it, our last
+ * batch included) that the new stream waits on -- nothing is recorded while the stream stays. */
+int order_after_last(gx_rt *rt, cudaStream_t stream) {
+    if (rt->order_valid && rt->order_stream != stream) {
+        CK(cudaEventRecord(rt->ev_order, rt->order_stream), "order event");
+        CK(cudaStreamWaitEvent(stream, rt->ev_order, 0), "order wait");
+    }
+    rt->order_stream = stream;
+    rt->order_valid = true;
+    return 0;
+}
+
 int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream,
                uint32_t flags = 0) {
+    if (int rc = order_after_last(rt, stream)) return rc;
     if (rt->engine == GX_ENGINE_JIT) {
         if (!cfg.jv[0].tried && !cfg.jv[1].tried && !cfg.jv[2].tried && !cfg.jv[3].tried) {
             uint64_t worst = 0; /* ring_ok before the first compile (jit_prepare sets it too) */
@@ -639,6 +660,10 @@ int gx_open(int cuda_device, gx_rt **out) {
     if (e != cudaSuccess) return -EFAULT;
     gx_rt *rt = new gx_rt();
     rt->dev = cuda_device;
+    if (cudaEventCreateWithFlags(&rt->ev_order, cudaEventDisableTiming) != cudaSuccess) {
+        delete rt;
+        return -EFAULT;
+    }
     rt->nsm = prop.multiProcessorCount;
     /* one shard per resident thread slot (2048 / SM); f4 hooks key shards by (%smid, %warpid, lane),
      * and %smid ranges over [0, %nsmid), which may exceed the SM count */
@@ -665,7 +690,7 @@ void gx_close(gx_rt *rt) {
     gx_daemon_stop(rt);
     cudaDeviceSynchronize();
     for (auto &m : rt->maps) {
-        cudaFree(m.data);
+        if (m.spec.type != GX_MAP_REGION) cudaFree(m.data);   /* a region's memory is the caller's */
         cudaFree(m.aux);
         cudaFree(m.base);
         cudaFree(m.base_aux);
@@ -677,6 +702,7 @@ void gx_close(gx_rt *rt) {
             if (v.mod && drv().moduleUnload) drv().moduleUnload(v.mod);
     }
     cudaFree(rt->d_stats);
+    if (rt->ev_order) cudaEventDestroy(rt->ev_order);
     rt->comm.reset();
     cudaFree(rt->ms.d);
     if (rt->pipe_init) {
@@ -764,6 +790,29 @@ int gx_create_map(gx_rt *rt, const gx_map_spec *spec, int *map_fd) {
     return 0;
 }
 
+int gx_region_map(gx_rt *rt, const void *dev_ptr, uint64_t len, int *map_fd) {
+    if (!rt || !map_fd) return -EINVAL;
+    if (!dev_ptr || !len || (uint64_t)(uintptr_t)dev_ptr + len < (uint64_t)(uintptr_t)dev_ptr)
+        return set_err(rt, -EINVAL, "bad device region");
+    int fd = -1;
+    for (int i = 0; i < GX_MAX_MAPS; i++)
+        if (!rt->maps[i].valid) {
+            fd = i;
+            break;
+        }
+    if (fd < 0) return set_err(rt, -ENOMEM, "too many maps");
+    Map m;
+    m.spec.type = GX_MAP_REGION;
+    m.spec.max_entries = 1;
+    m.data = const_cast<void *>(dev_ptr);
+    m.data_bytes = len;
+    m.valid = true;
+    rt->maps[fd] = m;
+    rt->version++;
+    *map_fd = fd;
+    return 0;
+}
+
 int gx_update_map(gx_rt *rt, int fd, const void *keys, const void *vals, uint64_t n, uint64_t flags) {
     if (!check_map(rt, fd)) return -ENOENT;
     if (n == 0) return 0;
@@ -773,8 +822,8 @@ int gx_update_map(gx_rt *rt, int fd, const void *keys, const void *vals, uint64_
     int rc0 = sync(rt);
     if (rc0) return rc0;
     const uint8_t *kb = (const uint8_t *)keys, *vb = (const uint8_t *)vals;
-    if (s.type == GX_MAP_RINGBUF || s.type == GX_MAP_PREFETCH_QUEUE)
-        return set_err(rt, -EINVAL, "ring buffers and prefetch queues have no keys");
+    if (s.type == GX_MAP_RINGBUF || s.type == GX_MAP_PREFETCH_QUEUE || s.type == GX_MAP_REGION)
+        return set_err(rt, -EINVAL, "ring buffers, prefetch queues and regions have no keys");
     if (flags > 2) return -EINVAL;
     if (s.type == GX_MAP_ARRAY || s.type == GX_MAP_PERTHREAD_ARRAY) {
         int first = 0;
@@ -1308,6 +1357,8 @@ int gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t g
     CUfunction fn = nullptr;
     if (drv().moduleGetFunction(&fn, k->mod, name) != CUDA_SUCCESS)
         return set_err(rt, -ENOENT, "no kernel '%s' in the instrumented module", name);
+    if (smem > 48 * 1024 && drv().funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+        return set_err(rt, -EINVAL, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
     if (drv().launchKernel(fn, grid[0], grid[1], grid[2], block[0], block[1], block[2], smem, (CUstream)stream, args,
                            nullptr) != CUDA_SUCCESS)
         return set_err(rt, -EFAULT, "instrumented kernel launch failed");
@@ -1315,11 +1366,18 @@ int gx_kernel_launch(gx_rt *rt, gx_kernel *k, const char *name, const uint32_t g
     return 0;
 }
 
-/* f3: the work-stealing thread-block scheduler (§4.3.2, §6.2.1; F-5) as a
- * persistent kernel: one worker per block, lane 0 drives it and calls the policy through the
- * inline hooks (gx_instrument).  Deques are [head, tail) index pairs packed in one u64 per worker:
- * the owner pops the head, thieves pop the tail, each with one CAS. */
+/* f3: the thread-block scheduler of PAPER.md §4.3.2 / §6.2.1 (F-5, F-6) in two modes,
+ * both driven by lane 0 of each block calling the policy through the inline hooks (gx_instrument):
+ *  - DEQUE: persistent workers, one per block.  Deques are [head, tail) index pairs packed in one
+ *    u64 per worker: the owner pops the head, thieves pop the tail, each with one CAS.
+ *  - CLC: one block per unit (the plain grid), and "steal" is Blackwell cluster launch control
+ *    ("MaxSteals (CLC)"): after its unit, a block whose should_try_steal says yes
+ *    cancels a not-yet-launched block with clusterlaunchcontrol.try_cancel and runs that block's
+ *    unit itself; a failed cancel (no block left to launch) or R0 == 0 ends the block.
+ * Every hook call can be logged ({record, R0, worker, per-worker sequence number}) so that the
+ * policy's decisions can be replayed through the oracle worker by worker. */
 static const char *kSchedSrc = R"CUDA(
+struct GxHookLog { unsigned rec[8]; unsigned long long r0; unsigned worker, seq; };
 __device__ __forceinline__ unsigned long long gx_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1329,11 +1387,45 @@ __device__ __forceinline__ void gx_spin_ns(unsigned long long ns) {
     const unsigned long long a = gx_now();
     while (gx_now() - a < ns) { }
 }
+struct GxSchedCtx {
+    unsigned w, seq;
+    GxHookLog *log;
+    unsigned long long log_cap, *log_n;
+    __device__ __forceinline__ unsigned long long hook(unsigned long long addr, unsigned kind, unsigned size) {
+        unsigned rec[8];
+        const unsigned long long r = gx_hook_event(1u, addr, kind, size, log ? rec : nullptr);
+        if (log) {
+            const unsigned long long i = atomicAdd(log_n, 1ull);
+            if (i < log_cap) {
+                GxHookLog *e = &log[i];
+                for (int k = 0; k < 8; k++) e->rec[k] = rec[k];
+                e->r0 = r;
+                e->worker = w;
+                e->seq = seq;
+            }
+        }
+        seq++;
+        return r;
+    }
+    /* one work unit: ENTER, [PROBE], the unit's body (a globaltimer spin), [RETPROBE], EXIT */
+    __device__ __forceinline__ unsigned long long unit(unsigned u, unsigned st, unsigned cost_us, bool probes) {
+        hook(u, 1u | (st << 16), cost_us);
+        if (probes) hook(1ull, 6u, 0u);                 /* device function 1 = the unit body */
+        const unsigned long long a = gx_now();
+        gx_spin_ns(1000ull * cost_us);
+        const unsigned long long b = gx_now() - a;
+        if (probes) hook(1ull, 7u, u);                  /* its return value: the unit id */
+        hook(u, 4u | (st << 16), cost_us);
+        return b;
+    }
+};
 extern "C" __global__ void gx_sched_worker(const unsigned *seg, const unsigned *off, unsigned long long *ht, unsigned W,
-                                           const unsigned *cost_us, unsigned steal_cost_us, unsigned *executed_by,
-                                           unsigned char *stolen, unsigned long long *busy_ns, unsigned long long *start_ns,
-                                           unsigned long long *end_ns, unsigned *steals) {
+                                           const unsigned *cost_us, unsigned steal_cost_us, unsigned probes,
+                                           unsigned *executed_by, unsigned char *stolen, unsigned long long *busy_ns,
+                                           unsigned long long *start_ns, unsigned long long *end_ns, unsigned *steals,
+                                           GxHookLog *log, unsigned long long log_cap, unsigned long long *log_n) {
     if (threadIdx.x != 0) return;      /* lane 0 is the worker; hooks run for the group {lane 0} */
+    GxSchedCtx x{blockIdx.x, 0u, log, log_cap, log_n};
     const unsigned w = blockIdx.x;
     start_ns[w] = gx_now();
     unsigned long long busy = 0;
@@ -1352,7 +1444,7 @@ extern "C" __global__ void gx_sched_worker(const unsigned *seg, const unsigned *
             }
         }
         if (!got) {
-            if (gx_hook_event(1u, 0ull, 5u, 0u) == 0) break;      /* should_try_steal -> no */
+            if (x.hook(0ull, 5u, 0u) == 0) break;      /* should_try_steal -> no */
             for (;;) {                 /* victim: largest deque, lowest id; take its tail */
                 int v = -1;
                 unsigned best = 0;
@@ -1375,11 +1467,7 @@ extern "C" __global__ void gx_sched_worker(const unsigned *seg, const unsigned *
             st = 1;
             nst++;
         }
-        gx_hook_event(1u, (unsigned long long)u, 1u | (st << 16), cost_us[u]);
-        const unsigned long long a = gx_now();
-        gx_spin_ns(1000ull * cost_us[u]);
-        busy += gx_now() - a;
-        gx_hook_event(1u, (unsigned long long)u, 4u | (st << 16), cost_us[u]);
+        busy += x.unit(u, st, cost_us[u], probes != 0);
         executed_by[u] = w;
         stolen[u] = (unsigned char)st;
     }
@@ -1387,70 +1475,159 @@ extern "C" __global__ void gx_sched_worker(const unsigned *seg, const unsigned *
     steals[w] = nst;
     end_ns[w] = gx_now();
 }
+extern "C" __global__ void gx_sched_clc(const unsigned *cost_us, unsigned steal_cost_us, unsigned probes,
+                                        unsigned *executed_by, unsigned char *stolen, unsigned long long *busy_ns,
+                                        unsigned long long *start_ns, unsigned long long *end_ns, unsigned *steals,
+                                        GxHookLog *log, unsigned long long log_cap, unsigned long long *log_n) {
+    __shared__ __align__(16) unsigned long long resp[2];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x != 0) return;
+    const unsigned bar_a = (unsigned)__cvta_generic_to_shared(&bar);
+    const unsigned resp_a = (unsigned)__cvta_generic_to_shared(resp);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar_a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    GxSchedCtx x{blockIdx.x, 0u, log, log_cap, log_n};
+    const unsigned w = blockIdx.x;
+    start_ns[w] = gx_now();
+    unsigned long long busy = 0;
+    unsigned nst = 0, u = w, st = 0, phase = 0;
+    for (;;) {
+        busy += x.unit(u, st, cost_us[u], probes != 0);
+        executed_by[u] = w;
+        stolen[u] = (unsigned char)st;
+        if (x.hook(0ull, 5u, 0u) == 0) break;          /* should_try_steal -> no */
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16;" :: "r"(bar_a) : "memory");
+        asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+                     :: "r"(resp_a), "r"(bar_a) : "memory");
+        unsigned done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(bar_a), "r"(phase) : "memory");
+        phase ^= 1u;
+        unsigned ok = 0, cx = 0, cy, cz;
+        asm volatile("{ .reg .pred p; .reg .b128 r; ld.shared.b128 r, [%4];\n"
+                     "  clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n"
+                     "  selp.u32 %3, 1, 0, p;\n"
+                     "  @p clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, %1, %2, _}, r; }"
+                     : "=r"(cx), "=r"(cy), "=r"(cz), "=r"(ok) : "r"(resp_a) : "memory");
+        if (!ok) break;                /* nothing left to launch: a later try_cancel would be undefined */
+        u = cx;
+        st = 1;
+        nst++;
+        gx_spin_ns(1000ull * steal_cost_us);
+    }
+    busy_ns[w] = busy;
+    steals[w] = nst;
+    end_ns[w] = gx_now();
+}
 )CUDA";
+
+int gx_sched_run_ex(gx_rt *rt, int prog_fd, uint32_t flags, uint32_t n_units, const uint32_t *cost_us,
+                    const uint32_t *home, uint32_t n_workers, uint32_t steal_cost_us, uint32_t smem_per_block,
+                    uint32_t *executed_by, uint8_t *stolen, uint64_t *busy_ns, uint64_t *end_ns, uint32_t *steals,
+                    uint64_t *makespan_ns, gx_hook_log *log, uint64_t log_cap, uint64_t *log_n) {
+    if (!rt || !cost_us || !n_units || !executed_by || !stolen || !busy_ns || !end_ns || !steals || !makespan_ns)
+        return -EINVAL;
+    if (flags & ~(uint32_t)(GX_SCHED_CLC | GX_SCHED_PROBES)) return set_err(rt, -EINVAL, "unknown sched flags 0x%x", flags);
+    if ((log_cap && !log) || (log && !log_n)) return set_err(rt, -EINVAL, "hook log needs log and log_n");
+    const bool clc = flags & GX_SCHED_CLC;
+    if (clc) {
+        if (home) return set_err(rt, -EINVAL, "GX_SCHED_CLC: unit u is block u's (home must be NULL)");
+        n_workers = n_units;
+    } else {
+        if (!home || !n_workers) return -EINVAL;
+        for (uint32_t u = 0; u < n_units; u++)
+            if (home[u] >= n_workers) return set_err(rt, -EINVAL, "unit %u homed on worker %u >= %u", u, home[u], n_workers);
+    }
+    gx_kernel *k = nullptr;
+    int rc = gx_instrument(rt, prog_fd, kSchedSrc, &k, nullptr, 0);
+    if (rc) return rc;
+    const uint32_t W = n_workers;
+    std::vector<uint32_t> off(W + 1, 0), seg(n_units), fill(W, 0);
+    std::vector<unsigned long long> ht(W);
+    if (!clc) {
+        for (uint32_t u = 0; u < n_units; u++) off[home[u] + 1]++;
+        for (uint32_t w = 0; w < W; w++) off[w + 1] += off[w];
+        for (uint32_t u = 0; u < n_units; u++) seg[off[home[u]] + fill[home[u]]++] = u; /* deque in unit order */
+        for (uint32_t w = 0; w < W; w++) ht[w] = (unsigned long long)(off[w + 1] - off[w]) << 32;
+    }
+    uint32_t *d_seg, *d_off, *d_cost, *d_exec, *d_steals;
+    unsigned long long *d_ht, *d_busy, *d_start, *d_end, *d_logn;
+    uint8_t *d_stolen;
+    void *d_log = nullptr;
+    CK(cudaMalloc(&d_seg, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_off, 4ull * (W + 1)), "sched");
+    CK(cudaMalloc(&d_cost, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_exec, 4ull * n_units), "sched");
+    CK(cudaMalloc(&d_stolen, n_units), "sched");
+    CK(cudaMalloc(&d_steals, 4ull * W), "sched");
+    CK(cudaMalloc(&d_ht, 8ull * W), "sched");
+    CK(cudaMalloc(&d_busy, 8ull * W), "sched");
+    CK(cudaMalloc(&d_start, 8ull * W), "sched");
+    CK(cudaMalloc(&d_end, 8ull * W), "sched");
+    CK(cudaMalloc(&d_logn, 8), "sched");
+    if (log_cap) CK(cudaMalloc(&d_log, sizeof(gx_hook_log) * log_cap), "sched log");
+    CK(cudaMemcpy(d_seg, seg.data(), 4ull * n_units, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_off, off.data(), 4ull * (W + 1), cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_cost, cost_us, 4ull * n_units, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemcpy(d_ht, ht.data(), 8ull * W, cudaMemcpyHostToDevice), "sched");
+    CK(cudaMemset(d_exec, 0xFF, 4ull * n_units), "sched");
+    CK(cudaMemset(d_stolen, 0, n_units), "sched");
+    CK(cudaMemset(d_steals, 0, 4ull * W), "sched");
+    CK(cudaMemset(d_busy, 0, 8ull * W), "sched");
+    CK(cudaMemset(d_start, 0xFF, 8ull * W), "sched");   /* blocks cancelled by CLC never start */
+    CK(cudaMemset(d_end, 0, 8ull * W), "sched");
+    CK(cudaMemset(d_logn, 0, 8), "sched");
+    uint32_t probes = (flags & GX_SCHED_PROBES) ? 1u : 0u;
+    const uint32_t block[3] = {32, 1, 1};
+    if (clc) {
+        void *args[] = {&d_cost, &steal_cost_us, &probes, &d_exec, &d_stolen, &d_busy, &d_start, &d_end, &d_steals,
+                        &d_log, &log_cap, &d_logn};
+        const uint32_t grid[3] = {n_units, 1, 1};
+        rc = gx_kernel_launch(rt, k, "gx_sched_clc", grid, block, smem_per_block, args, nullptr);
+    } else {
+        void *args[] = {&d_seg, &d_off, &d_ht, (void *)&W, &d_cost, &steal_cost_us, &probes, &d_exec, &d_stolen, &d_busy,
+                        &d_start, &d_end, &d_steals, &d_log, &log_cap, &d_logn};
+        const uint32_t grid[3] = {W, 1, 1};
+        rc = gx_kernel_launch(rt, k, "gx_sched_worker", grid, block, smem_per_block, args, nullptr);
+    }
+    if (!rc) {
+        CK(cudaDeviceSynchronize(), "sched run");
+        std::vector<unsigned long long> st(W), en(W), bu(W);
+        unsigned long long ln = 0;
+        CK(cudaMemcpy(executed_by, d_exec, 4ull * n_units, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(stolen, d_stolen, n_units, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(steals, d_steals, 4ull * W, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(st.data(), d_start, 8ull * W, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(en.data(), d_end, 8ull * W, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(bu.data(), d_busy, 8ull * W, cudaMemcpyDeviceToHost), "sched");
+        CK(cudaMemcpy(&ln, d_logn, 8, cudaMemcpyDeviceToHost), "sched");
+        if (log_cap) CK(cudaMemcpy(log, d_log, sizeof(gx_hook_log) * std::min<uint64_t>(ln, log_cap), cudaMemcpyDeviceToHost), "sched");
+        if (log_n) *log_n = ln;
+        const unsigned long long t0 = *std::min_element(st.begin(), st.end());
+        unsigned long long t1 = 0;
+        for (uint32_t w = 0; w < W; w++) {
+            busy_ns[w] = bu[w];
+            end_ns[w] = en[w] ? en[w] - t0 : 0;              /* 0: a block cancelled before it started */
+            t1 = std::max(t1, en[w]);
+        }
+        *makespan_ns = t1 - t0;
+        if (log && ln > log_cap) rc = set_err(rt, -ENOSPC, "hook log: %llu hooks ran, %llu fit", ln, (unsigned long long)log_cap);
+    }
+    cudaFree(d_seg); cudaFree(d_off); cudaFree(d_cost); cudaFree(d_exec); cudaFree(d_stolen); cudaFree(d_steals);
+    cudaFree(d_ht); cudaFree(d_busy); cudaFree(d_start); cudaFree(d_end); cudaFree(d_logn);
+    if (d_log) cudaFree(d_log);
+    gx_kernel_free(rt, k);
+    return rc;
+}
 
 int gx_sched_run(gx_rt *rt, int prog_fd, uint32_t n_units, const uint32_t *cost_us, const uint32_t *home, uint32_t n_workers,
                  uint32_t steal_cost_us, uint32_t *executed_by, uint8_t *stolen, uint64_t *busy_ns, uint64_t *end_ns,
                  uint32_t *steals, uint64_t *makespan_ns) {
-    if (!rt || !cost_us || !home || !n_workers || !n_units || !executed_by || !stolen || !busy_ns || !end_ns || !steals ||
-        !makespan_ns)
-        return -EINVAL;
-    for (uint32_t u = 0; u < n_units; u++)
-        if (home[u] >= n_workers) return set_err(rt, -EINVAL, "unit %u homed on worker %u >= %u", u, home[u], n_workers);
-    gx_kernel *k = nullptr;
-    int rc = gx_instrument(rt, prog_fd, kSchedSrc, &k, nullptr, 0);
-    if (rc) return rc;
-    std::vector<uint32_t> off(n_workers + 1, 0), seg(n_units), fill(n_workers, 0);
-    for (uint32_t u = 0; u < n_units; u++) off[home[u] + 1]++;
-    for (uint32_t w = 0; w < n_workers; w++) off[w + 1] += off[w];
-    for (uint32_t u = 0; u < n_units; u++) seg[off[home[u]] + fill[home[u]]++] = u; /* deque in unit order */
-    std::vector<unsigned long long> ht(n_workers);
-    for (uint32_t w = 0; w < n_workers; w++) ht[w] = (unsigned long long)(off[w + 1] - off[w]) << 32;
-    uint32_t *d_seg, *d_off, *d_cost, *d_exec, *d_steals;
-    unsigned long long *d_ht, *d_busy, *d_start, *d_end;
-    uint8_t *d_stolen;
-    CK(cudaMalloc(&d_seg, 4ull * n_units), "sched");
-    CK(cudaMalloc(&d_off, 4ull * (n_workers + 1)), "sched");
-    CK(cudaMalloc(&d_cost, 4ull * n_units), "sched");
-    CK(cudaMalloc(&d_exec, 4ull * n_units), "sched");
-    CK(cudaMalloc(&d_stolen, n_units), "sched");
-    CK(cudaMalloc(&d_steals, 4ull * n_workers), "sched");
-    CK(cudaMalloc(&d_ht, 8ull * n_workers), "sched");
-    CK(cudaMalloc(&d_busy, 8ull * n_workers), "sched");
-    CK(cudaMalloc(&d_start, 8ull * n_workers), "sched");
-    CK(cudaMalloc(&d_end, 8ull * n_workers), "sched");
-    CK(cudaMemcpy(d_seg, seg.data(), 4ull * n_units, cudaMemcpyHostToDevice), "sched");
-    CK(cudaMemcpy(d_off, off.data(), 4ull * (n_workers + 1), cudaMemcpyHostToDevice), "sched");
-    CK(cudaMemcpy(d_cost, cost_us, 4ull * n_units, cudaMemcpyHostToDevice), "sched");
-    CK(cudaMemcpy(d_ht, ht.data(), 8ull * n_workers, cudaMemcpyHostToDevice), "sched");
-    CK(cudaMemset(d_exec, 0xFF, 4ull * n_units), "sched");
-    CK(cudaMemset(d_stolen, 0, n_units), "sched");
-    uint32_t W = n_workers;
-    void *args[] = {&d_seg, &d_off, &d_ht, &W, &d_cost, &steal_cost_us, &d_exec, &d_stolen, &d_busy, &d_start, &d_end, &d_steals};
-    const uint32_t grid[3] = {n_workers, 1, 1}, block[3] = {32, 1, 1};
-    rc = gx_kernel_launch(rt, k, "gx_sched_worker", grid, block, 0, args, nullptr);
-    if (!rc) {
-        CK(cudaDeviceSynchronize(), "sched run");
-        std::vector<unsigned long long> st(n_workers), en(n_workers), bu(n_workers);
-        CK(cudaMemcpy(executed_by, d_exec, 4ull * n_units, cudaMemcpyDeviceToHost), "sched");
-        CK(cudaMemcpy(stolen, d_stolen, n_units, cudaMemcpyDeviceToHost), "sched");
-        CK(cudaMemcpy(steals, d_steals, 4ull * n_workers, cudaMemcpyDeviceToHost), "sched");
-        CK(cudaMemcpy(st.data(), d_start, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
-        CK(cudaMemcpy(en.data(), d_end, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
-        CK(cudaMemcpy(bu.data(), d_busy, 8ull * n_workers, cudaMemcpyDeviceToHost), "sched");
-        const unsigned long long t0 = *std::min_element(st.begin(), st.end());
-        unsigned long long t1 = 0;
-        for (uint32_t w = 0; w < n_workers; w++) {
-            busy_ns[w] = bu[w];
-            end_ns[w] = en[w] - t0;
-            t1 = std::max(t1, en[w]);
-        }
-        *makespan_ns = t1 - t0;
-    }
-    cudaFree(d_seg); cudaFree(d_off); cudaFree(d_cost); cudaFree(d_exec); cudaFree(d_stolen); cudaFree(d_steals);
-    cudaFree(d_ht); cudaFree(d_busy); cudaFree(d_start); cudaFree(d_end);
-    gx_kernel_free(rt, k);
-    return rc;
+    if (!home) return -EINVAL;
+    return gx_sched_run_ex(rt, prog_fd, 0, n_units, cost_us, home, n_workers, steal_cost_us, 0, executed_by, stolen,
+                           busy_ns, end_ns, steals, makespan_ns, nullptr, 0, nullptr);
 }
 
 void gx_kernel_free(gx_rt *rt, gx_kernel *k) {
@@ -1547,7 +1724,7 @@ static int ensure_base(gx_rt *rt, Map &m, bool retake = false) {
 int gx_merge_snapshot(gx_rt *rt, int fd) {
     if (!check_map(rt, fd)) return -ENOENT;
     Map &m = rt->maps[fd];
-    if (m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) return -EINVAL;
+    if (m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE || m.spec.type == GX_MAP_REGION) return -EINVAL;
     return ensure_base(rt, m, true);
 }
 
@@ -1956,7 +2133,8 @@ int comm_attach(gx_rt *rt, std::unique_ptr<GxComm> c) {
     /* the agreed initial state: every mergeable map's base snapshot, now */
     for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
         Map &m = rt->maps[fd];
-        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) continue;
+        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE || m.spec.type == GX_MAP_REGION)
+            continue;
         int rc = ensure_base(rt, m, true);
         if (rc) return rc;
     }
@@ -2012,7 +2190,8 @@ int gx_merge(gx_rt *rt, void *cuda_stream) {
     /* legality first, on every map (a refusal leaves every map untouched) */
     for (int fd = 0; fd < GX_MAX_MAPS; fd++) {
         const Map &m = rt->maps[fd];
-        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE) continue;
+        if (!m.valid || m.spec.type == GX_MAP_RINGBUF || m.spec.type == GX_MAP_PREFETCH_QUEUE || m.spec.type == GX_MAP_REGION)
+            continue;
         if (const char *why = merge_illegal(rt, fd))
             return set_err(rt, -EINVAL, "map %d cannot be merged (S3): %s", fd, why);
     }

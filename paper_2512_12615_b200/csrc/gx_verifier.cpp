@@ -29,7 +29,7 @@ namespace {
 
 /* --------------------------------------------------------------------------- encoding */
 enum { CL_LD = 0, CL_LDX = 1, CL_ST = 2, CL_STX = 3, CL_ALU = 4, CL_JMP = 5, CL_JMP32 = 6, CL_ALU64 = 7 };
-enum { HASH = 1, ARRAY = 2, PT = 6, RINGBUF = 27, PFQ = GX_MAP_TYPE_PFQ };
+enum { HASH = 1, ARRAY = 2, PT = 6, RINGBUF = 27, PFQ = GX_MAP_TYPE_PFQ, REGION = GX_MAP_TYPE_REGION };
 
 struct Raw {
     uint8_t code, dst, src;
@@ -1420,7 +1420,7 @@ struct Verifier {
         int32_t id = ins[pc].imm;
         char msg[128];
         if (id == 93 || id == 94) return fail(pc, GX_FORBIDDEN_SYNC, "bpf_spin_lock/unlock: GPU-wide synchronisation is forbidden on device hooks");
-        if (id != 1 && id != 2 && id != 130 && id != GX_FN_MEM_PREFETCH) {
+        if (id != 1 && id != 2 && id != 130 && id != GX_FN_MEM_PREFETCH && id != GX_FN_PREFETCH_L2) {
             snprintf(msg, sizeof msg, "helper %d is not available to device programs", id);
             return fail(pc, GX_BAD_HELPER, msg);
         }
@@ -1434,8 +1434,8 @@ struct Verifier {
         GxMapUse &u = out.use[m];
         u.used = true;
         if (id == 1 || id == 2) {
-            if (mi.type == RINGBUF || mi.type == PFQ)
-                return fail(pc, GX_BAD_HELPER, "map lookup/update on a ring buffer / prefetch queue");
+            if (mi.type == RINGBUF || mi.type == PFQ || mi.type == REGION)
+                return fail(pc, GX_BAD_HELPER, "map lookup/update on a ring buffer / prefetch queue / region");
             if (!check_arg_mem(pc, st, st.r[2], mi.key_size, mi.key_size, "key", kk, ka)) return false;
             if (kk == MK_MAPV) out.use[st.r[2].map].reads = out.use[st.r[2].map].used = true;
             if (id == 2) {
@@ -1449,6 +1449,15 @@ struct Verifier {
             } else {
                 P.ch += 1;
             }
+        } else if (id == GX_FN_PREFETCH_L2) {
+            /* gdev_prefetch_l2(region, addr, len) (F-7): addr and len are plain
+             * scalars checked against the region at run time (-EFAULT / -EINVAL); nothing is written */
+            if (mi.type != REGION) return fail(pc, GX_BAD_HELPER, "gdev_prefetch_l2 needs a device-region map");
+            for (int a = 2; a <= 3; a++)
+                if (st.r[a].type != SCALAR)
+                    return fail(pc, st.r[a].type == NOT_INIT ? GX_UNINIT_READ : GX_BAD_HELPER,
+                                a == 2 ? "prefetch address must be a scalar" : "prefetch length must be a scalar");
+            P.ch += 1;
         } else if (id == GX_FN_MEM_PREFETCH) {
             /* gdev_mem_prefetch(queue, addr, len) (F-1): addr and len are
              * plain scalars (no memory is touched), range errors are run-time -EINVAL */
@@ -2013,6 +2022,8 @@ struct Verifier {
                         g.imm = (uint64_t)(uint32_t)f.val_addr;
                     } else if (id == GX_FN_MEM_PREFETCH) {
                         g.op = GX_CALL_MEM_PREFETCH;
+                    } else if (id == GX_FN_PREFETCH_L2) {
+                        g.op = GX_CALL_PREFETCH_L2;
                     } else {
                         g.op = GX_CALL_RINGBUF_OUTPUT;
                         g.off = (int16_t)f.val_addr;
@@ -2131,6 +2142,7 @@ struct Verifier {
             u.effect = true;
             break;
         case GX_CALL_MEM_PREFETCH:
+        case GX_CALL_PREFETCH_L2:
             u.use = R(2) | R(3);
             u.def = 0x3F;
             u.effect = true;
@@ -2336,7 +2348,9 @@ int gx_verify_program(const uint8_t *slots, uint32_t n, const GxMapInfo *maps, c
     uint32_t comm = 1;
     for (int m = 0; m < GX_MAX_MAPS; m++) {
         const GxMapUse &u = out.use[m];
-        if (!u.used || !maps[m].valid || maps[m].type == PT || maps[m].type == RINGBUF || maps[m].type == PFQ) continue;
+        if (!u.used || !maps[m].valid || maps[m].type == PT || maps[m].type == RINGBUF || maps[m].type == PFQ ||
+            maps[m].type == REGION)
+            continue;
         if (u.writes && (u.non_add_write && !u.update_call)) comm = 0;
         if (u.reads && u.writes) comm = 0;
     }

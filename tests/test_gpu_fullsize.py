@@ -106,3 +106,58 @@ def test_c4_full_size(gpu):
     assert got_hits == want_hits
     assert (rt.array_u64(s.fds[(0, "list_bytes")]) == lbytes.cpu().numpy().astype(np.uint64)).all()
     assert int(rt.array_u64(s.fds[(0, "scan_pt")])[0]) == int(scan_bytes)
+
+
+def test_c5_full_size(gpu):
+    """C5: 2^28 multi-tenant events (the bench's single-GPU C5 batch), four programs through the
+    attach table; every tenant's maps against its closed form (closed_forms: c1_counts / c2_expected /
+    c3_expected / c4_expected restricted to the tenant's events, SURVEY.md §8c c.5 "C5 mix"), the
+    ringbuf = one {page, sm_id} record per FAULT event of tenant 2 (as a multiset)."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    n = 1 << 28
+    rt, s, ev = _run("C5", n)
+    w = ev.view(-1, 32).view(dtype=torch.int64)
+    addr, hookw, w3 = w[:, 0], w[:, 2], w[:, 3]
+    tenant = (hookw >> 8) & 0xFF
+    kind = hookw & 0xFF
+    sm, warp, lane, size = w3 & 0xFFFF, (w3 >> 16) & 0xFF, (w3 >> 24) & 0xFF, (w3 >> 32) & 0xFFFFFFFF
+    assert rt.stats()["events_skipped"] == 0
+    # tenant 0: P1
+    t0 = tenant == 0
+    want = torch.bincount(((addr[t0] >> 12) & 255), minlength=256)
+    assert (rt.array_u64(s.fds[(0, "counts")]) == want.cpu().numpy().astype(np.uint64)).all()
+    # tenant 1: P2
+    t1 = tenant == 1
+    hist = torch.bincount(sm[t1] * 64 + warp[t1], minlength=148 * 64)
+    assert (rt.array_u64(s.fds[(1, "hist")]) == hist.cpu().numpy().astype(np.uint64)).all()
+    cnt = torch.bincount(lane[t1], minlength=32)
+    byt = torch.zeros(32, dtype=torch.int64, device=ev.device).index_add_(0, lane[t1], size[t1])
+    pt = rt.array_u64(s.fds[(1, "lane_pt")]).reshape(32, 2)
+    assert (pt[:, 0] == cnt.cpu().numpy().astype(np.uint64)).all()
+    assert (pt[:, 1] == byt.cpu().numpy().astype(np.uint64)).all()
+    # tenant 2: P3' (page counts + unconditional FAULT records)
+    t2 = tenant == 2
+    pages, counts = torch.unique(addr[t2] >> 12, return_counts=True)
+    got = {k: int(v[0]) for k, v in rt.hash_items(s.fds[(2, "lfu")]).items()}
+    assert got == dict(zip(pages.cpu().tolist(), counts.cpu().tolist()))
+    f = t2 & (kind == 2)
+    want_rb = torch.stack([addr[f] >> 12, sm[f]], 1).cpu().numpy().astype(np.uint64)
+    recs = gx.gx_ringbuf_drain(rt.rt, s.fds[(2, "rb")])
+    assert len(recs) == len(want_rb) > 0 and all(len(r) == 16 for r in recs[:1000])
+    got_rb = np.frombuffer(b"".join(recs), dtype=np.uint64).reshape(-1, 2)
+    o1, o2 = np.lexsort(got_rb.T[::-1]), np.lexsort(want_rb.T[::-1])
+    assert (got_rb[o1] == want_rb[o2]).all()
+    # tenant 3: P4
+    t3 = tenant == 3
+    a3, s3 = addr[t3].contiguous(), size[t3]
+    bounds = torch.from_numpy(gen.c4_tables()["bounds"].astype(np.int64)).to(ev.device)
+    is_c = a3 < bounds[0]
+    lst = (torch.searchsorted(bounds, a3, right=True) - 1).clamp(0, 4095)[~is_c]
+    assert int(rt.array_u64(s.fds[(3, "cstat")])[0]) == int(is_c.sum())
+    h = torch.bincount(lst, minlength=4096).cpu().numpy()
+    got_hits = {k: int(v[0]) for k, v in rt.hash_items(s.fds[(3, "list_hits")]).items()}
+    assert got_hits == {int(k): int(h[k]) for k in np.nonzero(h)[0]}
+    lb = torch.zeros(4096, dtype=torch.int64, device=ev.device).index_add_(0, lst, s3[~is_c])
+    assert (rt.array_u64(s.fds[(3, "list_bytes")]) == lb.cpu().numpy().astype(np.uint64)).all()
+    assert int(rt.array_u64(s.fds[(3, "scan_pt")])[0]) == int(s3[~is_c].sum())

@@ -285,7 +285,31 @@ def test_overlapped_batches_parity(gpu, config, engine):
         rt.run(d_ev[k * n:(k + 1) * n], s.prog_arg, overlap=True)
     torch.cuda.synchronize()
     assert outputs(rt, s) == outputs(env, so)
-    assert rt.stats()["events_run"] + rt.stats()["events_skipped"] >= 0
+    st, ost = rt.stats(), env.stats()
+    assert st["events_run"] + st["events_skipped"] == 4 * n
+    assert (st["events_run"], st["events_skipped"]) == (ost["events_run"], ost["events_skipped"])
+
+
+@pytest.mark.parametrize("engine", ["jit", "jit_ring", "interp"])
+@pytest.mark.parametrize("config", ["C2", "C3"])
+def test_batches_on_different_streams_stay_ordered(gpu, config, engine):
+    """Batches of one runtime given to different streams run in submission order (include/gx.h):
+    4 batches alternating between two fresh streams, no host synchronisation in between, give the
+    oracle's maps over the concatenated events -- per-thread shards (C2) and hash + FETCH-ADD +
+    ringbuf (C3) would race if two batches overlapped."""
+    import torch
+    n = (1 << 18) + 32
+    ev = configs.events(config, configs.SEEDS[config], 4 * n)
+    env, so, _ = oracle_run(config, ev, threshold=2 if config == "C3" else None)
+    rt = make_runtime(engine)
+    s = configs.setup(rt, config, threshold=2 if config == "C3" else None)
+    d_ev = torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda()
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for k in range(4):
+        rt.run(d_ev[k * n:(k + 1) * n], s.prog_arg, stream=streams[k % 2])
+    torch.cuda.synchronize()
+    assert outputs(rt, s) == outputs(env, so)
 
 
 @pytest.mark.parametrize("mode,stages,release,claim,rpw", [

@@ -125,3 +125,81 @@ def test_daemon_perthread_snapshot(gpu):
     for name, nbytes in (("hist", 148 * 64 * 8), ("lane_pt", 32 * 16)):
         snap, ver = gx.gx_snapshot_read(rt.rt, s.fds[(0, name)], nbytes)
         assert ver == 2 and snap == env.dump(so.fds[(0, name)]), name
+
+
+# ---- gdev_prefetch_l2 (F-7): R0 against the oracle on both engines; the
+# prefetches themselves land in a real device buffer (registered as the region)
+L2CALL = """
+    ldxdw r2, [r1+0]
+    ldxdw r3, [r1+8]
+    lddw r1, map:region
+    call 1001
+    exit
+"""
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_prefetch_l2_parity(gpu, engine):
+    import torch
+    from oracle.oracle import Oracle
+    span = 4 << 20
+    buf = torch.empty(span, dtype=torch.uint8, device="cuda")
+    base = buf.data_ptr()
+    n = 20000 + 13
+    rng = np.random.default_rng(7)
+    off = rng.integers(-(16 << 10), span + (16 << 10), n)
+    lens = rng.choice(np.array([0, 1, 8, 128, 4096, 65535, 65536, 65537, 1 << 20], dtype=np.int64), n)
+    ev = gen.records(n, addr=(base + off).astype(np.uint64), ts=lens.astype(np.uint64))
+    env = Oracle()
+    want = env.run(ev, env.load_prog(asm.assemble(L2CALL, {"region": env.region_map(base, span)})))
+    rt = make_runtime(engine)
+    prog = rt.load_prog(asm.assemble(L2CALL, {"region": rt.region_map(base, span)}))
+    ret = torch.zeros(n, dtype=torch.int64, device="cuda")
+    rt.run(_dev(ev), prog, ret=ret)
+    torch.cuda.synchronize()
+    got = ret.cpu().numpy().view(np.uint64)
+    assert (got == want).all()
+    assert {0, 2**64 - 14, 2**64 - 22} <= set(want.tolist())      # every outcome occurs
+    assert rt.stats()["helper_errors"] == env.stats()["helper_errors"]
+
+
+def test_region_map_has_no_content(gpu):
+    import torch
+    import paper_2512_12615_b200 as gx
+    buf = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    rt = make_runtime("jit")
+    reg = rt.region_map(buf.data_ptr(), 4096)
+    assert rt.update_map(reg, b"\0" * 4, b"\0" * 8) == -22
+    with pytest.raises(gx.GxError):
+        rt.region_map(0, 16)
+
+
+@pytest.mark.parametrize("n", [1000, (1 << 16) + 17])
+def test_l2_stride_policy_instrumented(gpu, n):
+    """P7 inlined into the vector-add (gx_instrument): both loads of c[i] = a[i] + b[i] run the L2
+    stride prefetch policy; a and b share one registered buffer, so the prefetches ahead of a land
+    in b and those ahead of b's end fall outside (-EFAULT).  R0 per hook and outcome[] vs the oracle."""
+    import torch
+    import paper_2512_12615_b200 as gx
+    from gxin import instrument
+    from oracle.oracle import Oracle
+    buf = torch.randn(2 * n, device="cuda")
+    a, b = buf[:n], buf[n:]
+    c = torch.empty(n, device="cuda")
+    r = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+    dist, ln = 1024, 128
+    rt = gx.Runtime(0)
+    fds = instrument.setup_l2(rt, rt.region_map(buf.data_ptr(), 8 * n), dist, ln)
+    k = gx.gx_instrument(rt.rt, rt.load_prog(asm.assemble(instrument.P7_L2_STRIDE, fds)), instrument.VADD)
+    gx.gx_kernel_launch(rt.rt, k, "vadd", ((n + 255) // 256,), (256,), [a, b, c, r, n])
+    torch.cuda.synchronize()
+    assert torch.equal(c, a + b)
+    addr = np.empty(2 * n, dtype=np.uint64)
+    addr[0::2] = a.data_ptr() + 4 * np.arange(n, dtype=np.uint64)
+    addr[1::2] = b.data_ptr() + 4 * np.arange(n, dtype=np.uint64)
+    env = Oracle()
+    ofds = instrument.setup_l2(env, env.region_map(buf.data_ptr(), 8 * n), dist, ln)
+    want = env.run(gen.records(2 * n, addr=addr), env.load_prog(asm.assemble(instrument.P7_L2_STRIDE, ofds)))
+    assert (r.cpu().numpy().view(np.uint64) == want).all()
+    assert rt.dump(fds["outcome"]) == env.dump(ofds["outcome"])
+    gx.gx_kernel_free(rt.rt, k)

@@ -96,3 +96,69 @@ def test_prefetch_merge_is_union():
     assert env.merge([a, b]) == 0
     q = s.fds[(0, "pfq")]
     assert env.prefetch_requests(q) == whole.prefetch_requests(q)
+
+
+# ---- gdev_prefetch_l2 (PAPER.md:342 device-side prefetch.global.L2; F-7): a hint whose
+# only observable output is R0 -- the error cases below are read off the helper's definition
+L2CALL = """
+    ldxdw r2, [r1+0]
+    ldxdw r3, [r1+8]
+    lddw r1, map:region
+    call 1001
+    exit
+"""
+BASE, SPAN = 0x7F00_0000_0000, 1 << 20
+
+
+@pytest.mark.parametrize("addr,length,want", [
+    (BASE, 1, 0),                             # first byte
+    (BASE + SPAN - 1, 1, 0),                  # last byte
+    (BASE + SPAN - 65536, 65536, 0),          # ends exactly at the region end, maximum length
+    (BASE + 100, 65537, -22),                 # longer than 64 KiB
+    (BASE + 100, 0, -22),                     # empty
+    (BASE - 1, 2, -14),                       # starts one byte before the region
+    (BASE + SPAN - 1, 2, -14),                # ends one byte past it
+    (BASE + SPAN, 1, -14),                    # just after
+    (2**64 - 8, 16, -14),                     # wraps around the address space
+    (0, 16, -14),
+])
+def test_prefetch_l2_cases(addr, length, want):
+    from oracle.oracle import Oracle
+    env = Oracle()
+    reg = env.region_map(BASE, SPAN)
+    ev = gen.records(1, addr=np.uint64(addr), ts=np.uint64(length))
+    r0 = env.run(ev, env.load_prog(asm.assemble(L2CALL, {"region": reg})))
+    assert int(r0[0]) == want % 2**64
+    assert env.stats()["helper_errors"] == (1 if want else 0)
+
+
+def test_prefetch_l2_region_has_no_content():
+    """A region is not a keyed map: lookups fault, host writes and dumps are refused."""
+    from oracle.oracle import Oracle, OracleFault
+    env = Oracle()
+    reg = env.region_map(BASE, SPAN)
+    assert env.update_map(reg, b"\0" * 4, b"\0" * 8) == -22
+    with pytest.raises(OracleFault):
+        env.run(gen.records(1), env.load_prog(asm.assemble(
+            "stw [r10-4], 0\nlddw r1, map:region\nmov64 r2, r10\nadd64 r2, -4\ncall 1\nmov64 r0, 0\nexit",
+            {"region": reg})))
+    with pytest.raises(OSError):
+        env.region_map(0, 16)
+
+
+def test_l2_stride_policy_closed_form():
+    """P7, the device L2 stride prefetch policy (gxin/instrument.py): for an access at a the hook
+    prefetches [a + dist, a + dist + len); R0 is that call's result and outcome[] counts 0 / -EINVAL
+    / -EFAULT.  Closed form over a strided access stream crossing the region's end."""
+    from gxin import instrument
+    from oracle.oracle import ARRAY, Oracle
+    env = Oracle()
+    n, stride, dist, ln = 5000, 256, 4096, 128
+    reg = env.region_map(BASE, n * stride)
+    fds = instrument.setup_l2(env, reg, dist, ln)
+    addr = BASE + stride * np.arange(n, dtype=np.uint64)
+    r0 = env.run(gen.records(n, addr=addr), env.load_prog(asm.assemble(instrument.P7_L2_STRIDE, fds)))
+    inside = (addr + np.uint64(dist + ln)) <= np.uint64(BASE + n * stride)
+    want = np.where(inside, 0, 2**64 - 14).astype(np.uint64)
+    assert (r0 == want).all()
+    assert env.array_u64(fds["outcome"]).tolist() == [int(inside.sum()), 0, int((~inside).sum())]

@@ -7,9 +7,9 @@ from gxin import sched
 from oracle.oracle import Oracle
 
 
-def _run(policy, cost, home, W, steal_cost=0, budget=0):
+def _run(policy, cost, home, W, steal_cost=0, budget=0, max_steals=0):
     env = Oracle()
-    prog, fds = sched.setup(env, policy, W, budget_us=budget)
+    prog, fds = sched.setup(env, policy, W, budget_us=budget, max_steals=max_steals)
     r = env.sched_run(prog, cost, home, W, steal_cost)
     return r, env, fds
 
@@ -67,3 +67,36 @@ def test_latency_budget_caps_stolen_work():
     for u in np.nonzero(r["stolen"])[0]:
         last[r["executed_by"][u]] = max(last[r["executed_by"][u]], cost[u])
     assert (stolen_work <= budget + last).all()
+
+
+def test_max_steals_hand_example():
+    """MaxSteals with cap 1 on the victim example, timeline worked by hand (equal 10-us
+    units, free steals, lowest id first at equal times): w0 steals unit 3 at t=0, is refused at 10;
+    w1 runs 0,1,2 then steals unit 7 from w2 at t=30 (w1 moves before w2 at t=30) and is refused at
+    40; w2 runs 4,5,6, is granted at 30 but finds nothing.  Greedy instead has w0 steal unit 7 at 10."""
+    cost = np.full(8, 10)
+    home = np.array([1, 1, 1, 1, 2, 2, 2, 2])
+    r, env, fds = _run("max_steals", cost, home, 3, max_steals=1)
+    assert r["executed_by"].tolist() == [1, 1, 1, 0, 2, 2, 2, 1]
+    assert r["stolen"].tolist() == [0, 0, 0, 1, 0, 0, 0, 1]
+    assert r["steals"].tolist() == [1, 1, 0] and r["makespan_us"] == 40
+    assert env.array_u64(fds["steals"]).tolist() == [1, 1, 1]       # granted decisions
+    g, _, _ = _run("greedy", cost, home, 3)
+    assert g["executed_by"][7] == 0
+
+
+@pytest.mark.parametrize("kind", ["moderate", "heavy"])
+def test_max_steals_limits(kind):
+    """Cap 0 is FixedWork; a cap >= the unit count is Greedy; any cap bounds each worker's steals."""
+    cost, home = sched.workload(kind, 16)
+    f, _, _ = _run("fixed", cost, home, 16, steal_cost=2)
+    g, _, _ = _run("greedy", cost, home, 16, steal_cost=2)
+    m0, _, _ = _run("max_steals", cost, home, 16, steal_cost=2, max_steals=0)
+    mi, _, _ = _run("max_steals", cost, home, 16, steal_cost=2, max_steals=len(cost))
+    for a, b in ((m0, f), (mi, g)):
+        assert (a["executed_by"] == b["executed_by"]).all() and a["makespan_us"] == b["makespan_us"]
+    for cap in (1, 2, 3):
+        r, env, fds = _run("max_steals", cost, home, 16, steal_cost=2, max_steals=cap)
+        granted = env.array_u64(fds["steals"])
+        assert (r["steals"] <= cap).all() and (granted <= cap).all()
+        assert ((granted - r["steals"]) <= 1).all()                  # at most one granted attempt finds nothing

@@ -5,10 +5,10 @@ import pytest
 import paper_2512_12615_b200 as gx
 from gxin import asm, programs
 
-HASH, ARRAY, PT, RINGBUF, PFQ = 1, 2, 6, 27, 64
+HASH, ARRAY, PT, RINGBUF, PFQ, REGION = 1, 2, 6, 27, 64, 65
 MAPS = {0: (ARRAY, 4, 8, 16), 1: (HASH, 8, 8, 64), 2: (PT, 4, 16, 32), 3: (RINGBUF, 0, 0, 4096),
-        4: (ARRAY, 4, 2048, 1), 5: (PFQ, 0, 0, 64)}
-NAMES = {"arr": 0, "h": 1, "pt": 2, "rb": 3, "g": 4, "pfq": 5}
+        4: (ARRAY, 4, 2048, 1), 5: (PFQ, 0, 0, 64), 6: (REGION, 0, 0, 1)}
+NAMES = {"arr": 0, "h": 1, "pt": 2, "rb": 3, "g": 4, "pfq": 5, "reg": 6}
 
 
 def verify(text, strict=False, **kw):
@@ -38,6 +38,7 @@ ACCEPT = {
     "atomic_fetch": LOOKUP + "jeq r0, 0, +4\nmov64 r1, 1\natomic_fetch_add64 [r0+0], r1\nmov64 r0, r1\nexit\nmov64 r0, 0\nexit",
     "hash_update": "stdw [r10-8], 5\nstdw [r10-16], 7\nlddw r1, map:h\nmov64 r2, r10\nadd64 r2, -8\nmov64 r3, r10\nadd64 r3, -16\nmov64 r4, 0\ncall 2\nexit",
     "mem_prefetch": "ldxdw r2, [r1+0]\nmov64 r3, 4096\nlddw r1, map:pfq\ncall 1000\nexit",
+    "prefetch_l2": "ldxdw r2, [r1+0]\nmov64 r3, 128\nlddw r1, map:reg\ncall 1001\nexit",
     "mem_prefetch_policy": programs.P6.replace("map:pfq", "map:pfq").replace("mapval:pstat+0", "mapval:g+0"),
     "ringbuf": "stdw [r10-16], 1\nstdw [r10-8], 2\nlddw r1, map:rb\nmov64 r2, r10\nadd64 r2, -16\nmov64 r3, 16\nmov64 r4, 0\ncall 130\nexit",
     "percpu_rmw": "stw [r10-4], 3\nlddw r1, map:pt\nmov64 r2, r10\nadd64 r2, -4\ncall 1\njeq r0, 0, +3\nldxdw r1, [r0+8]\nadd64 r1, 1\nstxdw [r0+8], r1\nmov64 r0, 0\nexit",
@@ -85,6 +86,11 @@ REJECT = {
     "prefetch_on_array": ("mov64 r2, 0\nmov64 r3, 64\nlddw r1, map:arr\ncall 1000\nexit", False, "BAD_HELPER"),
     "prefetch_uninit_len": ("mov64 r2, 0\nlddw r1, map:pfq\ncall 1000\nexit", False, "UNINIT_READ"),
     "prefetch_ptr_len": ("mov64 r2, 0\nmov64 r3, r10\nlddw r1, map:pfq\ncall 1000\nexit", False, "BAD_HELPER"),
+    "prefetch_l2_on_queue": ("mov64 r2, 0\nmov64 r3, 64\nlddw r1, map:pfq\ncall 1001\nexit", False, "BAD_HELPER"),
+    "mem_prefetch_on_region": ("mov64 r2, 0\nmov64 r3, 64\nlddw r1, map:reg\ncall 1000\nexit", False, "BAD_HELPER"),
+    "prefetch_l2_uninit_len": ("mov64 r2, 0\nlddw r1, map:reg\ncall 1001\nexit", False, "UNINIT_READ"),
+    "prefetch_l2_ptr_addr": ("mov64 r2, r10\nmov64 r3, 8\nlddw r1, map:reg\ncall 1001\nexit", False, "BAD_HELPER"),
+    "lookup_on_region": ("stw [r10-4], 0\nlddw r1, map:reg\nmov64 r2, r10\nadd64 r2, -4\ncall 1\nmov64 r0, 0\nexit", False, "BAD_HELPER"),
     "lookup_on_prefetch_queue": ("stw [r10-4], 0\nlddw r1, map:pfq\nmov64 r2, r10\nadd64 r2, -4\ncall 1\nmov64 r0, 0\nexit", False, "BAD_HELPER"),
     "ringbuf_var_size": ("ldxdw r3, [r1+0]\nstdw [r10-8], 1\nlddw r1, map:rb\nmov64 r2, r10\nadd64 r2, -8\nmov64 r4, 0\ncall 130\nexit", False, "BAD_HELPER"),
     "bad_reg": (".raw 0xb7 11 0 0 0\nexit", False, "BAD_REG"),
