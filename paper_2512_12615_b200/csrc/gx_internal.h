@@ -41,8 +41,12 @@ struct GxInsn {
 #define GXF_FETCH 0x04    /* atomic returns the old value */
 #define GXF_W32 0x08      /* 32-bit atomic / memory width helper flag */
 #define GXF_KEY_MAPV 0x10 /* helper key pointer is a map value (else stack slot in off) */
+#define GXF_PT_VSTART 0x10 /* per-thread memory ops: the base register is a value start on every
+                              path (the access is word off >> 3 of the value; JIT register cache) */
 #define GXF_VAL_MAPV 0x20 /* helper value/data pointer is a map value (else stack slot) */
 #define GXF_PRIV 0x40     /* atomic target map is privatized in shared memory */
+#define GXF_NARROW 0x20   /* ALU64: operands and result below 2^32 on every explored path (the verifier's
+                             intervals), so the 32-bit operation, zero-extended, is exact */
 #define GXF_UNIFORM 0x80  /* verifier: branch operands are warp-uniform (hint) */
 
 /* sizes: aux low bits for memory ops = log2(size) */

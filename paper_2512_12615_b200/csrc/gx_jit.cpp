@@ -223,6 +223,48 @@ struct Gen {
     int hc_map_ = -1;    /* HASH map with the shared-memory key -> slot cache (GX_JIT_HASH_CACHE entries) */
     uint32_t hc_n_ = 0;
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
+    int pkc_fd_ = -1;    /* the per-thread map held in the register key cache (GX_JIT_PTKC), or -1 */
+    /* the per-thread key cache's access forms: key from the value-start pointer, constant word */
+    std::string pkc_key(const std::string &ptr) const {
+        const GxMapDesc &d = L.maps[pkc_fd_];
+        uint32_t lvs = 0;
+        while ((1u << lvs) < d.value_size) lvs++;
+        return "{ const uint32_t k_ = (uint32_t)(" + ptr + " - " + hex(d.data) + ") >> " + std::to_string(lvs) +
+               "; if (k_ != pkc.key) ptkc_switch<" + std::to_string(d.max_entries) + "u, " + std::to_string(d.value_size / 8) +
+               "u>(pkc, " + hex(d.data) + ", k_, shard); }";
+    }
+    /* picks the per-thread map for the key cache: every access to it is through a value-start pointer,
+     * at most 4 words per value, no helper writes it (map update) or reads through a map-value
+     * pointer (conservatively: no helper takes map-value pointers at all), the most accesses wins */
+    void pick_pkc(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+        pkc_fd_ = -1;
+        if (getenv("GX_JIT_PTKC") && atoi(getenv("GX_JIT_PTKC")) == 0) return;
+        std::map<int, int> hits;
+        std::set<int> bad;
+        bool mapv_helper = false;
+        for (size_t q = 0; q < images.size(); q++)
+            for (uint32_t i = 0; i < sizes[q]; i++) {
+                const GxInsn &g = images[q][i];
+                int fd = -1;
+                if (g.op == GX_LDX_PT) fd = (int)g.imm;
+                else if (g.op == GX_ST_PT || g.op == GX_ATOM_PT) fd = g.aux >> 4;
+                else if (g.op == GX_CALL_UPDATE_PT) bad.insert(g.aux);
+                if (g.op >= GX_CALL_LOOKUP_ARRAY && g.op <= GX_CALL_RINGBUF_OUTPUT && (g.flags & (GXF_KEY_MAPV | GXF_VAL_MAPV)))
+                    mapv_helper = true;
+                if (fd < 0) continue;
+                if (!(g.flags & GXF_PT_VSTART)) bad.insert(fd);
+                hits[fd]++;
+            }
+        if (mapv_helper) return;
+        int best = 0;
+        for (auto &kv : hits) {
+            const GxMapDesc &d = L.maps[kv.first];
+            if (bad.count(kv.first) || d.value_size > 32 || (d.value_size & (d.value_size - 1)) ||
+                (uint64_t)d.max_entries * d.value_size >= (1ull << 31))
+                continue;
+            if (kv.second > best) best = kv.second, pkc_fd_ = kv.first;
+        }
+    }
     void st(const std::string &x) { (*out_) << "  " << x << "\n"; }
     void me(const std::string &x) { (*out_) << "  { " << x << " }\n"; }
     std::string M() const { return dmode_ ? "exec" : "active"; }
@@ -288,7 +330,7 @@ struct Gen {
         }
         o << "template <bool FULL>\n__device__ __forceinline__ void prog" << q
           << "(const Ctx &c, unsigned active, uint64_t &retv, const uint32_t shard, uint32_t *spriv, "
-             "unsigned &c_herr, unsigned &c_drop, unsigned long long &c_rbb, unsigned &c_hfull, PtCache &ptc) {\n"
+             "unsigned &c_herr, unsigned &c_drop, unsigned long long &c_rbb, unsigned &c_hfull, PtCache &ptc, GxPkc &pkc) {\n"
              "  const unsigned lane = threadIdx.x & 31;\n"
              "  if (FULL) active = GX_ALL;\n"
              "  if (!((active >> lane) & 1)) return;\n"
@@ -370,6 +412,32 @@ struct Gen {
         auto ld_fix = [&](const std::string &v) {
             return sxf ? "sx(" + v + ", " + std::to_string(8u << lg) + ")" : v;
         };
+        if (g.flags & GXF_NARROW) {
+            /* the verifier proved operands and result below 2^32 on every path: the 32-bit operation,
+             * zero-extended, is the 64-bit one (and the compiler keeps the upper halves known-zero) */
+            const std::string a = "(uint32_t)" + d, b = (g.flags & GXF_X) ? "(uint32_t)" + s : std::to_string((uint32_t)g.imm) + "u";
+            const char *opc = nullptr;
+            switch (g.op) {
+            case GX_ADD64: opc = "+"; break;
+            case GX_SUB64: opc = "-"; break;
+            case GX_MUL64: opc = "*"; break;
+            case GX_OR64: opc = "|"; break;
+            case GX_AND64: opc = "&"; break;
+            case GX_XOR64: opc = "^"; break;
+            case GX_RSH64: opc = ">>"; break;
+            default: break;
+            }
+            if (opc) {
+                me(d + " = (uint64_t)(uint32_t)(" + a + " " + opc + " " + b + ");");
+                return;
+            }
+            if (g.op == GX_DIV64 || g.op == GX_MOD64) {
+                const bool dv = g.op == GX_DIV64;
+                me("const uint32_t t = " + b + ", a_ = " + a + "; " + d + " = (uint64_t)(t ? a_ " + (dv ? "/" : "%") + " t : " +
+                   (dv ? "0u" : "a_") + ");");
+                return;
+            }
+        }
         switch (g.op) {
         case GX_ADD64: me(d + " += " + S64 + ";"); break;
         case GX_SUB64: me(d + " -= " + S64 + ";"); break;
@@ -442,7 +510,10 @@ struct Gen {
             break;
         }
         case GX_LDX_PT:
-            if (ptc_)
+            if ((int)g.imm == pkc_fd_)
+                me(pkc_key(s) + " " + d + " = " + ld_fix("zx(pkc.v[" + std::to_string(g.off >> 3) + "] >> " +
+                                                          std::to_string(8 * (g.off & 7)) + ", " + std::to_string(lg) + ")") + ";");
+            else if (ptc_)
                 me("const uint64_t la_ = " + s + " + (int64_t)" + std::to_string(g.off) + "; " + d + " = " +
                    ld_fix("ptc_ld(ptc, la_, " + ptp((int)g.imm, "la_") + ", " + std::to_string(lg) + ")") + ";");
             else
@@ -461,7 +532,10 @@ struct Gen {
         }
         case GX_ST_PT: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            if (ptc_)
+            if ((g.aux >> 4) == pkc_fd_) {
+                const std::string w = "pkc.v[" + std::to_string(g.off >> 3) + "]";
+                me(pkc_key(d) + " " + w + " = word_set(" + w + ", " + std::to_string(g.off & 7) + ", " + std::to_string(lg) + ", " + v + ");");
+            } else if (ptc_)
                 me("const uint64_t la_ = " + d + " + (int64_t)" + std::to_string(g.off) + "; ptc_st(ptc, la_, " + ptp(g.aux >> 4, "la_") + ", " + std::to_string(lg) + ", " + v + ");");
             else
                 me("ptstore((uint64_t)" + ptp(g.aux >> 4, d + " + (int64_t)" + std::to_string(g.off)) + ", " + std::to_string(lg) +
@@ -486,8 +560,11 @@ struct Gen {
                 const std::string key = (g.flags & GXF_KEY_MAPV)
                                             ? "*(const uint32_t *)r2"
                                             : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
-                me("const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
-                   " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0;");
+                if (g.flags & GXF_SX) /* key below max_entries on every path (verifier): never NULL */
+                    me("const uint32_t k = " + key + "; r0 = " + hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u;");
+                else
+                    me("const uint32_t k = " + key + "; r0 = k < " + std::to_string(m.max_entries) + "u ? " + hex(m.data) +
+                       " + (uint64_t)k * " + std::to_string(m.value_size) + "u : 0;");
             }
             if (g.flags & GXF_FETCH) branch("r0 == 0", (uint32_t)g.imm, i + 1, (g.flags & GXF_UNIFORM) != 0);
             if (g.flags & GXF_W32) branch("r0 != 0", (uint32_t)g.imm, i + 1, (g.flags & GXF_UNIFORM) != 0);
@@ -619,6 +696,12 @@ struct Gen {
         }
         const int fd = g.aux >> 4;
         const std::string addr = R(g.dst) + " + (int64_t)" + std::to_string(g.off);
+        if (g.op == GX_ATOM_PT && fd == pkc_fd_) {
+            std::string e = "rmw_word(pkc.v[" + std::to_string(g.off >> 3) + "], " + std::to_string(g.off & 7) + ", " +
+                            (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
+            me(pkc_key(R(g.dst)) + " " + (fetch ? "const uint64_t old = " + e + "; " + ret + " = old;" : "(void)" + e + ";"));
+            return;
+        }
         if (g.op == GX_ATOM_PT) {
             std::string e = ptc_ ? "ptc_rmw(ptc, " + addr + ", " + ptp(fd, addr) + ", " +
                                        (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)"
@@ -678,6 +761,11 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_PROBE_W")) o << "#define GX_HASH_PROBE_W " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
+        pick_pkc(images, sizes);
+        if (pkc_fd_ >= 0)
+            o << "typedef PtKc<" << L.maps[pkc_fd_].max_entries << "u, " << L.maps[pkc_fd_].value_size / 8 << "u> GxPkc;\n";
+        else
+            o << "typedef PtKc<1u, 1u> GxPkc;\n";
         /* the first HASH map with 8-byte values that a program looks up gets the per-block key -> slot
          * cache (GX_JIT_HASH_CACHE entries, a power of two; 0 = off) */
         {
@@ -732,7 +820,8 @@ struct Gen {
     void instrument(const GxInsn *image, uint32_t n, const std::string &user) {
         ptc_ = false;
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
-        o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
+        o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\ntypedef PtKc<1u, 1u> GxPkc;\n\n";
+        pkc_fd_ = -1; /* no flush point in a user kernel */
         program(0, image, n);
         o << "/* rec (optional): receives the 32-B event record the program ran on (hook logs) */\n"
              "__device__ __forceinline__ uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size,\n"
@@ -754,9 +843,9 @@ struct Gen {
              "  uint64_t retv = 0;\n"
              "  unsigned herr = 0, drop = 0, hfull = 0;\n"
              "  unsigned long long rbb = 0;\n"
-             "  PtCache ptc;\n"
-             "  if (group == GX_ALL) prog0<true>(c, GX_ALL, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
-             "  else prog0<false>(c, group, retv, shard, nullptr, herr, drop, rbb, hfull, ptc);\n"
+             "  PtCache ptc;\n  GxPkc pkc;\n"
+             "  if (group == GX_ALL) prog0<true>(c, GX_ALL, retv, shard, nullptr, herr, drop, rbb, hfull, ptc, pkc);\n"
+             "  else prog0<false>(c, group, retv, shard, nullptr, herr, drop, rbb, hfull, ptc, pkc);\n"
              "  unsigned long long *st = (unsigned long long *)" << hex(L.stats) << ";\n"
              "  if (herr) atomicAdd(&st[" << GXS_HERR << "], herr);\n"
              "  if (drop) atomicAdd(&st[" << GXS_RB_DROPS << "], drop);\n"
@@ -802,7 +891,7 @@ struct Gen {
              "  /* per-thread event counts in 32 bits (register pressure), widened for the warp reduction */\n"
              "  unsigned c_run = 0, c_skip = 0, c_herr = 0, c_drop = 0, c_hfull = 0;\n"
              "  unsigned long long c_rbb = 0;\n"
-             "  PtCache ptc;\n"
+             "  PtCache ptc;\n  GxPkc pkc;\n"
              "  const uint64_t nrec = (n + 31) >> 5, nfull = n >> 5; /* records, whole records */\n"
              "  const uint64_t nwarps = (uint64_t)gridDim.x * " << B / 32 << ";\n"
              "  const uint64_t pol = evict_first_policy();\n"
@@ -1006,12 +1095,12 @@ struct Gen {
              * the whole-warp instance; a ragged tail record runs the masked one.  The run count (= n)
              * is added once at the end instead of per event. */
             o << "    if (rec < nfull) {\n"
-                 "      prog0<true>(c, GX_ALL, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                 "      prog0<true>(c, GX_ALL, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc, pkc);\n"
                  "      if (WANT_RET) ret[i] = retv;\n"
                  "    } else {\n"
                  "      const bool valid = i < n;\n"
                  "      const unsigned m = __ballot_sync(GX_ALL, valid);\n"
-                 "      prog0<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
+                 "      prog0<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc, pkc);\n"
                  "      if (WANT_RET && valid) ret[i] = retv;\n"
                  "    }\n";
         } else {
@@ -1029,13 +1118,16 @@ struct Gen {
                  "      todo &= ~m;\n"
                  "      switch (pq) {\n";
             for (size_t q = 0; q < images.size(); q++)
-                o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n"
-                  << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc);\n        break;\n";
+                o << "      case " << q << ":\n        if (m == GX_ALL) prog" << q << "<true>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc, pkc);\n"
+                  << "        else prog" << q << "<false>(c, m, retv, shard, spriv, c_herr, c_drop, c_rbb, c_hfull, ptc, pkc);\n        break;\n";
             o << "      default: break;\n      }\n    }\n"
                  "    if (WANT_RET && valid) ret[i] = retv;\n";
         }
         o << (two_level ? "    }\n  }\n" : "  }\n");
-        o << "  ptc_flush(ptc);\n"
+        o << "  ptc_flush(ptc);\n";
+        if (pkc_fd_ >= 0)
+            o << "  ptkc_flush(pkc, " << hex(L.maps[pkc_fd_].data) << ", shard);\n";
+        o << ""
              "  {\n"
              "  unsigned long long w_run = c_run, w_skip = c_skip, w_herr = c_herr, w_drop = c_drop, w_hfull = c_hfull;\n"
              "  for (int s = 16; s; s >>= 1) {\n"

@@ -553,6 +553,39 @@ __device__ __forceinline__ uint8_t *pt_phys_c(uint64_t data, uint64_t logical, u
     return reinterpret_cast<uint8_t *>(base + (uint64_t)(((kk * W + w) << 8) | (lo & 7)));
 }
 
+/* Per-thread key cache (GX_JIT_PTKC): ONE per-thread map of K entries x W words, one key at a time,
+ * its W value words held in registers.  Every access to that map goes through a value-start pointer
+ * (verifier GXF_PT_VSTART), so the key is (pointer - data) / (8 W) and the word is the access's
+ * constant offset / 8: a hit is register arithmetic; a miss writes the cached key's words back to
+ * this thread's shard and loads the new key's.  Exact: the shard belongs to this thread for the
+ * whole launch (no other thread, helper or program reads it -- the JIT checks) and the cache is
+ * written back before the launch ends (ptkc_flush). */
+template <uint32_t K, uint32_t W>
+struct PtKc {
+    uint32_t key = 0xFFFFFFFFu;
+    uint64_t v[W];
+};
+template <uint32_t K, uint32_t W>
+__device__ __forceinline__ void ptkc_switch(PtKc<K, W> &c, uint64_t data, uint32_t key, uint32_t shard) {
+    if (c.key != 0xFFFFFFFFu) {
+#pragma unroll
+        for (uint32_t w = 0; w < W; w++)
+            *reinterpret_cast<uint64_t *>(pt_phys_c<K, W>(data, data + (uint64_t)c.key * (W * 8) + 8 * w, shard)) = c.v[w];
+    }
+#pragma unroll
+    for (uint32_t w = 0; w < W; w++)
+        c.v[w] = *reinterpret_cast<const uint64_t *>(pt_phys_c<K, W>(data, data + (uint64_t)key * (W * 8) + 8 * w, shard));
+    c.key = key;
+}
+template <uint32_t K, uint32_t W>
+__device__ __forceinline__ void ptkc_flush(PtKc<K, W> &c, uint64_t data, uint32_t shard) {
+    if (c.key != 0xFFFFFFFFu) {
+#pragma unroll
+        for (uint32_t w = 0; w < W; w++)
+            *reinterpret_cast<uint64_t *>(pt_phys_c<K, W>(data, data + (uint64_t)c.key * (W * 8) + 8 * w, shard)) = c.v[w];
+    }
+}
+
 /* privatised write-only ADD accumulator: lo/hi u32 counters in shared memory; one shared atomic
  * per group when the group adds to one word, else one per lane */
 __device__ __forceinline__ void priv_one(uint32_t *lo, uint32_t *hi, uint32_t w, uint64_t v) {

@@ -492,6 +492,9 @@ struct Fact {
     int32_t key_addr = 0, val_addr = 0;
     int64_t rb_size = -1, rb_flags = -1;
     uint8_t br = 0;              /* conditional jumps: 1 = taken on some path, 2 = fell through on some path */
+    bool pt_vstart = false;      /* PTV memory insns: the base register is a value start (no offset) on every path */
+    uint8_t narrow = 0;          /* scalar ALU64: 1 = operands and result below 2^32 on every path, 2 = not */
+    uint8_t inrange = 0;         /* ARRAY / PERTHREAD lookups: 1 = key below max_entries on every path, 2 = not */
 };
 
 struct Checkpoint {
@@ -733,6 +736,7 @@ struct Verifier {
     }
 
     /* ---------------------------------------------------------------- stage 3 helpers */
+    bool last_vstart = false;    /* set by check_access: the map value pointer has no offset */
     bool record_mem(uint32_t pc, MemKind k, int map, int32_t saddr) {
         Fact &f = facts[pc];
         if (!f.seen) {
@@ -740,8 +744,10 @@ struct Verifier {
             f.kind = k;
             f.map = (int16_t)map;
             f.stack_addr = saddr;
+            f.pt_vstart = k == MK_PTV && last_vstart;
             return true;
         }
+        if (k == MK_PTV && !last_vstart) f.pt_vstart = false;
         if (f.kind != k || f.map != map || (k == MK_STACK && f.stack_addr != saddr))
             return fail(pc, GX_MIXED_PTR, "the same instruction accesses different pointer kinds/maps/stack offsets on different paths");
         return true;
@@ -796,6 +802,7 @@ struct Verifier {
             if ((t.v | t.m) & (size - 1)) return fail(pc, GX_MISALIGNED, "map value access not naturally aligned");
             kind = mi.type == PT ? MK_PTV : MK_MAPV;
             map = p.map;
+            last_vstart = p.off == 0 && sc_is_const(p.var) && p.var.t.v == 0;
             return true;
         }
         default: return fail(pc, GX_OOB_ACCESS, "bad pointer");
@@ -1041,8 +1048,19 @@ struct Verifier {
                 P.pc++;
                 return 0;
             }
+            const Scalar before = D.var;
             D.var = is64 ? sc_alu64(op, r.off, D.var, src.var) : sc_alu32(op, r.off, D.var, src.var);
             D.type = SCALAR;
+            if (is64) {
+                /* narrow: the 64-bit result equals the zero-extended 32-bit operation (ADD / SUB /
+                 * MUL / unsigned DIV, MOD / OR / AND / XOR, RSH by a count below 32) */
+                const bool kind_ok = op == 0x00 || op == 0x10 || op == 0x20 || op == 0x40 || op == 0x50 || op == 0xA0 ||
+                                     ((op == 0x30 || op == 0x90) && r.off == 0) || (op == 0x70 && src.var.umax < 32);
+                const bool nar = kind_ok && before.umax < (1ull << 32) && src.var.umax < (1ull << 32) &&
+                                 D.var.umax < (1ull << 32) && (op != 0x10 || before.umin >= src.var.umax);
+                Fact &f = facts[pc];
+                f.narrow = (f.narrow != 2 && nar) ? 1 : 2;
+            }
             P.pc++;
             return 0;
         }
@@ -1493,10 +1511,13 @@ struct Verifier {
             r0.var = sc_const(0);
             /* an ARRAY lookup whose key is provably below max_entries cannot return NULL */
             uint64_t kmax = 0;
-            if (mi.type == ARRAY && kk == MK_STACK && key_bound(st, ka, kmax) && kmax < mi.max_entries) {
+            const bool inr = (mi.type == ARRAY || mi.type == PT) && kk == MK_STACK && key_bound(st, ka, kmax) &&
+                             kmax < mi.max_entries;
+            if (inr && mi.type == ARRAY) {
                 r0.type = PTR_MAPV;
                 r0.id = 0;
             }
+            facts[pc].inrange = (facts[pc].inrange != 2 && inr) ? 1 : 2;
         } else {
             Scalar s = sc_unknown();
             s.smin = -4095;
@@ -1991,6 +2012,7 @@ struct Verifier {
                         g.aux = (uint16_t)r.off;
                     }
                     g.imm = is64 ? (uint64_t)(int64_t)r.imm : (uint64_t)(uint32_t)r.imm;
+                    if (is64 && f.narrow == 1) g.flags |= GXF_NARROW;
                 }
             } else if (cls == CL_LD) {
                 g.op = GX_LDIMM;
@@ -2016,7 +2038,10 @@ struct Verifier {
                     if (f.key_kind == MK_MAPV) g.flags |= GXF_KEY_MAPV;
                     if (f.val_kind == MK_MAPV) g.flags |= GXF_VAL_MAPV;
                     g.off = (int16_t)f.key_addr;
-                    if (id == 1) g.op = mi.type == ARRAY ? GX_CALL_LOOKUP_ARRAY : mi.type == PT ? GX_CALL_LOOKUP_PT : GX_CALL_LOOKUP_HASH;
+                    if (id == 1) {
+                        g.op = mi.type == ARRAY ? GX_CALL_LOOKUP_ARRAY : mi.type == PT ? GX_CALL_LOOKUP_PT : GX_CALL_LOOKUP_HASH;
+                        if (g.op != GX_CALL_LOOKUP_HASH && f.inrange == 1) g.flags |= GXF_SX; /* key always in range */
+                    }
                     else if (id == 2) {
                         g.op = mi.type == ARRAY ? GX_CALL_UPDATE_ARRAY : mi.type == PT ? GX_CALL_UPDATE_PT : GX_CALL_UPDATE_HASH;
                         g.imm = (uint64_t)(uint32_t)f.val_addr;
@@ -2046,7 +2071,9 @@ struct Verifier {
                 case MK_CTX: g.op = GX_LDX_CTX; g.off = (int16_t)f.stack_addr; break;
                 case MK_STACK: g.op = GX_LDX_STACK; g.off = (int16_t)f.stack_addr; break;
                 case MK_MAPV: g.op = GX_LDX_MAP; g.off = r.off; g.imm = (uint64_t)f.map; break;
-                case MK_PTV: g.op = GX_LDX_PT; g.off = r.off; g.imm = (uint64_t)f.map; break;
+                case MK_PTV: g.op = GX_LDX_PT; g.off = r.off; g.imm = (uint64_t)f.map;
+                    if (f.pt_vstart) g.flags |= GXF_PT_VSTART;
+                    break;
                 default: g.op = GX_OP_NOP;
                 }
             } else if (cls == CL_ST || (cls == CL_STX && (r.code & 0xE0) == 0x60)) {
@@ -2061,7 +2088,9 @@ struct Verifier {
                 switch (f.kind) {
                 case MK_STACK: g.op = GX_ST_STACK; g.off = (int16_t)f.stack_addr; break;
                 case MK_MAPV: g.op = GX_ST_MAP; g.off = r.off; break;
-                case MK_PTV: g.op = GX_ST_PT; g.off = r.off; break;
+                case MK_PTV: g.op = GX_ST_PT; g.off = r.off;
+                    if (f.pt_vstart) g.flags |= GXF_PT_VSTART;
+                    break;
                 default: g.op = GX_OP_NOP;
                 }
                 if (f.kind == MK_PTV) g.aux = (uint16_t)(lg(sz) | (f.map << 4));
@@ -2073,7 +2102,9 @@ struct Verifier {
                 switch (f.kind) {
                 case MK_STACK: g.op = GX_ATOM_STACK; g.off = (int16_t)f.stack_addr; break;
                 case MK_MAPV: g.op = GX_ATOM_MAP; g.off = r.off; break;
-                case MK_PTV: g.op = GX_ATOM_PT; g.off = r.off; break;
+                case MK_PTV: g.op = GX_ATOM_PT; g.off = r.off;
+                    if (f.pt_vstart) g.flags |= GXF_PT_VSTART;
+                    break;
                 default: g.op = GX_OP_NOP;
                 }
             }
