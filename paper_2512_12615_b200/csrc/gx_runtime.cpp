@@ -30,6 +30,7 @@
 
 #include <cuda.h>
 #include <nccl.h> /* types only: libnccl is dlopen'ed at gx_comm_init (no link-time dependency) */
+#include <nvtx3/nvToolsExt.h> /* header-only: ranges reach a profiler only when one injects itself */
 #include <chrono>
 
 extern "C" {
@@ -235,6 +236,27 @@ struct gx_rt {
 
 namespace {
 
+/* GX_LOG_LEVEL: 0 silent (default), 1 errors (every -errno with its text),
+ * 2 + JIT compiles (variant, block, grid, shared memory, milliseconds) and merges, 3 + every launch. */
+int log_level() {
+    static const int lv = getenv("GX_LOG_LEVEL") ? atoi(getenv("GX_LOG_LEVEL")) : 0;
+    return lv;
+}
+void gx_log(int level, const char *fmt, ...) {
+    if (level > log_level()) return;
+    char buf[768];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    fprintf(stderr, "[gx:%d] %s\n", level, buf);
+}
+/* NVTX range for the duration of a public call (no-op unless a profiler injects NVTX) */
+struct NvtxScope {
+    explicit NvtxScope(const char *name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
+
 int set_err(gx_rt *rt, int code, const char *fmt, ...) {
     char buf[512];
     va_list ap;
@@ -242,6 +264,7 @@ int set_err(gx_rt *rt, int code, const char *fmt, ...) {
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
     if (rt) rt->err = buf;
+    gx_log(1, "error %d: %s", code, buf);
     return code;
 }
 
@@ -442,7 +465,10 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
     uint64_t worst = 0;
     for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
     cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
-    cfg.jit_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    cfg.jit_ms += ms;
+    gx_log(2, "JIT variant %d (%s ingest%s): %zu program(s), block %u, grid %u, %u B dynamic shared, %.1f ms", k,
+           ring ? "ring" : "register", (k & 1) ? ", R0" : "", cfg.progs.size(), V.block, V.grid, V.smem, ms);
     return 0;
 }
 
@@ -577,6 +603,8 @@ int order_after_last(gx_rt *rt, cudaStream_t stream) {
 int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint64_t *d_ret, cudaStream_t stream,
                uint32_t flags = 0) {
     if (int rc = order_after_last(rt, stream)) return rc;
+    gx_log(3, "batch %llu: %llu events, %s engine, stream %p", (unsigned long long)rt->n_launches, (unsigned long long)n,
+           rt->engine == GX_ENGINE_JIT ? "jit" : "interp", (void *)stream);
     if (rt->engine == GX_ENGINE_JIT) {
         if (!cfg.jv[0].tried && !cfg.jv[1].tried && !cfg.jv[2].tried && !cfg.jv[3].tried) {
             uint64_t worst = 0; /* ring_ok before the first compile (jit_prepare sets it too) */
@@ -1001,6 +1029,7 @@ int gx_load_prog(gx_rt *rt, uint32_t hook, const void *insn_slots, uint32_t n_sl
 
 int gx_verify(gx_rt *rt, int prog_fd, const gx_verify_opts *opts, gx_verify_report *report, char *log,
               uint64_t log_len) {
+    NvtxScope nv("gx_verify");
     if (!check_prog(rt, prog_fd)) return -ENOENT;
     Prog &p = rt->progs[prog_fd];
     GxMapInfo mi[GX_MAX_MAPS];
@@ -1121,6 +1150,7 @@ int gx_attach(gx_rt *rt, int prog_fd, uint32_t kind, uint32_t tenant) {
 }
 
 int gx_run_batch(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, uint64_t *d_ret, void *stream) {
+    NvtxScope nv("gx_run_batch");
     return gx_run_batch_ex(rt, d_events, n, prog_fd, d_ret, stream, 0);
 }
 
@@ -1137,6 +1167,7 @@ int gx_run_batch_ex(gx_rt *rt, const void *d_events, uint64_t n, int prog_fd, ui
 }
 
 int gx_run_batch_host(gx_rt *rt, const void *h_events, uint64_t n, int prog_fd, uint64_t *h_ret) {
+    NvtxScope nv("gx_run_batch_host");
     if (!rt || (!h_events && n)) return -EINVAL;
     if (n == 0) return 0;
     if (prog_fd >= 0 && !check_prog(rt, prog_fd)) return -ENOENT;
@@ -2183,7 +2214,9 @@ int gx_comm_init_host(gx_rt *rt, const gx_comm_host_ops *ops, int nranks, int ra
 }
 
 int gx_merge(gx_rt *rt, void *cuda_stream) {
+    NvtxScope nv("gx_merge");
     if (!rt) return -EINVAL;
+    gx_log(2, "merge %llu", (unsigned long long)rt->merges);
     if (!rt->comm) return set_err(rt, -EINVAL, "gx_merge before gx_comm_init");
     CK(cudaSetDevice(rt->dev), "cudaSetDevice");
     cudaStream_t s = (cudaStream_t)cuda_stream;
