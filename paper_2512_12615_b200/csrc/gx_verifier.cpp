@@ -42,7 +42,11 @@ inline uint32_t size_of(uint8_t code) {
     return sz[(code >> 3) & 3];
 }
 
-/* --------------------------------------------------------------------------- tnum */
+/* --------------------------------------------------------------------------- tnum
+ * Tristate numbers (value v, unknown-bit mask m) with the published carry-propagation rules for
+ * addition and subtraction: the Linux kernel verifier's kernel/bpf/tnum.c (tnum_add / tnum_sub,
+ * whose sigma/chi/mu naming is kept here so the two can be compared), proved sound in Vishwanathan
+ * et al., "Sound, Precise, and Fast Abstract Interpretation with Tristate Numbers" (CGO 2022). */
 struct Tnum {
     uint64_t v, m;
 };
