@@ -338,7 +338,8 @@ struct Gen {
              "  const uint64_t r10 = 512;\n  (void)r10; (void)spriv; (void)shard;\n";
         for (int s : slots) o << "  uint64_t s" << s << " = 0;\n";
         o << "  uint32_t mypc = 0;\n  (void)mypc;\n";
-        std::ostringstream body;
+        std::ostringstream body, dbody;
+        reent_.clear();
         out_ = &body;
         /* uniform copy */
         dmode_ = false;
@@ -347,31 +348,59 @@ struct Gen {
             for (uint32_t i = b; i < e; i++) insn(im[i], i);
             if (e > b && !ends_block(im[e - 1])) goto_next(e);
         }
-        /* min-PC copy */
+        /* min-PC copy (emitted first: it records which pcs a lane's mypc can hold) */
+        out_ = &dbody;
+        dmode_ = true;
+        for (auto [b, e] : blocks) {
+            cur_block_ = b;
+            dbody << "  case " << b << ": D" << b << ": {\n";
+            for (uint32_t i = b; i < e; i++) insn(im[i], i);
+            if (e > b && !ends_block(im[e - 1])) goto_next(e);
+            dbody << "  }\n";
+        }
+        dmode_ = false;
+        out_ = &body;
+        /* the re-entry / dispatch switches list only the pcs mypc can hold: the targets and
+         * fall-throughs of conditional branches and backward jumps; forward unconditional
+         * transitions in the min-PC copy go straight to the next block (same lanes, same exec), so
+         * blocks reached only that way stay single-predecessor code the compiler can merge */
+        reent_.insert(0);
         body << " DIV:\n  for (;;) {\n"
                 "  const uint32_t pc_ = __reduce_min_sync(active, mypc);\n"
                 "  if (pc_ == 0xFFFFFFFFu) return;\n"
                 "  const unsigned exec = __ballot_sync(active, mypc == pc_);\n"
                 "  const unsigned live = __ballot_sync(active, mypc != 0xFFFFFFFFu);\n"
                 "  if (exec == live && (!FULL || live == GX_ALL)) {\n    if (mypc == 0xFFFFFFFFu) return;\n    active = FULL ? GX_ALL : live;\n    switch (pc_) {\n";
-        for (auto [b, e] : blocks) body << "    case " << b << ": goto U" << b << ";\n";
+        for (auto [b, e] : blocks)
+            if (reent_.count(b)) body << "    case " << b << ": goto U" << b << ";\n";
         body << "    default: return;\n    }\n  }\n  if (mypc != pc_) continue;\n  switch (pc_) {\n";
-        dmode_ = true;
-        for (auto [b, e] : blocks) {
-            body << "  case " << b << ": {\n";
-            for (uint32_t i = b; i < e; i++) insn(im[i], i);
-            if (e > b && !ends_block(im[e - 1])) goto_next(e);
-            body << "  }\n";
-        }
+        std::string ds = dbody.str();
+        /* drop the case labels no mypc value can select (their D<b> labels stay as goto targets) */
+        for (auto [b, e] : blocks)
+            if (!reent_.count(b)) {
+                const std::string cl = "  case " + std::to_string(b) + ": D" + std::to_string(b) + ":";
+                const size_t at = ds.find(cl);
+                if (at != std::string::npos) ds.replace(at, cl.size(), "  D" + std::to_string(b) + ":");
+            }
+        body << ds;
         body << "  default: mypc = 0xFFFFFFFFu; continue;\n  }\n  }\n";
-        dmode_ = false;
         o << body.str();
         o << "}\n\n";
     }
 
+    std::set<uint32_t> reent_; /* pcs a lane's mypc can hold (min-PC re-entry points) */
+    uint32_t cur_block_ = 0;
     void goto_next(uint32_t t) {
-        if (dmode_) st("mypc = " + std::to_string(t) + "u; continue;");
-        else st("goto U" + std::to_string(t) + ";");
+        if (dmode_) {
+            if (t > cur_block_) {
+                st("goto D" + std::to_string(t) + ";");
+            } else {
+                reent_.insert(t);
+                st("mypc = " + std::to_string(t) + "u; continue;");
+            }
+        } else {
+            st("goto U" + std::to_string(t) + ";");
+        }
     }
     /* a conditional branch.  `uni`: the verifier's divergence analysis proved the condition warp-
      * uniform (GXF_UNIFORM: every lane that reaches the branch together takes it the same way), so
@@ -379,6 +408,8 @@ struct Gen {
      * counts any split of such a branch in the divergent_steps stat (tests: it must stay 0). */
     void branch(const std::string &cond, uint32_t t, uint32_t nx, bool uni = false) {
         if (dmode_) {
+            reent_.insert(t);
+            reent_.insert(nx);
             st("mypc = (" + cond + ") ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; continue;");
             return;
         }
@@ -392,6 +423,8 @@ struct Gen {
             st("  if (tb_ != active && tb_ != 0 && (threadIdx.x & 31) == (unsigned)(__ffs(active) - 1)) "
                "atomicAdd((unsigned long long *)" + hex(L.stats) + " + " + std::to_string(GXS_DIVERGENT) + ", 1ull);");
         st("  if (tb_ == active) goto U" + std::to_string(t) + "; if (tb_ == 0) goto U" + std::to_string(nx) + ";");
+        reent_.insert(t);
+        reent_.insert(nx);
         st("  mypc = t_ ? " + std::to_string(t) + "u : " + std::to_string(nx) + "u; goto DIV; }");
     }
     void exit_lanes(const std::string &val) {
@@ -429,6 +462,10 @@ struct Gen {
             }
             if (opc) {
                 me(d + " = (uint64_t)(uint32_t)(" + a + " " + opc + " " + b + ");");
+                return;
+            }
+            if (g.op == GX_MOV64) {
+                me(d + " = (uint64_t)" + b + ";");
                 return;
             }
             if (g.op == GX_DIV64 || g.op == GX_MOD64) {

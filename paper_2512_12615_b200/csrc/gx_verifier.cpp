@@ -1018,6 +1018,10 @@ struct Verifier {
             }
             if (op == 0xB0 && r.off == 0) { /* MOV */
                 if (!is64 && is_ptr(src)) return fail(pc, GX_PTR_LEAK, "32-bit move of a pointer") ? 0 : -1;
+                if (is64) { /* narrow: a scalar below 2^32 (the JIT zero-extends explicitly) */
+                    Fact &f = facts[pc];
+                    f.narrow = (f.narrow != 2 && src.type == SCALAR && src.var.umax < (1ull << 32)) ? 1 : 2;
+                }
                 D = src;
                 if (!is64) D.var = sc_trunc32(D.var);
                 P.pc++;
