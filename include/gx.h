@@ -129,6 +129,9 @@ typedef struct {
     uint64_t ringbuf_drops;    /* ringbuf_output calls dropped (-EAGAIN) */
     uint64_t hash_full;        /* hash inserts refused because max_entries was reached */
     uint64_t warp_steps;       /* interpreted warp-instructions (all paths; 0 for the JIT engine) */
+    uint64_t bounds_violations; /* GX_JIT_BOUNDS=1 (debug mode of the JIT engine): map accesses whose
+                                   address fell outside their map -- redirected to a scratch word and
+                                   counted instead of executed (0 in the default mode) */
 } gx_batch_stats;
 
 /* ---------------------------------------------------------------- runtime */

@@ -61,7 +61,8 @@ class gx_verify_report(C.Structure):
 
 class gx_batch_stats(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("events_run", "events_skipped", "divergent_steps", "helper_errors",
-                                          "ringbuf_bytes", "ringbuf_drops", "hash_full", "warp_steps")]
+                                          "ringbuf_bytes", "ringbuf_drops", "hash_full", "warp_steps",
+                                          "bounds_violations")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

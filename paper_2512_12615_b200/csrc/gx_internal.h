@@ -133,6 +133,9 @@ struct GxPublishItem {
     uint32_t nshards;
 };
 
-enum { GXS_RUN = 0, GXS_SKIP, GXS_DIVERGENT, GXS_HERR, GXS_RB_BYTES, GXS_RB_DROPS, GXS_HFULL, GXS_STEPS };
+enum { GXS_RUN = 0, GXS_SKIP, GXS_DIVERGENT, GXS_HERR, GXS_RB_BYTES, GXS_RB_DROPS, GXS_HFULL, GXS_STEPS,
+       GXS_BOUNDS,             /* GX_JIT_BOUNDS=1: map accesses outside their map (redirected, counted) */
+       GXS_SCRATCH = 15,       /* where a redirected access lands */
+       GXS_N = 16 };
 
 #endif

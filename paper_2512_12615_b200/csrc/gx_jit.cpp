@@ -104,10 +104,14 @@ struct Gen {
      * span fits 32-bit index arithmetic */
     std::string ptp(int fd, const std::string &logical) {
         const GxMapDesc &d = L.maps[fd];
+        std::string e;
         if ((uint64_t)d.max_entries * d.value_size < (1ull << 31))
-            return "pt_phys_c<" + std::to_string(d.max_entries) + "u, " + std::to_string(d.value_size / 8) + "u>(" +
-                   hex(d.data) + ", " + logical + ", shard)";
-        return "gxd::pt_phys(" + md(fd) + ", " + logical + ", shard)";
+            e = "pt_phys_c<" + std::to_string(d.max_entries) + "u, " + std::to_string(d.value_size / 8) + "u>(" +
+                hex(d.data) + ", " + logical + ", shard)";
+        else
+            e = "gxd::pt_phys(" + md(fd) + ", " + logical + ", shard)";
+        if (bounds_) e = "(uint8_t *)" + ck("(uint64_t)" + e, 1, fd); /* the physical word within the shards */
+        return e;
     }
     static std::string slot(int addr) { return "s" + std::to_string(addr >> 3); }
 
@@ -224,6 +228,45 @@ struct Gen {
     uint32_t hc_n_ = 0;
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     int pkc_fd_ = -1;    /* the per-thread map held in the register key cache (GX_JIT_PTKC), or -1 */
+    bool bounds_ = false; /* GX_JIT_BOUNDS=1: every map access checked against its map (debug mode) */
+    /* [lo, hi) of a map's device allocation (per-thread maps: the physical shard array) */
+    void map_range(int fd, uint64_t &lo, uint64_t &hi) const {
+        const GxMapDesc &d = L.maps[fd];
+        lo = d.data;
+        uint64_t bytes = 0;
+        switch (d.type) {
+        case 2: bytes = (uint64_t)d.max_entries * d.value_size; break;                  /* ARRAY */
+        case 6: bytes = (uint64_t)d.max_entries * d.value_size * d.nshards; break;      /* PERTHREAD */
+        case 1: bytes = ((uint64_t)d.cap_mask + 1 + 2) * 16; break;                      /* HASH keys + values */
+        default: bytes = 0;
+        }
+        /* GX_JIT_BOUNDS=2: the checked ranges halved -- the checker's own self-test (accesses to the
+         * upper halves of the maps must then be counted) */
+        if (getenv("GX_JIT_BOUNDS") && atoi(getenv("GX_JIT_BOUNDS")) == 2) bytes /= 2;
+        hi = lo + bytes;
+    }
+    /* a checked address expression (unchanged when the mode is off) */
+    std::string ck(const std::string &addr, unsigned size, int fd) const {
+        if (!bounds_) return addr;
+        uint64_t lo = 0, hi = 0;
+        if (fd >= 0) map_range(fd, lo, hi);
+        if (fd < 0 || hi == lo)
+            return "gx_chk_any((uint64_t)(" + addr + "), " + std::to_string(size) + "u)";
+        return "gx_chk((uint64_t)(" + addr + "), " + std::to_string(size) + "u, " + hex(lo) + ", " + hex(hi) + ", " +
+               "(unsigned long long *)" + hex(L.stats) + ")";
+    }
+    /* gx_chk_any: inside some map of the launch (helper arguments through map-value pointers) */
+    void emit_chk_any() {
+        o << "__device__ __forceinline__ uint64_t gx_chk_any(uint64_t a, uint32_t size) {\n";
+        for (int m = 0; m < GX_MAX_MAPS; m++) {
+            uint64_t lo, hi;
+            if (!L.maps[m].data) continue;
+            map_range(m, lo, hi);
+            if (hi > lo) o << "  if (a >= " << hex(lo) << " && a < " << hex(hi) << ") return gx_chk(a, size, " << hex(lo) << ", "
+                           << hex(hi) << ", (unsigned long long *)" << hex(L.stats) << ");\n";
+        }
+        o << "  return gx_chk(a, size, 0, 0, (unsigned long long *)" << hex(L.stats) << ");\n}\n";
+    }
     /* the per-thread key cache's access forms: key from the value-start pointer, constant word */
     std::string pkc_key(const std::string &ptr) const {
         const GxMapDesc &d = L.maps[pkc_fd_];
@@ -239,6 +282,9 @@ struct Gen {
     void pick_pkc(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
         pkc_fd_ = -1;
         if (getenv("GX_JIT_PTKC") && atoi(getenv("GX_JIT_PTKC")) == 0) return;
+        /* single-program launches only: in an attach-table launch the cached words stay live across
+         * every program's code (C5: 4 % slower with the cache, C2: 14 % faster; profiles/r2_ptkc.md) */
+        if (images.size() != 1 && !(getenv("GX_JIT_PTKC") && atoi(getenv("GX_JIT_PTKC")) == 2)) return;
         std::map<int, int> hits;
         std::set<int> bad;
         bool mapv_helper = false;
@@ -542,8 +588,8 @@ struct Gen {
             break;
         case GX_LDX_MAP: {
             const bool coh = L.maps[g.imm].coherent;
-            me(d + " = " + ld_fix(std::string("gload<") + (coh ? "true" : "false") + ">(" + s + " + (int64_t)" +
-                                  std::to_string(g.off) + ", " + std::to_string(lg) + ")") + ";");
+            me(d + " = " + ld_fix(std::string("gload<") + (coh ? "true" : "false") + ">(" +
+                                  ck(s + " + (int64_t)" + std::to_string(g.off), 1u << lg, (int)g.imm) + ", " + std::to_string(lg) + ")") + ";");
             break;
         }
         case GX_LDX_PT:
@@ -564,7 +610,7 @@ struct Gen {
         }
         case GX_ST_MAP: {
             const std::string v = (g.flags & GXF_X) ? s : hex(g.imm);
-            me("gstore(" + d + " + (int64_t)" + std::to_string(g.off) + ", " + std::to_string(lg) + ", " + v + ");");
+            me("gstore(" + ck(d + " + (int64_t)" + std::to_string(g.off), 1u << lg, -1) + ", " + std::to_string(lg) + ", " + v + ");");
             break;
         }
         case GX_ST_PT: {
@@ -584,7 +630,7 @@ struct Gen {
             const GxMapDesc &m = L.maps[g.aux];
             if (g.op == GX_CALL_LOOKUP_HASH) {
                 std::string key = (g.flags & GXF_KEY_MAPV)
-                                      ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
+                                      ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)" + ck("r2", 4, -1) : "*(const uint64_t *)" + ck("r2", 8, -1))
                                       : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
                 if ((int)g.aux == hc_map_)
@@ -595,7 +641,7 @@ struct Gen {
                        M() + "); }");
             } else {
                 const std::string key = (g.flags & GXF_KEY_MAPV)
-                                            ? "*(const uint32_t *)r2"
+                                            ? "*(const uint32_t *)" + ck("r2", 4, -1)
                                             : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
                 if (g.flags & GXF_SX) /* key below max_entries on every path (verifier): never NULL */
                     me("const uint32_t k = " + key + "; r0 = " + hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u;");
@@ -610,7 +656,7 @@ struct Gen {
         case GX_CALL_UPDATE_ARRAY: case GX_CALL_UPDATE_PT: {
             const GxMapDesc &m = L.maps[g.aux];
             const std::string key = (g.flags & GXF_KEY_MAPV)
-                                        ? "*(const uint32_t *)r2"
+                                        ? "*(const uint32_t *)" + ck("r2", 4, -1)
                                         : "(uint32_t)(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             std::ostringstream b;
             /* ARRAY: lanes writing the same key keep the sequential result -- the group's last lane's
@@ -621,7 +667,7 @@ struct Gen {
             b << " if (r4 > 2) rc = -22; else if (k >= " << m.max_entries << "u) rc = -7; else if (r4 == 1) rc = -17; else";
             b << (g.op == GX_CALL_UPDATE_ARRAY ? " if ((int)lane == 31 - __clz(kg_)) {" : " {");
             for (uint32_t w = 0; w < m.value_size / 8; w++) {
-                const std::string v = (g.flags & GXF_VAL_MAPV) ? "((const uint64_t *)r3)[" + std::to_string(w) + "]"
+                const std::string v = (g.flags & GXF_VAL_MAPV) ? "((const uint64_t *)" + ck("r3", 8, -1) + ")[" + std::to_string(w) + "]"
                                                                : "s" + std::to_string((uint32_t)g.imm / 8 + w);
                 const std::string logical = hex(m.data) + " + (uint64_t)k * " + std::to_string(m.value_size) + "u + " +
                                             std::to_string(8 * w);
@@ -637,10 +683,10 @@ struct Gen {
         case GX_CALL_UPDATE_HASH: {
             const GxMapDesc &m = L.maps[g.aux];
             std::string key = (g.flags & GXF_KEY_MAPV)
-                                  ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)r2" : "*(const uint64_t *)r2")
+                                  ? (m.key_size == 4 ? "(uint64_t)*(const uint32_t *)" + ck("r2", 4, -1) : "*(const uint64_t *)" + ck("r2", 8, -1))
                                   : "(" + slot(g.off) + " >> " + std::to_string(8 * (g.off & 7)) + ")";
             if (m.key_size == 4) key = "(" + key + " & 0xFFFFFFFFull)";
-            const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)r3" : "s" + std::to_string((uint32_t)g.imm / 8);
+            const std::string v = (g.flags & GXF_VAL_MAPV) ? "*(const uint64_t *)" + ck("r3", 8, -1) : "s" + std::to_string((uint32_t)g.imm / 8);
             st("{ const uint64_t k_ = " + key + ", v_ = " + v + ";");
             st("  const int64_t rc = gxd::hash_update_coop(" + md(g.aux) + ", k_, v_, r4, true, " + M() + ");");
             st("  if (rc) c_herr++; if (rc == -7) c_hfull++; r0 = (uint64_t)rc; }");
@@ -661,7 +707,7 @@ struct Gen {
             }
             std::ostringstream b;
             b << "{ ";
-            if (g.flags & GXF_VAL_MAPV) b << "const uint64_t *w = (const uint64_t *)r2;";
+            if (g.flags & GXF_VAL_MAPV) b << "const uint64_t *w = (const uint64_t *)" << ck("r2", 8, -1) << ";";
             else {
                 b << "const uint64_t w[" << (size + 7) / 8 << "] = {";
                 for (uint32_t k = 0; k < (size + 7) / 8; k++) b << (k ? ", " : "") << "s" << ((uint16_t)g.off / 8 + k);
@@ -732,7 +778,8 @@ struct Gen {
             return;
         }
         const int fd = g.aux >> 4;
-        const std::string addr = R(g.dst) + " + (int64_t)" + std::to_string(g.off);
+        const std::string addr = g.op == GX_ATOM_MAP ? ck(R(g.dst) + " + (int64_t)" + std::to_string(g.off), w32 ? 4u : 8u, fd)
+                                                     : R(g.dst) + " + (int64_t)" + std::to_string(g.off);
         if (g.op == GX_ATOM_PT && fd == pkc_fd_) {
             std::string e = "rmw_word(pkc.v[" + std::to_string(g.off >> 3) + "], " + std::to_string(g.off & 7) + ", " +
                             (w32 ? "true" : "false") + ", " + std::to_string(op) + "u, " + v + ", r0)";
@@ -788,6 +835,7 @@ struct Gen {
         const int minb = getenv("GX_JIT_MINB") ? atoi(getenv("GX_JIT_MINB")) : 1;
         const bool punroll = !getenv("GX_JIT_PUNROLL") || atoi(getenv("GX_JIT_PUNROLL")) != 0;
         ptc_ = getenv("GX_JIT_PTCACHE") && atoi(getenv("GX_JIT_PTCACHE")) != 0;
+        bounds_ = getenv("GX_JIT_BOUNDS") && atoi(getenv("GX_JIT_BOUNDS")) != 0;
         ifconv_on_ = !getenv("GX_JIT_IFCONV") || atoi(getenv("GX_JIT_IFCONV")) != 0;
         if (const char *e = getenv("GX_JIT_WAIT_HINT")) o << "#define GX_WAIT_HINT " << atoi(e) << "\n";
         if (const char *e = getenv("GX_JIT_HASH_L1PROBE")) o << "#define GX_HASH_L1PROBE " << atoi(e) << "\n";
@@ -799,6 +847,10 @@ struct Gen {
         if (const char *e = getenv("GX_JIT_PT_HINT")) o << "#define GX_PT_HINT " << atoi(e) << "\n";
         o << "#include \"gx_jit_rt.cuh\"\nusing namespace gxj;\n\n";
         pick_pkc(images, sizes);
+        if (bounds_) {
+            pkc_fd_ = -1;  /* every per-thread access through the checked physical address */
+            emit_chk_any();
+        }
         if (pkc_fd_ >= 0)
             o << "typedef PtKc<" << L.maps[pkc_fd_].max_entries << "u, " << L.maps[pkc_fd_].value_size / 8 << "u> GxPkc;\n";
         else

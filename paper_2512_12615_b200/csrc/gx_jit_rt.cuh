@@ -553,6 +553,15 @@ __device__ __forceinline__ uint8_t *pt_phys_c(uint64_t data, uint64_t logical, u
     return reinterpret_cast<uint8_t *>(base + (uint64_t)(((kk * W + w) << 8) | (lo & 7)));
 }
 
+/* GX_JIT_BOUNDS=1 (debug mode; SURVEY.md §5 "bounds checks of our own"): an access of `size` bytes
+ * at a must lie in [lo, hi) and be naturally aligned; otherwise it is counted in stats[GXS_BOUNDS]
+ * and redirected to stats[GXS_SCRATCH] so that nothing faults */
+__device__ __forceinline__ uint64_t gx_chk(uint64_t a, uint32_t size, uint64_t lo, uint64_t hi, unsigned long long *stats) {
+    if (a >= lo && a < hi && size <= hi - a && (a & (size - 1)) == 0) return a;
+    atomicAdd(&stats[GXS_BOUNDS], 1ull);
+    return reinterpret_cast<uint64_t>(&stats[GXS_SCRATCH]);
+}
+
 /* Per-thread key cache (GX_JIT_PTKC): ONE per-thread map of K entries x W words, one key at a time,
  * its W value words held in registers.  Every access to that map goes through a value-start pointer
  * (verifier GXF_PT_VSTART), so the key is (pointer - data) / (8 W) and the word is the access's

@@ -703,8 +703,8 @@ int gx_open(int cuda_device, gx_rt **out) {
     if (const char *e = getenv("GX_ENGINE")) rt->engine = strcmp(e, "interp") == 0 ? GX_ENGINE_INTERP : GX_ENGINE_JIT;
     for (auto &row : rt->attach)
         for (int &x : row) x = -1;
-    if (cudaMalloc(&rt->d_stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(rt->d_stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (cudaMalloc(&rt->d_stats, GXS_N * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(rt->d_stats, 0, GXS_N * sizeof(unsigned long long)) != cudaSuccess) {
         delete rt;
         return -ENOMEM;
     }
@@ -1672,7 +1672,7 @@ int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
     if (!rt || !out) return -EINVAL;
     int rc0 = sync(rt);
     if (rc0) return rc0;
-    unsigned long long h[8];
+    unsigned long long h[GXS_N];
     CK(cudaMemcpy(h, rt->d_stats, sizeof h, cudaMemcpyDeviceToHost), "stats");
     CK(cudaMemset(rt->d_stats, 0, sizeof h), "stats reset");
     out->events_run = h[GXS_RUN];
@@ -1683,6 +1683,7 @@ int gx_get_stats(gx_rt *rt, gx_batch_stats *out) {
     out->ringbuf_drops = h[GXS_RB_DROPS];
     out->hash_full = h[GXS_HFULL];
     out->warp_steps = h[GXS_STEPS];
+    out->bounds_violations = h[GXS_BOUNDS];
     return 0;
 }
 
