@@ -228,6 +228,16 @@ struct Gen {
     uint32_t hc_n_ = 0;
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     int pkc_fd_ = -1;    /* the per-thread map held in the register key cache (GX_JIT_PTKC), or -1 */
+    std::vector<const uint16_t *> nin_; /* per program: registers narrow on entry to each slot (verifier) */
+    const uint16_t *cur_nin_ = nullptr;
+    /* at a block start: re-state the registers the verifier proved below 2^32 there, so that the
+     * compiler knows their upper halves are zero across loop back-edges and joins */
+    void narrow_entry(uint32_t b) {
+        if (!cur_nin_ || (getenv("GX_JIT_NARROW") && atoi(getenv("GX_JIT_NARROW")) == 0)) return;
+        const uint16_t m = cur_nin_[b];
+        for (int k = 0; k < 10; k++)
+            if ((m >> k) & 1) (*out_) << "  " << R(k) << " = (uint64_t)(uint32_t)" << R(k) << ";\n";
+    }
     bool bounds_ = false; /* GX_JIT_BOUNDS=1: every map access checked against its map (debug mode) */
     /* [lo, hi) of a map's device allocation (per-thread maps: the physical shard array) */
     void map_range(int fd, uint64_t &lo, uint64_t &hi) const {
@@ -329,6 +339,7 @@ struct Gen {
      * all 32 lanes are live again -- so every uniform-copy collective compiles without the
      * runtime-mask convergence checks (REDUX.OR + BRA.DIV per collective, profiles/r1_ncu_c2_jit.md). */
     void program(int q, const GxInsn *im0, uint32_t n) {
+        cur_nin_ = (size_t)q < nin_.size() ? nin_[q] : nullptr;
         std::set<uint32_t> targets, leaders{0};
         std::map<uint32_t, int> tcount;
         for (uint32_t i = 0; i < n; i++) {
@@ -391,6 +402,7 @@ struct Gen {
         dmode_ = false;
         for (auto [b, e] : blocks) {
             body << " U" << b << ":\n";
+            if (b) narrow_entry(b);
             for (uint32_t i = b; i < e; i++) insn(im[i], i);
             if (e > b && !ends_block(im[e - 1])) goto_next(e);
         }
@@ -400,6 +412,7 @@ struct Gen {
         for (auto [b, e] : blocks) {
             cur_block_ = b;
             dbody << "  case " << b << ": D" << b << ": {\n";
+            if (b) narrow_entry(b);
             for (uint32_t i = b; i < e; i++) insn(im[i], i);
             if (e > b && !ends_block(im[e - 1])) goto_next(e);
             dbody << "  }\n";
@@ -1287,8 +1300,9 @@ const char *gx_jit_kernel_name(int variant) {
 }
 
 std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes,
-                          int block, unsigned vmask) {
+                          int block, unsigned vmask, const std::vector<const uint16_t *> *narrow_in) {
     Gen g(L);
+    if (narrow_in && narrow_in->size() == images.size()) g.nin_ = *narrow_in;
     g.kernel(images, sizes, block, vmask);
     return g.o.str();
 }

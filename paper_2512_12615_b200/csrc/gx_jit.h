@@ -12,7 +12,8 @@ const char *gx_jit_kernel_name(int variant);
 /* CUDA C++ source of one launch configuration (programs in launch-slot order), the kernels of
  * the variants in `vmask` only. */
 std::string gx_jit_source(const GxLaunch &L, const std::vector<const GxInsn *> &images,
-                          const std::vector<uint32_t> &sizes, int block, unsigned vmask = GX_JIT_V_ALL);
+                          const std::vector<uint32_t> &sizes, int block, unsigned vmask = GX_JIT_V_ALL,
+                          const std::vector<const uint16_t *> *narrow_in = nullptr);
 /* f4: CUDA C++ of the program as inline __device__ hooks (gx_hook_access / gx_hook_block_enter)
  * followed by the user's kernels; no privatised maps (L must have none). */
 std::string gx_jit_instrument_source(const GxLaunch &L, const GxInsn *image, uint32_t n, const std::string &user);

@@ -410,16 +410,19 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
     auto t0 = std::chrono::steady_clock::now();
     std::vector<const GxInsn *> images;
     std::vector<uint32_t> sizes;
+    std::vector<const uint16_t *> nin;
     for (int q : cfg.progs) {
-        images.push_back(rt->progs[q].vr.image.data());
-        sizes.push_back((uint32_t)rt->progs[q].vr.image.size());
+        const GxVerifyResult &vr = rt->progs[q].vr;
+        images.push_back(vr.image.data());
+        sizes.push_back((uint32_t)vr.image.size());
+        nin.push_back(vr.narrow_in.size() == vr.image.size() ? vr.narrow_in.data() : nullptr);
     }
     const bool ring = k < 2;
     /* fewer, larger blocks keep the per-block privatised-shard flush small; one 1024-thread block
      * per SM measured fastest on every config (profiles/r1_jit_variants.md); 256-thread blocks only
      * if the 1024-thread kernel cannot be resident at all */
     for (int B : {gx_jit_block(), 256}) {
-        std::string src = gx_jit_source(cfg.h, images, sizes, B, 1u << k);
+        std::string src = gx_jit_source(cfg.h, images, sizes, B, 1u << k, &nin);
         if (const char *dump = getenv("GX_JIT_DUMP")) {
             if (FILE *f = fopen(dump, "w")) {
                 fputs(src.c_str(), f);
@@ -1122,9 +1125,10 @@ int gx_jit_offline(const void *insn_slots, uint32_t n_slots, const gx_map_spec *
     h.single = 0;
     std::vector<const GxInsn *> images{vr.image.data()};
     std::vector<uint32_t> sizes{(uint32_t)vr.image.size()};
+    std::vector<const uint16_t *> nin{vr.narrow_in.size() == vr.image.size() ? vr.narrow_in.data() : nullptr};
     unsigned vmask = GX_JIT_V_ALL; /* GX_JIT_VMASK: the launch variants to generate (GX_JIT_V_* bits) */
     if (const char *e = getenv("GX_JIT_VMASK")) vmask = (unsigned)strtoul(e, nullptr, 0) & GX_JIT_V_ALL;
-    std::string s = gx_jit_source(h, images, sizes, gx_jit_block(), vmask ? vmask : GX_JIT_V_ALL);
+    std::string s = gx_jit_source(h, images, sizes, gx_jit_block(), vmask ? vmask : GX_JIT_V_ALL, &nin);
     if (src && src_len) {
         size_t k = std::min<size_t>(src_len - 1, s.size());
         memcpy(src, s.data(), k);

@@ -499,6 +499,8 @@ struct Fact {
     bool pt_vstart = false;      /* PTV memory insns: the base register is a value start (no offset) on every path */
     uint8_t narrow = 0;          /* scalar ALU64: 1 = operands and result below 2^32 on every path, 2 = not */
     uint8_t inrange = 0;         /* ARRAY / PERTHREAD lookups: 1 = key below max_entries on every path, 2 = not */
+    bool nin_seen = false;
+    uint16_t nin = 0;            /* registers r0..r9 that are scalars below 2^32 on entry, every path */
 };
 
 struct Checkpoint {
@@ -982,6 +984,14 @@ struct Verifier {
     int step(Path &P, std::vector<Path> &pending) {
         uint32_t pc = P.pc;
         State &st = P.st;
+        {
+            uint16_t m = 0;
+            for (int k = 0; k < 10; k++)
+                if (st.r[k].type == SCALAR && st.r[k].var.umax < (1ull << 32)) m |= (uint16_t)(1u << k);
+            Fact &fn = facts[pc];
+            fn.nin = fn.nin_seen ? (uint16_t)(fn.nin & m) : m;
+            fn.nin_seen = true;
+        }
         const Raw &r = ins[pc];
         uint32_t cls = r.code & 7, op = r.code & 0xF0;
         bool x = r.code & 0x08;
@@ -2308,6 +2318,12 @@ struct Verifier {
         map[N] = np;
         std::vector<GxInsn> c;
         c.reserve(np);
+        /* the narrow-register set of a compacted slot: the state before the first original slot
+         * mapped onto it (removed slots before a survivor never execute) */
+        std::vector<uint16_t> nin(np + 1, 0);
+        for (int i = (int)N - 1; i >= 0; i--)
+            if (!is_second[i] && map[i] < np + 1) nin[map[i]] = facts[i].nin_seen ? facts[i].nin : 0;
+        out.narrow_in.assign(nin.begin(), nin.begin() + np);
         for (uint32_t i = 0; i < N; i++) {
             if (removed[i]) continue;
             GxInsn g = im[i];

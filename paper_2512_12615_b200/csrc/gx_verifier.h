@@ -39,6 +39,9 @@ struct GxVerifyResult {
     gx_verify_report report{};
     std::string log;
     std::vector<GxInsn> image;     /* pre-decoded program (same slot count) */
+    std::vector<uint16_t> narrow_in; /* per image slot: registers r0..r9 holding a scalar below 2^32 on
+                                        entry on every explored path (the JIT zero-extends them at
+                                        block starts so the compiler keeps their upper halves known) */
     GxMapUse use[GX_MAX_MAPS];
     uint32_t stack_depth = 0;
 };
