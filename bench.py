@@ -557,6 +557,28 @@ def c1_measure(device):
                 stream.synchronize()
                 steady[overlap] = a.elapsed_time(b2) / 500
                 del g
+            # the single-launch floor, timed the same way over the same rotating batches: a program that
+            # only reads each event's addr (the whole 32-B sector streams from HBM), and a plain torch
+            # reduction over the batch bytes -- what one launch of any kernel reading 32 MiB costs here
+            floors = {}
+            rt_floor = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
+            from gxin import asm
+            pf = rt_floor.load_prog(asm.assemble("ldxdw r0, [r1+0]\nexit", {}))
+            for name, fn in (("read_only_program", lambda b: rt_floor.run(b, pf, stream=stream)),
+                             ("torch_sum", lambda b: b.view(torch.int64).sum())):
+                for k in range(2 * nb):
+                    fn(bufs[k % nb])
+                stream.synchronize()
+                ts = []
+                for k in range(5 * nb):
+                    a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    fn(bufs[k % nb])
+                    b2.record(stream)
+                    ts.append((a, b2))
+                stream.synchronize()
+                floors[name] = float(np.median([a.elapsed_time(b2) for a, b2 in ts])) * 1e3
+            rt_floor.close()
         counts = rt.array_u64(s.fds[(0, "counts")])
         runs = 3 * nb + 5 * nb + 2 * (100 + 500)
         assert int(counts.sum()) == runs * n, "counter total != events (north star invariant)"
@@ -567,6 +589,8 @@ def c1_measure(device):
                        "steady_hbm_frac": bw(steady[False]) / peaks["hbm_gbs"],
                        "steady_pdl_us": steady[True] * 1e3, "steady_pdl_events_per_s": n / (steady[True] / 1e3),
                        "steady_pdl_hbm_frac": bw(steady[True]) / peaks["hbm_gbs"], "counter_total_ok": True,
+                       "single_launch_floor_us": floors,
+                       "single_vs_floor": min(floors.values()) / (single * 1e3),
                        "flush": "8 rotating 32-MiB batches (256 MiB > L2)"}
         rt.close()
         del bufs
