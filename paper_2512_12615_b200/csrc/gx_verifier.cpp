@@ -2318,11 +2318,14 @@ struct Verifier {
         map[N] = np;
         std::vector<GxInsn> c;
         c.reserve(np);
-        /* the narrow-register set of a compacted slot: the state before the first original slot
-         * mapped onto it (removed slots before a survivor never execute) */
+        /* the narrow-register set of a compacted slot: the entry state of its surviving original
+         * slot.  (Not that of a removed slot mapped onto it: one removed from the end of the
+         * preceding block lies on the fall-through path only -- the fuzz caught a join taking a
+         * predecessor's narrower state.  Removed slots define dead registers only, so the survivor's
+         * state holds for every live register on every way in.) */
         std::vector<uint16_t> nin(np + 1, 0);
-        for (int i = (int)N - 1; i >= 0; i--)
-            if (!is_second[i] && map[i] < np + 1) nin[map[i]] = facts[i].nin_seen ? facts[i].nin : 0;
+        for (uint32_t i = 0; i < N; i++)
+            if (!removed[i]) nin[map[i]] = facts[i].nin_seen ? facts[i].nin : 0;
         out.narrow_in.assign(nin.begin(), nin.begin() + np);
         for (uint32_t i = 0; i < N; i++) {
             if (removed[i]) continue;
