@@ -72,7 +72,8 @@ enum { GX_FN_MEM_PREFETCH = 1000 };
 enum { GX_FN_PREFETCH_L2 = 1001 };
 /* hook kinds (event hook word bits 0-7): PAPER.md:225-230 (gdev_mem_ops.access), 260-262
  * (gdev_sched_ops.enter), 303 (fault-style records) */
-enum { GX_HOOK_MEM_ACCESS = 0, GX_HOOK_BLOCK_ENTER = 1, GX_HOOK_FAULT = 2 };
+enum { GX_HOOK_MEM_ACCESS = 0, GX_HOOK_BLOCK_ENTER = 1, GX_HOOK_FAULT = 2,
+       GX_HOOK_FENCE = 3 /* gdev_mem_ops.fence: f4 gx_hook_fence */ };
 /* update flags, bpf.h:1300-1302 */
 enum { GX_ANY = 0, GX_NOEXIST = 1, GX_EXIST = 2 };
 
@@ -174,6 +175,7 @@ int  gx_prefetch_drain(gx_rt *rt, int map_fd, uint64_t *reqs, uint64_t cap, uint
  * together with user_src (CUDA C++ with extern "C" __global__ kernels) in one NVRTC sm_100a module:
  *     uint64_t gx_hook_access(unsigned group, const void *addr, uint32_t size, bool is_write);
  *     uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost);
+ *     uint64_t gx_hook_fence(unsigned group, uint64_t scope);                  (kind GX_HOOK_FENCE)
  *     uint64_t gx_hook_probe(unsigned group, uint64_t fn);                     (kind GX_HOOK_PROBE)
  *     uint64_t gx_hook_retprobe(unsigned group, uint64_t fn, uint32_t retval);  (kind GX_HOOK_RETPROBE)
  *     uint64_t gx_hook_event(unsigned group, uint64_t addr, uint32_t hook, uint32_t size,

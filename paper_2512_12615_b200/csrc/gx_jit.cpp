@@ -963,6 +963,10 @@ struct Gen {
              "__device__ __forceinline__ uint64_t gx_hook_block_enter(unsigned group, uint64_t unit, uint32_t cost) {\n"
              "  return gx_hook_event(group, unit, 1u, cost);\n"
              "}\n"
+             "/* memory-fence hook (gdev_mem_ops.fence, PAPER.md:225-230): addr = the caller's scope id */\n"
+             "__device__ __forceinline__ uint64_t gx_hook_fence(unsigned group, uint64_t scope) {\n"
+             "  return gx_hook_event(group, scope, 3u, 0u);\n"
+             "}\n"
              "/* device-function entry / return hooks (gdev_sched_ops.probe / .retprobe, PAPER.md:265-267):\n"
              " * addr = the caller's function id, size = the low 32 bits of the return value (retprobe) */\n"
              "__device__ __forceinline__ uint64_t gx_hook_probe(unsigned group, uint64_t fn) {\n"
