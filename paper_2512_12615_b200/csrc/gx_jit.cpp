@@ -519,6 +519,13 @@ struct Gen {
             case GX_RSH64: opc = ">>"; break;
             default: break;
             }
+            if (g.op == GX_RSH64) {
+                /* a 32-bit shift the compiler cannot re-widen (it otherwise folds a preceding narrow
+                 * add into a 64-bit add + funnel shift to keep the carry bit it then masks off) */
+                me("{ uint32_t t_; asm(\"shr.b32 %0, %1, %2;\" : \"=r\"(t_) : \"r\"(" + a + "), \"r\"((uint32_t)(" + b +
+                   "))); " + d + " = (uint64_t)t_; }");
+                return;
+            }
             if (opc) {
                 me(d + " = (uint64_t)(uint32_t)(" + a + " " + opc + " " + b + ");");
                 return;
