@@ -724,7 +724,7 @@ def f2_l2_line():
     import paper_2512_12615_b200 as gx
     from gxin import asm, instrument
     n = 1 << 28
-    err, buf = cr.cudaMallocManaged(8 * n, cr.cudaMemAttachFlags.cudaMemAttachGlobal)
+    err, buf = cr.cudaMallocManaged(8 * n, cr.cudaMemAttachGlobal)
     if int(err) != 0:
         print(json.dumps({"f2": "l2_uvm", "skipped": f"cudaMallocManaged: {err}"}), file=sys.stderr, flush=True)
         return
@@ -751,8 +751,10 @@ def f2_l2_line():
     k0 = gx.gx_instrument(rt.rt, rt.load_prog(asm.assemble("mov64 r0, 0\nexit")), "#define GX_HOOKS 0\n" + instrument.VADD)
     line["ms_plain"] = timed(k0)
     gx.gx_kernel_free(rt.rt, k0)
+    # the first access of every 64-KiB chunk prefetches one line d ahead (a per-access prefetch
+    # floods the fault handler: measured 4.3x slower than no prefetch at all)
     for dist, ln in ((0, 0), (1 << 20, 128), (4 << 20, 128), (16 << 20, 128)):
-        fds = instrument.setup_l2(rt, region, dist, ln)
+        fds = instrument.setup_l2(rt, region, dist, ln, mask=(64 << 10) - 1)
         k = gx.gx_instrument(rt.rt, rt.load_prog(asm.assemble(instrument.P7_L2_STRIDE, fds)), instrument.VADD)
         key = "ms_hooks_no_prefetch" if ln == 0 else f"ms_l2_dist_{dist >> 20}MiB"
         line[key] = timed(k)

@@ -45,9 +45,11 @@ PI = """
 """
 
 # P7: GPU L2 stride prefetch (Table 1 "GPU L2 Stride Prefetch ... Device"): on an access
-# at addr, prefetch [addr + dist, addr + dist + len) into L2 (gdev_prefetch_l2, helper 1001) with
-# dist and len from cfg (the host side of the policy sets the stride distance); R0 = the helper's
-# result; outcome[0 | 1 | 2] counts issued / -EINVAL / -EFAULT
+# at addr whose bits under cfg.mask are zero (the first access of each mask+1-byte chunk; mask 0 =
+# every access), prefetch [addr + dist, addr + dist + len) into L2 (gdev_prefetch_l2, helper 1001);
+# dist / len / mask from cfg (the host side of the policy sets the stride distance).  R0 = the
+# helper's result (0 when not triggered); outcome[0 | 1 | 2 | 3] counts issued / -EINVAL / -EFAULT /
+# not triggered
 P7_L2_STRIDE = """
     ldxdw r6, [r1+0]          ; addr
     stw [r10-4], 0
@@ -58,6 +60,12 @@ P7_L2_STRIDE = """
     jeq r0, 0, out
     ldxdw r7, [r0+0]          ; dist
     ldxdw r3, [r0+8]          ; len
+    ldxdw r8, [r0+16]         ; trigger mask
+    mov64 r9, 0
+    mov64 r2, 3
+    mov64 r4, r6
+    and64 r4, r8
+    jne r4, 0, count          ; not the first access of its chunk
     mov64 r2, r6
     add64 r2, r7
     lddw r1, map:region
@@ -85,10 +93,10 @@ out:
 """
 
 
-def setup_l2(engine, region_fd, dist, length):
-    """Maps of P7 on `engine` (oracle or runtime) around an existing region map: cfg {dist, len},
-    outcome[3].  Returns the asm symbol table."""
+def setup_l2(engine, region_fd, dist, length, mask=0):
+    """Maps of P7 on `engine` (oracle or runtime) around an existing region map: cfg {dist, len,
+    mask}, outcome[4].  Returns the asm symbol table."""
     ARRAY = 2
-    cfg = engine.create_map(ARRAY, 4, 16, 1)
-    engine.update_map(cfg, (0).to_bytes(4, "little"), int(dist).to_bytes(8, "little") + int(length).to_bytes(8, "little"))
-    return {"region": region_fd, "cfg": cfg, "outcome": engine.create_map(ARRAY, 4, 8, 3)}
+    cfg = engine.create_map(ARRAY, 4, 24, 1)
+    engine.update_map(cfg, (0).to_bytes(4, "little"), b"".join(int(x).to_bytes(8, "little") for x in (dist, length, mask)))
+    return {"region": region_fd, "cfg": cfg, "outcome": engine.create_map(ARRAY, 4, 8, 4)}

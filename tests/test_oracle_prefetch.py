@@ -161,4 +161,24 @@ def test_l2_stride_policy_closed_form():
     inside = (addr + np.uint64(dist + ln)) <= np.uint64(BASE + n * stride)
     want = np.where(inside, 0, 2**64 - 14).astype(np.uint64)
     assert (r0 == want).all()
-    assert env.array_u64(fds["outcome"]).tolist() == [int(inside.sum()), 0, int((~inside).sum())]
+    assert env.array_u64(fds["outcome"]).tolist() == [int(inside.sum()), 0, int((~inside).sum()), 0]
+
+
+def test_l2_stride_policy_trigger_mask():
+    """P7 with a trigger mask: only accesses at a chunk start (addr & mask == 0) prefetch; the others
+    return 0 and are counted as not triggered."""
+    from gxin import instrument
+    from oracle.oracle import Oracle
+    env = Oracle()
+    n, stride, dist, ln, mask = 4096, 256, 8192, 128, 4095
+    reg = env.region_map(BASE, n * stride)
+    fds = instrument.setup_l2(env, reg, dist, ln, mask)
+    addr = BASE + stride * np.arange(n, dtype=np.uint64)
+    r0 = env.run(gen.records(n, addr=addr), env.load_prog(asm.assemble(instrument.P7_L2_STRIDE, fds)))
+    trig = (addr & np.uint64(mask)) == 0
+    inside = (addr + np.uint64(dist + ln)) <= np.uint64(BASE + n * stride)
+    want = np.where(trig & ~inside, 2**64 - 14, 0).astype(np.uint64)
+    assert (r0 == want).all()
+    assert env.array_u64(fds["outcome"]).tolist() == [int((trig & inside).sum()), 0, int((trig & ~inside).sum()),
+                                                      int((~trig).sum())]
+    assert int(trig.sum()) == n * stride // (mask + 1)
