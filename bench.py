@@ -563,7 +563,12 @@ def c1_measure(device):
             floors = {}
             rt_floor = gx.Runtime(device, engine=gx.GX_ENGINE_JIT)
             from gxin import asm
-            pf = rt_floor.load_prog(asm.assemble("ldxdw r0, [r1+0]\nexit", {}))
+            # the addr must stay live (an unused load is dead code to the compiler): a never-taken
+            # (addresses are 8-aligned) branch to a counter update keeps every event's read
+            cfd = rt_floor.create_map(gx.GX_MAP_ARRAY, 4, 8, 1)
+            pf = rt_floor.load_prog(asm.assemble(
+                "ldxdw r2, [r1+0]\njne r2, 1, out\nstw [r10-4], 0\nlddw r1, map:c\nmov64 r2, r10\nadd64 r2, -4\n"
+                "call 1\njeq r0, 0, out\nmov64 r1, 1\natomic_add64 [r0+0], r1\nout:\nmov64 r0, 0\nexit", {"c": cfd}))
             for name, fn in (("read_only_program", lambda b: rt_floor.run(b, pf, stream=stream)),
                              ("torch_sum", lambda b: b.view(torch.int64).sum())):
                 for k in range(2 * nb):

@@ -1261,8 +1261,8 @@ struct Gen {
         for (uint32_t k = 0; k < L.n_priv; k++) {
             const GxMapDesc &m = L.maps[L.priv_maps[k]];
             const uint32_t nw = m.max_entries * m.value_size / 8;
-            o << "  for (uint32_t w = threadIdx.x; w < " << nw << "u; w += " << B << ") {\n"
-              << "    const uint64_t v = (uint64_t)spriv[" << m.priv_off / 4 << " + w] | ((uint64_t)spriv["
+            o << "  for (uint32_t w = threadIdx.x; w < " << nw << "u; w += " << B << ") {\n";
+            o << "    const uint64_t v = (uint64_t)spriv[" << m.priv_off / 4 << " + w] | ((uint64_t)spriv["
               << m.priv_off / 4 + nw << " + w] << 32);\n"
               << "    if (v) atomicAdd((unsigned long long *)" << hex(m.data) << " + w, (unsigned long long)v);\n  }\n";
         }
