@@ -111,6 +111,7 @@ struct LaunchCfg {
         uint32_t grid = 0, block = 256;
     } jv[4];
     bool ring_ok = true;
+    bool jit_failed = false;   /* the JIT could not compile this configuration: interpreter launches */
     std::string jit_log;
     double jit_ms = 0;
 };
@@ -402,6 +403,10 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
     if (V.fn) return 0;
     if (V.tried) return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
     V.tried = true;
+    if (getenv("GX_JIT_INJECT_FAILURE") && atoi(getenv("GX_JIT_INJECT_FAILURE")) != 0) { /* fault injection (tests) */
+        cfg.jit_log = "injected failure (GX_JIT_INJECT_FAILURE)";
+        return set_err(rt, -ENOSYS, "JIT unavailable: %s", cfg.jit_log.c_str());
+    }
     Drv &d = drv();
     if (!d.ok) {
         cfg.jit_log = "driver entry points unavailable";
@@ -608,15 +613,28 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
     if (int rc = order_after_last(rt, stream)) return rc;
     gx_log(3, "batch %llu: %llu events, %s engine, stream %p", (unsigned long long)rt->n_launches, (unsigned long long)n,
            rt->engine == GX_ENGINE_JIT ? "jit" : "interp", (void *)stream);
-    if (rt->engine == GX_ENGINE_JIT) {
+    /* a launch configuration the JIT cannot compile (e.g. an NVRTC resource limit) runs on the
+     * interpreter -- the same semantics on the same GPU -- and says so at GX_LOG_LEVEL 1 */
+    bool jit_ok = rt->engine == GX_ENGINE_JIT && !cfg.jit_failed;
+    int vk = 0;
+    if (jit_ok) {
         if (!cfg.jv[0].tried && !cfg.jv[1].tried && !cfg.jv[2].tried && !cfg.jv[3].tried) {
             uint64_t worst = 0; /* ring_ok before the first compile (jit_prepare sets it too) */
             for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
             cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
         }
-        const int vk = jit_variant(cfg, n, d_ret != nullptr);
+        vk = jit_variant(cfg, n, d_ret != nullptr);
         int rc = jit_prepare(rt, cfg, vk);
-        if (rc) return rc;
+        if (rc == -ENOSYS) {
+            cfg.jit_failed = true;
+            jit_ok = false;
+            gx_log(1, "JIT variant %d unavailable (%s): this launch configuration runs on the interpreter", vk,
+                   rt->err.c_str());
+        } else if (rc) {
+            return rc;
+        }
+    }
+    if (jit_ok) {
         const LaunchCfg::JitVar &V = cfg.jv[vk];
         const void *ev = d_events;
         uint64_t nn = n;

@@ -38,3 +38,26 @@ def test_log_level(gpu, level):
     assert ("[gx:3] batch 0: 4096 events" in err) == (level >= 3)
     if level == 0:
         assert "[gx:" not in err
+
+
+def test_jit_failure_falls_back_to_the_interpreter(gpu, monkeypatch):
+    """A launch configuration the JIT cannot compile runs on the interpreter (same GPU, same
+    semantics): GX_JIT_INJECT_FAILURE makes every compile fail; C3 still matches the oracle and the
+    interpreter's warp steps show it ran."""
+    import numpy as np
+    import torch
+    from gxin import configs
+    from gpu_util import make_runtime, oracle_run, outputs
+    monkeypatch.setenv("GX_JIT_INJECT_FAILURE", "1")
+    n = 4096 + 17
+    ev = configs.events("C3", configs.SEEDS["C3"], n)
+    env, so, r0o = oracle_run("C3", ev, threshold=2)
+    rt = make_runtime("jit")
+    s = configs.setup(rt, "C3", threshold=2)
+    ret = torch.zeros(n, dtype=torch.int64, device="cuda")
+    rt.run(torch.from_numpy(np.ascontiguousarray(ev).view(np.uint8).reshape(-1, 32)).cuda(), s.prog_arg, ret=ret)
+    torch.cuda.synchronize()
+    st = rt.stats()
+    assert (ret.cpu().numpy().view(np.uint64) == r0o).all()
+    assert outputs(rt, s) == outputs(env, so)
+    assert st["warp_steps"] > 0
