@@ -441,12 +441,6 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     else if (me) mypc = npc;
                     continue;
                 }
-                if (in.op == GX_ST_STACK) {
-                    if (me) word_store(&K[(in.off >> 3) * 32 + lane], in.off & 7, in.aux, S);
-                    if (uni) pc = npc;
-                    else if (me) mypc = npc;
-                    continue;
-                }
                 if (in.op >= GX_JEQ && in.op <= GX_JSET32) {
                     const bool is32 = in.op >= GX_JEQ32;
                     const uint32_t cop = is32 ? in.op - (GX_JEQ32 - GX_JEQ) : in.op;
@@ -494,7 +488,9 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                         *RD = v;
                     }
                     break;
-                /* GX_ST_STACK: the fast path above */
+                case GX_ST_STACK:
+                    if (me) word_store(&K[(in.off >> 3) * 32 + lane], in.off & 7, in.aux, S);
+                    break;
                 case GX_ST_MAP:
                     if (me) gstore(R[in.dst * 32 + lane] + in.off, in.aux, S);
                     break;
