@@ -430,17 +430,6 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     else if (me) mypc = npc;
                     continue;
                 }
-                if (in.op == GX_LDX_CTX || in.op == GX_LDX_STACK) {
-                    /* ctx / stack loads: lane-private shared-memory rows, one predicated write */
-                    const uint64_t *base = in.op == GX_LDX_CTX ? C : K;
-                    uint64_t v = base[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
-                    if (in.aux < 3) v &= (1ull << (8u << in.aux)) - 1;
-                    if (in.flags & GXF_SX) v = sext(v, 8u << in.aux);
-                    if (me) *RD = v;
-                    if (uni) pc = npc;
-                    else if (me) mypc = npc;
-                    continue;
-                }
                 if (in.op >= GX_JEQ && in.op <= GX_JSET32) {
                     const bool is32 = in.op >= GX_JEQ32;
                     const uint32_t cop = is32 ? in.op - (GX_JEQ32 - GX_JEQ) : in.op;
@@ -472,7 +461,22 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                 /* ALU64 / ALU32 / END / ldimm64: the fast path above (alu_eval) */
 
                 /* ---------------- memory */
-                /* GX_LDX_CTX / GX_LDX_STACK: the fast path above */
+                case GX_LDX_CTX:
+                    if (me) {
+                        uint64_t v = C[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
+                        if (in.aux < 3) v &= (1ull << (8u << in.aux)) - 1;
+                        if (in.flags & GXF_SX) v = sext(v, 8u << in.aux);
+                        *RD = v;
+                    }
+                    break;
+                case GX_LDX_STACK:
+                    if (me) {
+                        uint64_t v = K[(in.off >> 3) * 32 + lane] >> (8 * (in.off & 7));
+                        if (in.aux < 3) v &= (1ull << (8u << in.aux)) - 1;
+                        if (in.flags & GXF_SX) v = sext(v, 8u << in.aux);
+                        *RD = v;
+                    }
+                    break;
                 case GX_LDX_MAP:
                     if (me) {
                         uint64_t v = gload(R[in.src * 32 + lane] + in.off, in.aux, M[in.imm].coherent);
