@@ -430,33 +430,6 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     else if (me) mypc = npc;
                     continue;
                 }
-                if (in.op >= GX_JEQ && in.op <= GX_JSET32) {
-                    const bool is32 = in.op >= GX_JEQ32;
-                    const uint32_t cop = is32 ? in.op - (GX_JEQ32 - GX_JEQ) : in.op;
-                    uint64_t d = R[in.dst * 32 + lane], s = S;
-                    int64_t sd = (int64_t)d, ss = (int64_t)s;
-                    if (is32) {
-                        d = (uint32_t)d;
-                        s = (uint32_t)s;
-                        sd = (int32_t)d;
-                        ss = (int32_t)s;
-                    }
-                    switch (cop) {
-                    case GX_JEQ: taken = d == s; break;
-                    case GX_JNE: taken = d != s; break;
-                    case GX_JGT: taken = d > s; break;
-                    case GX_JGE: taken = d >= s; break;
-                    case GX_JLT: taken = d < s; break;
-                    case GX_JLE: taken = d <= s; break;
-                    case GX_JSGT: taken = sd > ss; break;
-                    case GX_JSGE: taken = sd >= ss; break;
-                    case GX_JSLT: taken = sd < ss; break;
-                    case GX_JSLE: taken = sd <= ss; break;
-                    default: taken = (d & s) != 0; break;
-                    }
-                    tgt = in.aux;
-                    goto do_branch;
-                }
                 switch (in.op) {
                 /* ALU64 / ALU32 / END / ldimm64: the fast path above (alu_eval) */
 
@@ -768,7 +741,33 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                     npc = 0xFFFFFFFFu;
                     break;
                 default:
-                    {
+                    if (in.op >= GX_JEQ && in.op <= GX_JSET32) {
+                        const bool is32 = in.op >= GX_JEQ32;
+                        const uint32_t cop = is32 ? in.op - (GX_JEQ32 - GX_JEQ) : in.op;
+                        uint64_t d = R[in.dst * 32 + lane], s = S;
+                        int64_t sd = (int64_t)d, ss = (int64_t)s;
+                        if (is32) {
+                            d = (uint32_t)d;
+                            s = (uint32_t)s;
+                            sd = (int32_t)d;
+                            ss = (int32_t)s;
+                        }
+                        switch (cop) {
+                        case GX_JEQ: taken = d == s; break;
+                        case GX_JNE: taken = d != s; break;
+                        case GX_JGT: taken = d > s; break;
+                        case GX_JGE: taken = d >= s; break;
+                        case GX_JLT: taken = d < s; break;
+                        case GX_JLE: taken = d <= s; break;
+                        case GX_JSGT: taken = sd > ss; break;
+                        case GX_JSGE: taken = sd >= ss; break;
+                        case GX_JSLT: taken = sd < ss; break;
+                        case GX_JSLE: taken = sd <= ss; break;
+                        default: taken = (d & s) != 0; break;
+                        }
+                        tgt = in.aux;
+                        goto do_branch;
+                    } else {
                         /* GX_OP_NOP: an instruction the verifier proved unreachable -- trap */
                         active &= ~exec;
                         if (me) c_herr++;
