@@ -23,6 +23,7 @@ from gpu_util import make_runtime
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("GX_FUZZ_CASES", "2000"))
+SEED0 = int(os.environ.get("GX_FUZZ_SEED0", "0"))    # extended campaigns: a fresh seed range
 
 
 def _oracle(texts, ev, seed):
@@ -80,7 +81,7 @@ def _run_cases(engine, seeds, threads):
 
 def test_fuzz_interp(gpu):
     os.environ.pop("GX_JIT_INGEST", None)
-    n = _run_cases("interp", list(range(N_CASES)), threads=8)
+    n = _run_cases("interp", list(range(SEED0, SEED0 + N_CASES)), threads=8)
     print(f"interp: {N_CASES} cases, {n} programs byte-equal to the oracle")
 
 
@@ -90,7 +91,7 @@ def test_fuzz_jit(gpu):
     ncpu = len(os.sched_getaffinity(0))
     k = max(50, N_CASES // 5)
     try:
-        n = _run_cases("jit", list(range(10000, 10000 + k)), threads=max(4, ncpu))
+        n = _run_cases("jit", list(range(SEED0 + 10000, SEED0 + 10000 + k)), threads=max(4, ncpu))
     finally:
         os.environ.pop("GX_JIT_UNIFORM_CHECK", None)
     print(f"jit (register ingest): {k} cases, {n} programs byte-equal to the oracle, no split at a GXF_UNIFORM branch")
@@ -101,7 +102,7 @@ def test_fuzz_jit_ring(gpu):
     try:
         ncpu = len(os.sched_getaffinity(0))
         k = max(50, N_CASES // 5)
-        n = _run_cases("jit", list(range(20000, 20000 + k)), threads=max(4, ncpu))
+        n = _run_cases("jit", list(range(SEED0 + 20000, SEED0 + 20000 + k)), threads=max(4, ncpu))
     finally:
         os.environ.pop("GX_JIT_INGEST", None)
     print(f"jit (TMA ring ingest): {k} cases, {n} programs byte-equal to the oracle")
