@@ -232,61 +232,6 @@ __device__ __forceinline__ uint64_t group_cmpxchg(unsigned mask, uint64_t addr, 
     }
 }
 
-/* a3 fast path: every register-to-register op (ALU64, ALU32, END, ldimm64) as one value -- the
- * same semantics as the interpreter's per-op cases -- so the loop stores it with one predicated
- * write instead of a guarded block per op */
-__device__ __forceinline__ uint64_t alu_eval(const GxInsn &in, uint64_t D, uint64_t S, const GxMapDesc *M) {
-    switch (in.op) {
-    case GX_ADD64: return D + S;
-    case GX_SUB64: return D - S;
-    case GX_MUL64: return D * S;
-    case GX_DIV64: return S ? D / S : 0;
-    case GX_SDIV64: {
-        const int64_t d = (int64_t)D, s = (int64_t)S;
-        return s == 0 ? 0 : (d == INT64_MIN && s == -1) ? (uint64_t)d : (uint64_t)(d / s);
-    }
-    case GX_MOD64: return S ? D % S : D;
-    case GX_SMOD64: {
-        const int64_t d = (int64_t)D, s = (int64_t)S;
-        return s == 0 ? (uint64_t)d : s == -1 ? 0 : (uint64_t)(d % s);
-    }
-    case GX_OR64: return D | S;
-    case GX_AND64: return D & S;
-    case GX_XOR64: return D ^ S;
-    case GX_LSH64: return D << (S & 63);
-    case GX_RSH64: return D >> (S & 63);
-    case GX_ARSH64: return (uint64_t)((int64_t)D >> (S & 63));
-    case GX_NEG64: return 0 - D;
-    case GX_MOV64: return S;
-    case GX_MOVSX64: return sext(S, in.aux);
-    case GX_ADD32: return (uint32_t)((uint32_t)D + (uint32_t)S);
-    case GX_SUB32: return (uint32_t)((uint32_t)D - (uint32_t)S);
-    case GX_MUL32: return (uint32_t)((uint32_t)D * (uint32_t)S);
-    case GX_DIV32: { const uint32_t s = (uint32_t)S; return s ? (uint32_t)D / s : 0; }
-    case GX_SDIV32: {
-        const int32_t d = (int32_t)D, s = (int32_t)S;
-        return (uint32_t)(s == 0 ? 0 : (d == INT32_MIN && s == -1) ? d : d / s);
-    }
-    case GX_MOD32: { const uint32_t s = (uint32_t)S; return s ? (uint32_t)D % s : (uint32_t)D; }
-    case GX_SMOD32: {
-        const int32_t d = (int32_t)D, s = (int32_t)S;
-        return (uint32_t)(s == 0 ? d : s == -1 ? 0 : d % s);
-    }
-    case GX_OR32: return (uint32_t)D | (uint32_t)S;
-    case GX_AND32: return (uint32_t)D & (uint32_t)S;
-    case GX_XOR32: return (uint32_t)D ^ (uint32_t)S;
-    case GX_LSH32: return (uint32_t)((uint32_t)D << (S & 31));
-    case GX_RSH32: return (uint32_t)D >> (S & 31);
-    case GX_ARSH32: return (uint32_t)((int32_t)D >> (S & 31));
-    case GX_NEG32: return (uint32_t)(0u - (uint32_t)D);
-    case GX_MOV32: return (uint32_t)S;
-    case GX_MOVSX32: return (uint32_t)sext(S, in.aux);
-    case GX_LE: return in.aux < 64 ? D & ((1ull << in.aux) - 1) : D;
-    case GX_BE: return bswap_w(D, in.aux);
-    default: /* GX_LDIMM */ return (in.flags & GXF_VAL_MAPV) ? M[in.aux].data + in.imm : in.imm;
-    }
-}
-
 struct Smem {
     GxInsn *prog;
     GxMapDesc *maps;
@@ -421,17 +366,66 @@ extern "C" __global__ void __launch_bounds__(GX_BLOCK) gx_exec_kernel(const GxLa
                 bool taken = false;
                 uint64_t *const RD = &R[in.dst * 32 + lane];
                 const uint64_t S = (in.flags & GXF_X) ? R[in.src * 32 + lane] : in.imm;
-                if (in.op >= GX_ADD64 && in.op <= GX_LDIMM) {
-                    /* register-to-register ops: one value, one predicated write (the register rows
-                     * of lanes outside `exec` are never written) */
-                    const uint64_t W = alu_eval(in, *RD, S, M);
-                    if (me) *RD = W;
-                    if (uni) pc = npc;
-                    else if (me) mypc = npc;
-                    continue;
-                }
                 switch (in.op) {
-                /* ALU64 / ALU32 / END / ldimm64: the fast path above (alu_eval) */
+                /* ---------------- ALU64 */
+                case GX_ADD64: if (me) *RD = *RD + S; break;
+                case GX_SUB64: if (me) *RD = *RD - S; break;
+                case GX_MUL64: if (me) *RD = *RD * S; break;
+                case GX_DIV64: if (me) *RD = S ? *RD / S : 0; break;
+                case GX_SDIV64:
+                    if (me) {
+                        int64_t d = (int64_t)*RD, s = (int64_t)S;
+                        *RD = s == 0 ? 0 : (d == INT64_MIN && s == -1) ? (uint64_t)d : (uint64_t)(d / s);
+                    }
+                    break;
+                case GX_MOD64: if (me) *RD = S ? *RD % S : *RD; break;
+                case GX_SMOD64:
+                    if (me) {
+                        int64_t d = (int64_t)*RD, s = (int64_t)S;
+                        *RD = s == 0 ? (uint64_t)d : s == -1 ? 0 : (uint64_t)(d % s);
+                    }
+                    break;
+                case GX_OR64: if (me) *RD = *RD | S; break;
+                case GX_AND64: if (me) *RD = *RD & S; break;
+                case GX_XOR64: if (me) *RD = *RD ^ S; break;
+                case GX_LSH64: if (me) *RD = *RD << (S & 63); break;
+                case GX_RSH64: if (me) *RD = *RD >> (S & 63); break;
+                case GX_ARSH64: if (me) *RD = (uint64_t)((int64_t)*RD >> (S & 63)); break;
+                case GX_NEG64: if (me) *RD = 0 - *RD; break;
+                case GX_MOV64: if (me) *RD = S; break;
+                case GX_MOVSX64: if (me) *RD = sext(S, in.aux); break;
+                /* ---------------- ALU32 (results zero-extended) */
+                case GX_ADD32: if (me) *RD = (uint32_t)((uint32_t)*RD + (uint32_t)S); break;
+                case GX_SUB32: if (me) *RD = (uint32_t)((uint32_t)*RD - (uint32_t)S); break;
+                case GX_MUL32: if (me) *RD = (uint32_t)((uint32_t)*RD * (uint32_t)S); break;
+                case GX_DIV32: if (me) { uint32_t s = (uint32_t)S; *RD = s ? (uint32_t)*RD / s : 0; } break;
+                case GX_SDIV32:
+                    if (me) {
+                        int32_t d = (int32_t)*RD, s = (int32_t)S;
+                        *RD = (uint32_t)(s == 0 ? 0 : (d == INT32_MIN && s == -1) ? d : d / s);
+                    }
+                    break;
+                case GX_MOD32: if (me) { uint32_t s = (uint32_t)S; *RD = s ? (uint32_t)*RD % s : (uint32_t)*RD; } break;
+                case GX_SMOD32:
+                    if (me) {
+                        int32_t d = (int32_t)*RD, s = (int32_t)S;
+                        *RD = (uint32_t)(s == 0 ? d : s == -1 ? 0 : d % s);
+                    }
+                    break;
+                case GX_OR32: if (me) *RD = (uint32_t)*RD | (uint32_t)S; break;
+                case GX_AND32: if (me) *RD = (uint32_t)*RD & (uint32_t)S; break;
+                case GX_XOR32: if (me) *RD = (uint32_t)*RD ^ (uint32_t)S; break;
+                case GX_LSH32: if (me) *RD = (uint32_t)((uint32_t)*RD << (S & 31)); break;
+                case GX_RSH32: if (me) *RD = (uint32_t)*RD >> (S & 31); break;
+                case GX_ARSH32: if (me) *RD = (uint32_t)((int32_t)*RD >> (S & 31)); break;
+                case GX_NEG32: if (me) *RD = (uint32_t)(0u - (uint32_t)*RD); break;
+                case GX_MOV32: if (me) *RD = (uint32_t)S; break;
+                case GX_MOVSX32: if (me) *RD = (uint32_t)sext(S, in.aux); break;
+                case GX_LE: if (me && in.aux < 64) *RD = *RD & ((1ull << in.aux) - 1); break;
+                case GX_BE: if (me) *RD = bswap_w(*RD, in.aux); break;
+                case GX_LDIMM: /* the pre-decoder dropped the second slot */
+                    if (me) *RD = (in.flags & GXF_VAL_MAPV) ? M[in.aux].data + in.imm : in.imm;
+                    break;
 
                 /* ---------------- memory */
                 case GX_LDX_CTX:
