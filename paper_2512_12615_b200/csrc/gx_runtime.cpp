@@ -595,14 +595,15 @@ void daemon_main(gx_rt *rt) {
 
 /* Batches of one runtime run in submission order whatever streams they are given: per-thread
  * shards are plain read-modify-writes keyed by the resident thread, and the privatised and
- * hash-cache flushes assume one batch at a time.  Same-stream order is free; on a stream change the
- * previous stream gets an event (recorded now: after everything already submitted to it, our last
- * batch included) that the new stream waits on -- nothing is recorded while the stream stays. */
+ * hash-cache flushes assume one batch at a time.  Every batch records an event right after its
+ * kernel on its own stream (while that stream surely exists -- a caller's stream may be gone by
+ * the next batch); a batch on a different stream first waits on it.  Same-stream order is free. */
 int order_after_last(gx_rt *rt, cudaStream_t stream) {
-    if (rt->order_valid && rt->order_stream != stream) {
-        CK(cudaEventRecord(rt->ev_order, rt->order_stream), "order event");
-        CK(cudaStreamWaitEvent(stream, rt->ev_order, 0), "order wait");
-    }
+    if (rt->order_valid && rt->order_stream != stream) CK(cudaStreamWaitEvent(stream, rt->ev_order, 0), "order wait");
+    return 0;
+}
+int order_record(gx_rt *rt, cudaStream_t stream) {
+    CK(cudaEventRecord(rt->ev_order, stream), "order event");
     rt->order_stream = stream;
     rt->order_valid = true;
     return 0;
@@ -685,8 +686,9 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
         rt->last_smem = cfg.smem;
     }
     rt->n_launches++;
-    if (rt->dmn.running) return daemon_publish(rt, stream);
-    return 0;
+    if (rt->dmn.running) /* the publish point belongs to this batch: the order event follows it */
+        if (int rc = daemon_publish(rt, stream)) return rc;
+    return order_record(rt, stream);
 }
 
 int sync(gx_rt *rt) {
