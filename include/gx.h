@@ -25,7 +25,8 @@
  *   - Maps are runtime-owned device memory, freed by gx_close.  Host map reads/writes are
  *     synchronous and ordered after all prior gx_run_batch calls on any stream of the runtime.
  *   - Batches of one gx_rt run one after another in submission order, even when they are given
- *     different streams (a stream change makes the new stream wait for the previous one).
+ *     different streams (every batch records an event on its stream; a batch on another stream
+ *     waits on it).  Under CUDA graph capture, give the runtime's batches the capturing stream.
  *   - One gx_rt per CUDA device.  A gx_rt is not thread-safe.
  *
  * Event record (the ctx every program sees in r1; read-only; 32 B, 32-B aligned):
