@@ -1275,7 +1275,10 @@ struct Gen {
 
 /* read at every compile (a compiled configuration keeps its shared-memory size in LaunchCfg) */
 int gx_jit_stages() {
-    int v = 2; /* profiles/r1_jit_variants.md §9: 2 stages of 32 KiB beat 3 (-5 % on C2), 4 and 6 */
+    /* 4 stages of 32 KiB (round 2, profiles/r2_stages.md): once the per-thread key cache took the
+     * per-thread RMWs off C2, the deeper ring wins (C2 5.27 -> 4.90 ms, C5 3.79 -> 3.49, C1 2^26
+     * 0.313 -> 0.303; C3 6.16 -> 6.28).  Round 1 measured 2 best (profiles/r1_jit_variants.md §9). */
+    int v = 4;
     if (const char *e = getenv("GX_JIT_STAGES")) v = atoi(e);
     return std::max(0, std::min(8, v));
 }
