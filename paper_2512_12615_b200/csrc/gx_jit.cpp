@@ -228,6 +228,7 @@ struct Gen {
     uint32_t hc_n_ = 0;
     bool ptc_ = false;   /* per-thread words through the register write-back cache (GX_JIT_PTCACHE=1; measured slower on C2) */
     int pkc_fd_ = -1;    /* the per-thread map held in the register key cache (GX_JIT_PTKC), or -1 */
+    int stages_ = 4;     /* event-ring depth of this module (gx_jit_stages_for) */
     std::vector<const uint16_t *> nin_; /* per program: registers narrow on entry to each slot (verifier) */
     const uint16_t *cur_nin_ = nullptr;
     /* at a block start: re-state the registers the verifier proved below 2^32 there, so that the
@@ -903,8 +904,9 @@ struct Gen {
          * the runtime picks per launch (gx_runtime.cpp launch_cfg) */
         /* only the instances `vmask` asks for (GX_JIT_V_*): a module per launch variant keeps NVRTC
          * time proportional to what runs -- each instance inlines every program U times */
-        const int S = gx_jit_stages();
-        if (vmask & (GX_JIT_V_RING | GX_JIT_V_RING_R)) body("gx_body_ring", S >= 2 ? S : 3, B, U, punroll, images);
+        const int S = gx_jit_stages_for(images, sizes);
+        stages_ = S >= 2 ? S : 3;
+        if (vmask & (GX_JIT_V_RING | GX_JIT_V_RING_R)) body("gx_body_ring", stages_, B, U, punroll, images);
         if (vmask & (GX_JIT_V_REG | GX_JIT_V_REG_R)) body("gx_body_reg", 0, B, U, punroll, images);
         const std::string lb = "__launch_bounds__(" + std::to_string(B) + (minb > 0 ? ", " + std::to_string(minb) : std::string()) + ")";
         const char *args = "(const uint4 *__restrict__ ev, uint64_t n, uint64_t *__restrict__ ret, unsigned long long *__restrict__ gstats)";
@@ -1039,7 +1041,7 @@ struct Gen {
             const bool stat = !getenv("GX_JIT_RING_CLAIM") || strcmp(getenv("GX_JIT_RING_CLAIM"), "dynamic") != 0;
             /* static assignment may give each warp P consecutive records of a (W x P)-record stage
              * (GX_JIT_RING_RPW): bigger bulk copies, the same number of streams per SM */
-            const int P = stat ? gx_jit_ring_rpw() : 1;
+            const int P = stat ? gx_jit_ring_rpw(stages_) : 1;
             const int CW = W * P; /* records per chunk (one stage) */
             o << "  extern __shared__ __align__(128) uint4 gx_ring[];\n"
                  "  __shared__ __align__(8) uint64_t gx_full[" << S << "];\n"
@@ -1283,12 +1285,23 @@ int gx_jit_stages() {
     return std::max(0, std::min(8, v));
 }
 
-int gx_jit_ring_rpw() {
+/* The ring depth of one launch configuration: the default (4) unless the launch is ONE program that
+ * probes a hash map -- its probe chain walks through L1, which a deeper ring's shared memory takes
+ * away (C3: 6.16 ms at 2 stages, 6.28-6.48 at 4; profiles/r2_stages.md).  GX_JIT_STAGES overrides. */
+int gx_jit_stages_for(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes) {
+    if (getenv("GX_JIT_STAGES")) return gx_jit_stages();
+    if (images.size() == 1)
+        for (uint32_t i = 0; i < sizes[0]; i++)
+            if (images[0][i].op == GX_CALL_LOOKUP_HASH) return 2;
+    return gx_jit_stages();
+}
+
+int gx_jit_ring_rpw(int stages) {
     int v = 1;
     if (const char *e = getenv("GX_JIT_RING_RPW")) v = atoi(e);
     if (getenv("GX_JIT_RING_CLAIM") && strcmp(getenv("GX_JIT_RING_CLAIM"), "dynamic") == 0) v = 1;
     v = std::max(1, std::min(4, v));
-    const int st = gx_jit_stages() >= 2 ? gx_jit_stages() : 3;
+    const int st = stages >= 2 ? stages : 3;
     while (v > 1 && st * v * (gx_jit_block() / 32) > 200) v--; /* the ring stays within 200 KiB of SMEM */
     return v;
 }

@@ -22,7 +22,7 @@ int gx_jit_compile(const std::string &src, std::vector<char> &cubin, std::string
 /* preferred threads per block of the generated kernel (1024; GX_JIT_BLOCK = 256 / 512 for experiments);
  * the runtime falls back to 256 only when a 1024-thread block cannot be resident */
 int gx_jit_block();
-/* depth of the shared-memory event ring (cp.async / TMA staging, a1): 2 by default
+/* depth of the shared-memory event ring (cp.async / TMA staging, a1): 4 by default
  * (GX_JIT_STAGES; < 2 = register loads, GX_JIT_UNROLL records per iteration).  Dynamic shared memory per block =
  * gx_jit_smem(block) bytes. */
 int gx_jit_stages();
@@ -31,8 +31,10 @@ int gx_jit_stages();
 int gx_jit_stage_mode();
 /* records per warp per ring stage with static record assignment (GX_JIT_RING_RPW, 1 by default; a
  * stage then holds (block/32) x rpw records, brought in by one bulk copy) */
-int gx_jit_ring_rpw();
-inline unsigned gx_jit_smem(int block) {
-    const int s = gx_jit_stages();
-    return (unsigned)(block / 32) * (unsigned)(s >= 2 ? s : 3) * (unsigned)gx_jit_ring_rpw() * 1024u; /* the ring stages */
+int gx_jit_ring_rpw(int stages);
+/* the ring depth of one launch configuration (default 4; 2 for a single program that probes a hash map) */
+int gx_jit_stages_for(const std::vector<const GxInsn *> &images, const std::vector<uint32_t> &sizes);
+inline unsigned gx_jit_smem(int block, int stages) {
+    const int s = stages >= 2 ? stages : 3;
+    return (unsigned)(block / 32) * (unsigned)s * (unsigned)gx_jit_ring_rpw(s) * 1024u; /* the ring stages */
 }

@@ -441,7 +441,7 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
         CUfunction fn = nullptr;
         if (d.moduleGetFunction(&fn, mod, gx_jit_kernel_name(k)) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "cuModuleGetFunction(%s) failed", gx_jit_kernel_name(k));
-        const unsigned smem = ring ? gx_jit_smem(B) : 0u;
+        const unsigned smem = ring ? gx_jit_smem(B, gx_jit_stages_for(images, sizes)) : 0u;
         if (ring && d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
             return set_err(rt, -EFAULT, "cuFuncSetAttribute(%u B dynamic shared) failed", smem);
         /* shared-memory carve-out preference (GX_JIT_CARVEOUT percent; -1 = the driver's choice): a
