@@ -196,3 +196,42 @@ def test_jit_variants_compile_offline(knobs, progs, monkeypatch):
         if rc == -38:
             pytest.skip(log)
         assert rc == 0, (name, knobs, log[-2000:])
+
+
+def _jit_source(name, **env):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        specs = programs.maps_of(name)
+        fds = {k: i for i, k in enumerate(specs)}
+        maps = {fds[k]: (s.type, s.key_size, s.value_size, s.max_entries) for k, s in specs.items()}
+        rc, src, log = gx.gx_jit_offline(programs.build(name, fds), maps)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    if rc == -38:
+        pytest.skip(log)
+    assert rc == 0, log[-2000:]
+    return src
+
+
+def test_codegen_decisions_offline():
+    """The round-2 code-generation decisions, visible in the generated source:
+    the per-thread key cache on P2's lane map (a value-start map, single program), 32-bit
+    arithmetic and the PTX shift on P4's binary search (verifier intervals), the ring depth --
+    4 stages, 2 for a single program that probes a hash map (P3) -- and none of it when disabled."""
+    p2 = _jit_source("P2", GX_JIT_VMASK="1")
+    assert "ptkc_switch<32u, 2u>" in p2 and "ptkc_flush(pkc" in p2
+    assert "gx_full[4]" in p2
+    assert "ptkc_switch" not in _jit_source("P2", GX_JIT_VMASK="1", GX_JIT_PTKC="0")
+    p3 = _jit_source("P3", GX_JIT_VMASK="1")
+    assert "gx_full[2]" in p3
+    p4 = _jit_source("P4", GX_JIT_VMASK="4")
+    assert "shr.b32" in p4 and "(uint64_t)(uint32_t)((uint32_t)r1 + (uint32_t)r9)" in p4
+    assert "r8 = (uint64_t)(uint32_t)r8;" in p4          # block-entry re-statement at the loop head
+    # the NULL test after an in-range ARRAY lookup is gone from the lookup itself
+    assert "0x7f0200000000ull + (uint64_t)k * 8u;" in p4
