@@ -468,11 +468,10 @@ int jit_prepare(gx_rt *rt, LaunchCfg &cfg, int k) {
         V.grid = (uint32_t)rt->nsm * (uint32_t)bps;
         break;
     }
-    /* ALU-heavy single programs (a bounded loop: > 64 instructions on the worst path) keep
-     * per-lane register ingest -- the ring's per-record bookkeeping costs more than it hides */
-    uint64_t worst = 0;
-    for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
-    cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
+    /* every large batch takes the ring (round 1 kept ALU-heavy single programs -- a bounded loop,
+     * > 64 instructions on the worst path -- on register ingest; after round 2's code-generation
+     * changes the ring wins for them too: C4 4.08 -> 4.01 ms, profiles/r2_stages.md) */
+    cfg.ring_ok = true;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     cfg.jit_ms += ms;
     gx_log(2, "JIT variant %d (%s ingest%s): %zu program(s), block %u, grid %u, %u B dynamic shared, %.1f ms", k,
@@ -619,11 +618,6 @@ int launch_cfg(gx_rt *rt, LaunchCfg &cfg, const void *d_events, uint64_t n, uint
     bool jit_ok = rt->engine == GX_ENGINE_JIT && !cfg.jit_failed;
     int vk = 0;
     if (jit_ok) {
-        if (!cfg.jv[0].tried && !cfg.jv[1].tried && !cfg.jv[2].tried && !cfg.jv[3].tried) {
-            uint64_t worst = 0; /* ring_ok before the first compile (jit_prepare sets it too) */
-            for (int q : cfg.progs) worst = std::max<uint64_t>(worst, rt->progs[q].vr.report.worst_insns);
-            cfg.ring_ok = !(cfg.progs.size() == 1 && worst > 64);
-        }
         vk = jit_variant(cfg, n, d_ret != nullptr);
         int rc = jit_prepare(rt, cfg, vk);
         if (rc == -ENOSYS) {
